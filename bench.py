@@ -1,0 +1,293 @@
+#!/usr/bin/env python
+"""Benchmark of the multistep BSDE hot path on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "cfg 2"): 1-D call under different borrowing /
+lending rates, P = 2^16 grid points on [-16, 16] (W-space), N = 256 time steps,
+L = 16 Gauss-Hermite nodes, K = Ky = Kz = 1..6.  One bench *step* is the backward
+sweep n = N-K .. 0 (Eq. 20) of all six K; updates = P * (N - K + 1) summed over K.
+Setup (grids, tap tables, the K closed-form initial layers and their splines) is
+outside the device-timed region; the e2e number includes it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): 1-D has no data-path exchange ("replicas only"), each rank
+solves the same workload on its own GPU; value = all ranks' updates / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid-point·time-step updates/s (fp64) + time-to-solution at fixed error vs host oracle"
+UNIT = "updates/s"
+KS = [1, 2, 3, 4, 5, 6]
+# Algorithmic FP64 flops per point-step of the fused kernel:
+#   per tap: 2 fields x 4 FMA (16) + driver diff-rates (8) + accumulations (6)   = 30
+#   per point: K*L taps, + 2 per tap at j = Ky (E[y]), Picard 30 x (8 + 2)       = 300
+#   spline of the new level: 2 fields x 21                                       = 42
+FLOP_TAP, FLOP_PICARD, FLOP_SPLINE = 30, 300, 42
+
+
+def flops_per_point_step(K, L=16):
+    return K * L * FLOP_TAP + L * 2 + FLOP_PICARD + FLOP_SPLINE
+
+
+def peak_fp64_tflops(sm_mhz=1965.0, nsm=148):
+    # B200: 64 FP64 FMA per clock per SM (B200_PROFILING.md / SURVEY A.4), 2 flops per FMA
+    return nsm * 64 * 2 * sm_mhz * 1e6 / 1e12
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            dist.init_process_group("nccl" if os.environ.get("BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+        return dist, dist.get_rank(), ws
+    return None, 0, 1
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.p is None:
+            return
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+            out, _ = self.p.communicate()
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        smax = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names[1:], r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        load = [float(r[0]) for r in self.rows if r[2] and float(r[2] or 0) > 200.0] or sm
+        load.sort()
+        return {"sm_mhz": load[len(load) // 2] if load else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def flush_l2(torch, buf):
+    buf.add_(1.0)        # 512 MiB write > 126 MB L2
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    from paper_1909_13560_b200 import Solver, workloads as W, query_workspace
+    dist, rank, world = _dist()
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    specs = {K: W.cfg2(K) for K in KS}
+    ws = {K: torch.empty(query_workspace(specs[K]), dtype=torch.uint8, device="cuda") for K in KS}
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    k6 = [0.0, 0]
+
+    def one_step(timed=True):
+        tot, upd, launches, y0 = 0.0, 0, 0, {}
+        for K in KS:
+            flush_l2(torch, flush)
+            s = Solver(specs[K], device=dev, stream=stream, workspace=ws[K])
+            n0 = s.kernel_launches
+            torch.cuda.synchronize()
+            r = s.solve()                              # device-timed sweep (CUDA events on `stream`)
+            tot += r.t_sweep_s
+            upd += r.updates
+            if K == 6 and timed:
+                k6[0] += r.t_sweep_s
+                k6[1] += r.updates // 65536
+            launches += s.kernel_launches - n0
+            y0[K] = (r.y0, r.z0[0])
+            s.close()
+        return tot, upd, launches, y0
+
+    for _ in range(args.warmup):
+        one_step(timed=False)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times, upds, launches = [], 0, 0
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            t, u, nl, y0 = one_step()
+            times.append(t)
+            upds += u
+            launches += nl
+    torch.cuda.synchronize()
+    elapsed = sum(times)
+    if dist:
+        tt = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    value = upds * world / elapsed
+    k6_time, k6_launches = k6
+
+    # ---- average launch duration of the dominant kernel (quad1d_fused, K = 6): the sweep is
+    # one kernel per step back to back, so the CUDA-event time of the K = 6 sweeps of the
+    # timed region divided by their launches (gaps included, so a lower bound on the rate)
+    launch_s = k6_time / k6_launches
+    fl = flops_per_point_step(6) * 65536
+    clocks = clk.summary()
+    peak = peak_fp64_tflops(1965.0)
+    achieved = fl / launch_s / 1e12
+    roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "quad1d_fused<DRV_DIFF> (K=6)", "flops_per_launch": fl, "launch_us": round(launch_s * 1e6, 3),
+            "peak_note": "FP64 pipe: 148 SM x 64 DFMA/clk x 2 x 1965 MHz (derived; DESIGN.md Roofline)"}
+
+    # ---- e2e: setup (host config -> device) + sweep + final layers device -> host, host clock
+    host = np.empty(65536, dtype=np.float64)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_upd, h2d, d2h = 0, 0, 0
+    for _ in range(args.steps):
+        for K in KS:
+            s = Solver(specs[K], device=dev, stream=stream, workspace=ws[K])
+            r = s.solve()
+            s.layer(0, out=host)
+            s.layer(1, out=host)
+            e2e_upd += r.updates
+            h2d += K * 16 * 56 + 2 * 16 * 8 + 1024          # tap table + GL rule + config/params
+            d2h += 2 * 65536 * 8 + 32                        # y, z of layer 0 + y0/z0
+            s.close()
+    torch.cuda.synchronize()
+    e2e_t = time.perf_counter() - t0
+    if dist:
+        tt = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+    e2e = {"value": e2e_upd * world / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+           "d2h_bytes_per_step": d2h // args.steps,
+           "note": "bsde_setup + bsde_solve + bsde_get_layer(y, z) per K, host wall clock"}
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "cfg2: 1-D differential-rates call, P=65536, N=256, L=16, K=1..6 (one step = six sweeps)",
+                      "global_batch": 65536 * world, "seq_len": 256, "parallelism": f"replicas{world}",
+                      "l2": "flushed (512 MiB write) before every sweep; sweep state ~6 MiB is L2-resident by design"},
+           "roofline": roof, "e2e": e2e, "gpu_launches": launches // max(args.steps, 1),
+           "clocks": clocks,
+           "accuracy": {str(K): {"y0": y0[K][0], "z0": y0[K][1]} for K in KS},
+           "reference_solution": list(W.reference_solution(specs[1])[:1]) + [W.reference_solution(specs[1])[1][0]]}
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0:
+        print(json.dumps(out))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _oracle_sample(max_seconds=12.0, steps_per_K=12):
+    """Time the oracle (as it stands) on a bounded sample of cfg 2: steps_per_K backward
+    steps of each K after its (untimed) setup."""
+    import oracle
+    from paper_1909_13560_b200 import workloads as W
+    nthreads = os.cpu_count() or 1
+    tot_t, tot_u = 0.0, 0
+    for K in KS:
+        o = oracle.Oracle(W.cfg2(K), nthreads=nthreads)
+        for _ in range(steps_per_K):
+            t0 = time.perf_counter()
+            o.step()
+            tot_t += time.perf_counter() - t0
+            tot_u += 65536
+            if tot_t > max_seconds:
+                break
+        o.close()
+    return tot_u / tot_t, tot_u, tot_t, nthreads
+
+
+def cpu_baseline(args):
+    v, u, t, nt = _oracle_sample()
+    return {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
+            "sample": f"cfg2, up to 12 backward steps per K=1..6 after untimed setup ({u} updates in {t:.2f} s)"}
+
+
+def run_reference(args):
+    dist, rank, world = _dist()
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    for _ in range(args.warmup):
+        _oracle_sample(max_seconds=3.0, steps_per_K=1)
+    vals, us, ts = [], 0, 0.0
+    for _ in range(args.steps):
+        v, u, t, nt = _oracle_sample(max_seconds=8.0, steps_per_K=4)
+        vals.append(v)
+        us += u
+        ts += t
+    value = us / ts
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ts / args.steps * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": "cfg2: 1-D differential-rates call, P=65536, N=256, L=16, K=1..6",
+                      "global_batch": 65536, "seq_len": 256, "parallelism": "host cores (OpenMP)"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "kind": "oracle", "cores": os.cpu_count(),
+                            "sample": "each step: 4 backward steps of each K=1..6 of cfg2 (setup untimed)"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

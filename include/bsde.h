@@ -1,0 +1,173 @@
+/*
+ * bsde.h -- C ABI of the B200-native multistep BSDE solver
+ * (Kapllani & Teng, "Multistep schemes for solving backward stochastic
+ *  differential equations on GPU", arXiv 1909.13560).
+ *
+ * One context solves one decoupled BSDE (Eq. 2)
+ *     -dy_t = f(t, y_t, z_t) dt - z_t dW_t,   y_T = g(W_T),
+ * backward in time with the fully discrete multistep scheme of Eq. 20
+ * on a uniform tensor grid of a truncated box
+ * (PAPER.md:334-337, 367-371).  Conditional expectations are Gauss-Hermite
+ * quadratures of spline-interpolated values (Eq. 21); z^n is
+ * explicit, y^n is solved by Picard iteration (p = 30 at
+ * PAPER.md:493).  All numerical work runs in hand-written sm_100a fp64 kernels.
+ *
+ * Conventions
+ *  - No C++ exception crosses this boundary; every call returns bsde_status.
+ *  - Host pointers are plain host memory; device pointers are CUDA device memory
+ *    of cfg.device.  The library never frees memory it did not allocate.
+ *  - Layout of a layer (bsde_get_layer): fp64, row-major over the d axes (the last
+ *    axis contiguous), npts[0]*...*npts[d-1] values; field 0 = y, field k = z_k.
+ *  - A context is used from one host thread.  Calls are stream-ordered on
+ *    cfg.stream (or a library-owned stream); bsde_step does not synchronise.
+ *  - Determinism: results are bitwise identical across runs for a fixed config.
+ */
+#ifndef BSDE_H
+#define BSDE_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BSDE_OK = 0,
+  BSDE_ERR_INVALID_ARGUMENT = 1, /* config outside the documented ranges; nothing allocated */
+  BSDE_ERR_RESOURCE_LIMIT = 2,   /* device memory / workspace / constant arena too small   */
+  BSDE_ERR_SINGULAR = 3,         /* reserved (the spline matrix is never singular)          */
+  BSDE_ERR_NUMERICAL_DOMAIN = 4, /* a non-finite y or z was produced (details: last_error)  */
+  BSDE_ERR_CUDA = 5,             /* a CUDA runtime error (message in last_error)            */
+  BSDE_ERR_COMM = 6,             /* reserved for the multi-GPU halo exchange                */
+  BSDE_ERR_STATE = 7             /* e.g. bsde_step at n == 0                                */
+} bsde_status;
+
+/* Driver f(t, y, z) in the paper's sign convention -dy = f dt - z dW (Eq. 2).
+ * Parameters p = driver_params. */
+typedef enum {
+  BSDE_DRV_ZERO = 0,       /* f = 0                                                        */
+  BSDE_DRV_AFFINE = 1,     /* f = p0 y + sum_k p[1+k] z_k + p4 : Black-Scholes Eq. 29/30,
+                              Ex. 4 Eq. 34 (p = 1, -1/2, -1/2), exchange Eq. 36             */
+  BSDE_DRV_EX1 = 2,        /* f = -y^3 + 5/2 y^2 - 3/2 y          (Eq. 22)   */
+  BSDE_DRV_EX2 = 3,        /* f = 1/2 (e^{t^2} - 4 t y - 3 e^{t^2 - y e^{-t^2}} + z^2 e^{-t^2})
+                                                                  (Eq. 24)   */
+  BSDE_DRV_DIFF_RATES = 4  /* f = -(r y + sum_k th_k z_k) + (R - r) max(sum_k pi_k z_k - y, 0)
+                              p0 = r (lending), p1 = R (borrowing), p2..4 = th_k, p5..7 = pi_k
+                              (wealth equation Eq. 28 with a borrowing rate; R21) */
+} bsde_driver_id;
+
+/* Terminal condition g(w), w = W_T, in W-space (R20); z_T = grad g (Eq. 4). */
+typedef enum {
+  BSDE_TERM_CONST = 0,        /* g = p0                                                    */
+  BSDE_TERM_POLY = 1,         /* g = prod_a (p[4a] + p[4a+1] w_a + p[4a+2] w_a^2 + p[4a+3] w_a^3) */
+  BSDE_TERM_LOGISTIC = 2,     /* g = 1/(1 + exp(-(sum_a w_a/sqrt(d) + T)))  (Eq. 22 for d=1)*/
+  BSDE_TERM_EX2 = 3,          /* g = ln(sin w + 3) e^{T^2}                      (Eq. 24)   */
+  BSDE_TERM_CALL_W = 4,       /* S = p0 exp((p2 - p3^2/2) T + p3 w), g = (S - p1)^+ (Eq. 30, 32) */
+  BSDE_TERM_SIN_SUM = 5,      /* g = sin(sum_a w_a + T)                         (Eq. 34)   */
+  BSDE_TERM_EXCHANGE_W = 6,   /* S_k = p[k] exp((p[2+k] - s_k^2/2) T + (A w)_k), s = (p4, p5),
+                                 rho = p6, A = [[s1, 0], [rho s2, s2 sqrt(1-rho^2)]],
+                                 g = (S_1 - S_2)^+                               (Eq. 36)   */
+  BSDE_TERM_GEO_BASKET_W = 7  /* S_k = p[k] exp((p4 - s_k^2/2) T + s_k w_k), s_k = p[5+k],
+                                 G = (prod_k S_k)^{1/d}, g = (G - p3)^+     (BASELINE cfg 5) */
+} bsde_terminal_id;
+
+typedef struct {
+  uint32_t struct_size;      /* caller sets sizeof(bsde_config) (ABI versioning)          */
+  int32_t  d;                /* Brownian dimension, 1..3                                  */
+  int32_t  m;                /* solution dimension, must be 1                             */
+  double   t0, T;            /* time interval; dt = (T - t0)/N, t_n = t0 + n dt */
+  int32_t  N;                /* time steps, N >= max(Ky, Kz)                               */
+  int32_t  Ky, Kz;           /* multistep levels, 1..6 (Tables 1-2)     */
+  int32_t  L;                /* Gauss-Hermite nodes per axis, 1..64 (Eq. 21)              */
+  int64_t  npts[3];          /* grid points per axis incl. both ends, >= 4; 0 -> balance rule
+                                M = 2 ceil(X/dx), dx = dt^{(q+1)/r}, q = min(Ky+1, Kz, 3),
+                                npts = M + 1 (R3)              */
+  double   xlo[3], xhi[3];   /* truncated box in W-space                    */
+  int32_t  r;                /* balance-rule interpolation order (0 -> 4)                  */
+  int32_t  driver_id;   double driver_params[12];
+  int32_t  terminal_id; double terminal_params[12];
+  int32_t  picard_max;       /* Picard iterations (30)                       */
+  double   picard_tol;       /* <= 0: exactly picard_max iterations (R8)          */
+  int32_t  bootstrap;        /* 0: closed-form initial layers; 1: one-step scheme (K = 1) with
+                                bootstrap_substeps sub-steps per interval */
+  int32_t  bootstrap_substeps;
+  int32_t  smoothing;        /* 1: cell-average the kinked payoff at the terminal layer
+                                (R11)                          */
+  int32_t  nranks, rank;     /* slab partition along axis 0 (d >= 2); 1/0 for one GPU       */
+  const void* nccl_unique_id;/* reserved for the multi-GPU path; NULL                       */
+  void*    stream;           /* cudaStream_t to run on; NULL -> library-owned stream        */
+  int32_t  device;           /* CUDA device ordinal                                         */
+  int32_t  kernel_variant;   /* 0: auto (fastest available), 1: generic reference kernels   */
+} bsde_config;
+
+typedef struct {
+  double  y0, z0[3];         /* solution at t0 and x = 0 (grid value if x = 0 is a grid point,
+                                else the spline of layer 0 at 0; R4)             */
+  double  t_setup_s;         /* bsde_setup wall time (host clock)                          */
+  double  t_sweep_s;         /* backward sweep n = N-K..0 (CUDA events on the stream)      */
+  double  t_total_s;         /* setup + sweep + result read-back                           */
+  int64_t updates;           /* npts_total * (number of sweep steps performed)              */
+  int32_t picard_max_used;
+} bsde_result;
+
+typedef struct bsde_ctx bsde_ctx;
+
+/* Device bytes the context needs (values, coefficient ring of K levels, scratch).
+ * Errors: INVALID_ARGUMENT for an invalid config.                                      */
+bsde_status bsde_query_workspace(const bsde_config* cfg, size_t* bytes);
+
+/* Validate, build grids / Gauss-Hermite rule / weight rows / tap tables, allocate (or
+ * adopt the caller's d_workspace of `bytes` >= bsde_query_workspace; caller-owned, must
+ * outlive the context), compute the K initial layers and their splines.  On return the
+ * newest level is N-K+1.  On failure nothing stays allocated and *out = NULL.          */
+bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, bsde_ctx** out);
+
+/* One backward step n+1 -> n (Eq. 20): fused quadrature/z/Picard kernel, then the
+ * spline build of the new level into the ring slot of level n+K.  Asynchronous.
+ * Errors: STATE at n == 0; CUDA on a launch failure.                                  */
+bsde_status bsde_step(bsde_ctx* ctx);
+
+/* Remaining steps to n = 0, then the evaluation point; synchronises the stream and
+ * checks the device non-finite flag (NUMERICAL_DOMAIN).  res may be NULL.             */
+bsde_status bsde_solve(bsde_ctx* ctx, bsde_result* res);
+
+/* index n of the newest level                                                         */
+bsde_status bsde_level(const bsde_ctx* ctx, int32_t* n_out);
+
+/* Copy field (0 = y, k = z_k) of the newest level to host memory (count = total points). */
+bsde_status bsde_get_layer(const bsde_ctx* ctx, int32_t field, double* host_dst, int64_t count);
+
+/* Picard iteration count per point of the newest level (0 for initial layers).         */
+bsde_status bsde_get_picard_counts(const bsde_ctx* ctx, int32_t* host_dst, int64_t count);
+
+/* Grid actually used: points per axis and dx (axes >= d report 1 and 0).              */
+bsde_status bsde_query_grid(const bsde_ctx* ctx, int64_t npts[3], double dx[3]);
+
+/* Tap table of level j (1..K) on `axis`: for each node l < L the cell offset q, the 4
+ * cubic B-spline basis weights at theta, the Gauss-Hermite weight w/sqrt(pi) and the
+ * Brownian increment sqrt(2 j dt) a_l (Eq. 21).  Host arrays of L,
+ * 4L, L, L entries.                                                                   */
+bsde_status bsde_query_taps(const bsde_ctx* ctx, int32_t level, int32_t axis, int32_t* q,
+                            double* basis4, double* w, double* dw);
+
+/* Values of all fields of the newest level's spline at the host point x[d] (clamped to
+ * the box).  out[1+d] host.                                                           */
+bsde_status bsde_eval(bsde_ctx* ctx, const double* x, double* out);
+
+/* Device pointer of field `field` of the newest level (npts contiguous doubles, valid
+ * until the next bsde_step).                                                          */
+bsde_status bsde_layer_device_ptr(const bsde_ctx* ctx, int32_t field, const double** dptr);
+
+/* Number of kernels launched by this context so far.                                  */
+bsde_status bsde_kernel_launches(const bsde_ctx* ctx, int64_t* count);
+
+/* Message of the last failing call on ctx (owned by ctx; valid until the next call), or
+ * of the last failing bsde_setup/bsde_query_workspace when ctx == NULL (thread-local). */
+const char* bsde_last_error(const bsde_ctx* ctx);
+
+/* Release library-owned memory and streams; never the caller's workspace.              */
+void bsde_destroy(bsde_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSDE_H */

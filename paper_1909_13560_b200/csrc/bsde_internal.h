@@ -1,0 +1,92 @@
+// bsde_internal.h -- data structures shared by the host runtime (host.cu) and the
+// kernels (kernels.cu) of the B200 multistep BSDE solver.  Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bsde {
+
+constexpr int kMaxD = 3;
+constexpr int kMaxK = 6;
+constexpr int kMaxL = 64;
+constexpr int kPcrLevels = 5;       // PCR levels of the constant (1,4,1) system; coupling
+                                    // after 5 levels: a5/b5 = 5.0e-19
+constexpr int kPcrHalo = (1 << kPcrLevels) - 1;   // 31
+constexpr int kSmoothGL = 16;       // Gauss-Legendre nodes per axis for d >= 2 smoothing
+
+// One entry of a per-level, per-axis tap table (translation-invariant stencil,
+// PAPER.md:391-392): node l of level j shifts every grid point by
+// s = sqrt(2 j dt) a_l = (q + theta) dx.
+struct AxisTap {
+  int32_t q;          // integer cell offset floor(s/dx)
+  int32_t pad;
+  double B[4];        // cubic B-spline basis at theta: (1-t)^3/6, (3t^3-6t^2+4)/6, ...
+  double w;           // omega_l / sqrt(pi)
+  double s;           // Brownian increment sqrt(2 j dt) a_l
+};
+
+// Per-(level, node) record of the fused 1-D kernel: the stencil (q, B) of AxisTap and the
+// scheme weights folded in on the host: wcz = w ([j==1] - gz_j), wgz = w gz_j s,
+// wgy = w gy_j, wy = w [j == Ky] (Eq. 20 with Eq. 21).
+struct Tap1D {
+  int32_t q;
+  int32_t pad;
+  double B[4];
+  double wcz, wgz, wgy, wy;
+};
+
+struct Problem {
+  int32_t d;
+  int32_t driver_id, terminal_id;
+  int32_t smoothing;
+  double dp[12];
+  double tp[12];
+  double T, t0, dt;
+  int32_t N;
+};
+
+struct Grid {
+  int32_t d;
+  int64_t P[kMaxD];        // points per axis
+  double xlo[kMaxD], xhi[kMaxD], dx[kMaxD];
+  int64_t vstride[kMaxD];  // value layout strides (row-major, last axis contiguous)
+  int64_t cstride[kMaxD];  // coefficient layout strides (extent P+3 per axis, storage k+1)
+  int64_t npts;            // product of P
+  int64_t cfield;          // elements of one coefficient field (incl. padding)
+};
+
+// Per-step parameters of the fused quadrature / z / Picard kernel (Eq. 20).
+struct StepArgs {
+  const double* ring;      // coefficient ring base
+  int64_t slot_elems;      // elements per ring slot (F * cfield)
+  int32_t slot[kMaxK];     // ring slot of level n+j, j = 1..K (index j-1); slot[0] receives
+                           // the spline of values_in (built at the start of the step)
+  double t_level[kMaxK];   // t_{n+j}
+  double czj[kMaxK];       // coefficient of E[z^{n+j}] in z^n*gz0: [j==1] - gz_j
+  double gzj[kMaxK];       // gz_j (0 for j > Kz): coefficient of E[f dW]
+  double gyj[kMaxK];       // gy_j (0 for j > Ky): coefficient of E[f]
+  int32_t K, Ky, Kz, L;
+  int32_t ring_slots;      // RS: level m lives in ring slot m % RS
+  int32_t tap_off;         // byte offset of the AxisTap table (K x d x L) in the constant arena
+  int32_t tap1_off;        // byte offset of the Tap1D table (K x L, d = 1) in the constant arena
+  double gz0, ky_dt_gy0, ky_dt, tn;
+  int32_t picard_max;
+  double picard_tol;
+  const double* values_in; // level n+1 values (input of the level-1 spline)
+  double* values;          // out: F * npts (level n)
+  int32_t* picard;         // out: npts
+  unsigned long long* bad; // min index of a non-finite output
+  unsigned long long* phase_ns;  // optional (debug): per-CTA %globaltimer stamps of the fused kernel
+};
+
+// Geometry of the fused 1-D step kernel (kernels.cu, quad1d_fused).
+struct Fused1D {
+  int variant;               // index into the instantiated (R, C, threads, unroll) table
+  int TP;                    // points per CTA
+  int WMAX;                  // doubles per field buffer in shared memory
+  int WP;                    // doubles per PCR scratch array
+  double alpha[kPcrLevels];  // PCR elimination ratios
+  double inv_b;              // 1 / b after the last PCR level
+};
+
+}  // namespace bsde

@@ -1,0 +1,601 @@
+// fused1d.cuh -- the d = 1 fused step kernel (included by kernels.cu, which owns the
+// constant tap arena).  This is the hot kernel of BASELINE cfg 2.
+//
+// One CTA per tile of TP consecutive points (TP = 32 * NT/(32 C) * R, about P / #SMs).
+// Per backward step t_{n+1} -> t_n (Eq. 20):
+//  (1) the not-a-knot spline of the level-(n+1) values on the CTA's own tile is solved by
+//      constant-coefficient PCR in shared memory (tile + 31-point decay halo, DESIGN.md
+//      "spline"; the values arrive by cp.async.bulk) and written to the ring slot of n+1.
+//  (2) levels K..1: windows of B-spline coefficients c[lo+q_min-1 .. hi+q_max+2] are
+//      streamed from the ring by cp.async.bulk (one elected thread, mbarrier completion),
+//      double-buffered against the computation of the previous level.
+//  (3) each warp owns one chunk of Gauss-Hermite nodes (lambda = chunk, chunk + C, ...) and
+//      each lane R consecutive points (odd R: conflict-free 8-byte smem access); every
+//      lane of a warp reads the same tap (q, B, weights) from constant memory
+//      (the translation-invariant stencil of PAPER.md:391-392).
+//  (4) the C partial sums per point are reduced in a fixed order in smem and the
+//      epilogue (z explicit, y by Picard, Eq. 20) writes level n.
+// All CTAs of a launch are co-resident (cooperative launch) and synchronise with their
+// neighbours only, through per-CTA progress flags; bsde_solve runs all remaining steps in
+// one launch (persistent), bsde_step one step per launch.  Levels are processed K..1 so the
+// wait for the neighbours' level-(n+1) coefficients is hidden behind levels K..2.
+#pragma once
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(smem_addr(bar)), "r"(phase) : "memory");
+  } while (!done);
+}
+// order generic-proxy accesses (smem and global) before subsequent async-proxy (bulk copy) ones
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PHASE_STAMP(i)                                                                          \
+  do {                                                                                          \
+    if (s.phase_ns != nullptr && threadIdx.x == 0)                                              \
+      s.phase_ns[((size_t)it_stamp * gridDim.x + blockIdx.x) * 16 + (i)] = gtimer();              \
+  } while (0)
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// window of level j: storage indices [clo, clo + nwin) of the coefficient array
+__device__ __forceinline__ void level_window(int qmin, int qmax, int64_t lo, int64_t hi, int64_t P,
+                                             int64_t& clo, int& nwin) {
+  const int64_t a = lo + qmin, b = hi - 1 + qmax;                 // nodes ascending
+  clo = max((int64_t)0, min(a, P - 1));
+  const int64_t chi = max((int64_t)0, min(b, P - 1));
+  nwin = (int)(chi - clo + 4);
+}
+
+// Launch parameters of the fused kernel.  All CTAs of a launch are co-resident
+// (cooperative launch); CTAs synchronise only with the neighbours they exchange data
+// with, through per-CTA progress flags:
+//   ring_flag[b] = it + 1  once CTA b wrote its tile of the level-(n+1) coefficients (step it)
+//   done_flag[b] = it + 1  once CTA b wrote its tile of the level-n values (end of step it)
+struct Persist1D {
+  int n0, nsteps, ring_mode, cur;
+  double t0, dt;
+  double* vbuf[2];
+  unsigned* ring_flag;
+  unsigned* done_flag;
+  int D[kMaxK + 1];  // D[j]: CTA distance of level j's window (j >= 1); D[0]: values halo of phase A
+  int DK;            // max of D
+};
+
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// warp 0 waits until flag[b'] >= target for all CTAs b' within distance D of b (one lane per
+// flag, so a satisfied wait costs one acquire round trip)
+__device__ __forceinline__ void wait_neighbours_warp(const unsigned* flag, int b, int D, int nb, unsigned target) {
+  const int lane = threadIdx.x & 31;
+  const int a = max(0, b - D), e = min(nb - 1, b + D);
+  for (int q0 = a; q0 <= e; q0 += 32) {
+    const int q = q0 + lane;
+    bool ok = q > e;
+    while (!__all_sync(0xffffffffu, ok)) {
+      if (!ok) ok = ld_acquire(flag + q) >= target;
+      if (!__all_sync(0xffffffffu, ok)) __nanosleep(32);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <int DRV, int R, int C, int NT, int MB>
+__global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Problem pb, Fused1D fz, Persist1D pp) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);        // 0/1: level buffers, 2: values tile
+  const int WM = fz.WMAX, WP = fz.WP;
+  double* const buf0 = reinterpret_cast<double*>(smem_raw + 128);
+  double* const buf1 = buf0 + 2 * WM;
+  double* const Fs = buf1 + 2 * WM;                 // 2 x (WP + 4): values of the tile + PCR halo
+  double* const T0 = Fs + 2 * (WP + 4);             // 2 x WP
+  double* const T1 = T0 + 2 * WP;                   // 2 x WP
+  constexpr int NWPG = NT / (32 * C);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int chunk = warp / NWPG, pg = warp % NWPG;
+  const int P = (int)g.P[0];
+  const int TP = fz.TP;
+  const int bid = blockIdx.x, nb = gridDim.x;
+  const int lo = bid * TP;
+  const int hi = min(lo + TP, P);
+  const int li0 = (pg * 32 + lane) * R;              // first local point of this lane
+  const bool active = lo + li0 < hi;
+  const int L = s.L, K = s.K;
+  const int H = kPcrHalo;
+  const int tile_last = lo + NWPG * 32 * R - 1;      // last point of the full tile (incl. idle lanes)
+  const Tap1D* const tap0 = taps1d(s.tap1_off);
+  const double inv_gz0 = 1.0 / s.gz0;
+  // coefficients this CTA owns (c indices k = storage - 1) and the PCR extent around them
+  const int k0 = lo == 0 ? -1 : lo, k1 = hi == P ? P + 1 : hi;
+  const int base = k0 - 4 - H;
+  const int Wa = (k1 - k0) + 8 + 2 * H;
+  const bool fastA = base >= 2 && base + Wa - 1 <= P - 3;        // no end rows in the PCR window
+
+  int it_stamp = 0;
+  PHASE_STAMP(0);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    fence_mbar_init();
+  }
+  grid_dep_wait();            // previous kernel in the stream has completed
+  __syncthreads();
+  PHASE_STAMP(1);
+  uint32_t ph[3] = {0, 0, 0};
+
+  for (int it = 0; it < pp.nsteps; ++it) {
+    it_stamp = it;
+    // ---------------- step parameters
+    int slot[kMaxK];
+    double tlev[kMaxK];
+    double tn;
+    const double* vin;
+    double* vout;
+    if (pp.ring_mode) {
+      const int n = pp.n0 - it;
+#pragma unroll
+      for (int j = 1; j <= kMaxK; ++j) {
+        slot[j - 1] = (n + j) % s.ring_slots;
+        tlev[j - 1] = pp.t0 + (n + j) * pp.dt;
+      }
+      tn = pp.t0 + n * pp.dt;
+      vin = pp.vbuf[(pp.cur + it) & 1];
+      vout = pp.vbuf[(pp.cur + it + 1) & 1];
+    } else {
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j) { slot[j] = s.slot[j]; tlev[j] = s.t_level[j]; }
+      tn = s.tn;
+      vin = s.values_in;
+      vout = s.values;
+    }
+    // bulk-load level j's window into buffer b (called by warp 0).  Level 1 (slot n+1) is
+    // written in phase A of this step by the CTAs within D[1]: wait for their ring flags.
+    auto issue_level = [&](int j, int b) {
+      if (j == 1) wait_neighbours_warp(pp.ring_flag, bid, pp.D[1], nb, (unsigned)it + 1);
+      if (lane != 0) return;
+      const Tap1D* tj = tap0 + (j - 1) * L;
+      int64_t clo;
+      int nwin;
+      level_window(tj[0].q, tj[L - 1].q, lo, hi, P, clo, nwin);
+      const int64_t s0 = clo & ~(int64_t)1;
+      const int64_t s1 = (clo + nwin + 1) & ~(int64_t)1;
+      const uint32_t bytes = (uint32_t)((s1 - s0) * sizeof(double));
+      const double* Cf = s.ring + (int64_t)slot[j - 1] * s.slot_elems;
+      double* dst = b ? buf1 : buf0;
+      mbar_expect_tx(&bar[b], 2 * bytes);
+      bulk_g2s(dst, Cf + s0, bytes, &bar[b]);
+      bulk_g2s(dst + WM, Cf + g.cfield + s0, bytes, &bar[b]);
+    };
+    // Levels are processed K, K-1, ..., 2, then 1: levels >= 2 only need ring slots written
+    // in earlier steps, so they run before this step's spline (phase A) and hide the wait
+    // for the neighbours' level-(n+1) values; level j uses buffer (K - j) & 1.
+    // Slots of levels n+2..n+K were written in phase A of earlier steps by CTAs up to DK
+    // away: their ring flags of step it-1 cover all of them.
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 0) {
+      if (it > 0 && K >= 2) wait_neighbours_warp(pp.ring_flag, bid, pp.DK, nb, (unsigned)it);
+      if (K >= 2) issue_level(K, 0);
+      if (K >= 3) issue_level(K - 1, 1);
+    }
+    __syncthreads();
+    PHASE_STAMP(2);
+
+    Driver<DRV, 1> drv(pb.dp);
+    double Az[R], Af[R], Ay[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) { Az[r] = 0.0; Af[r] = 0.0; Ay[r] = 0.0; }
+    // one level of taps on the window in buffer b
+    auto level = [&](int j, int b) {
+      const Tap1D* tj = tap0 + (j - 1) * L;
+      int wbase, nwin;
+      {
+        int64_t clo;
+        level_window(tj[0].q, tj[L - 1].q, lo, hi, P, clo, nwin);
+        wbase = (int)(clo & ~(int64_t)1);
+        nwin += (int)clo - wbase;
+      }
+      mbar_wait(&bar[b], ph[b]);
+      ph[b] ^= 1u;
+      const double* const wy = b ? buf1 : buf0;
+      const double* const wz = wy + WM;
+      drv.at(tlev[j - 1]);
+      const bool yj = (j == s.Ky);
+      const int rel0 = lo - wbase + li0;               // lane's first cell relative to the window (q = 0)
+      // taps whose cells stay inside [0, P-2] for the whole tile (q ascending in lambda)
+      const int qlo = -lo, qhi = P - 2 - tile_last;
+      for (int l = chunk; l < L; l += C) {
+        const Tap1D& t = tj[l];
+        const int q = t.q;
+        double yh[R], zh[R];
+        if (q >= qlo && q <= qhi) {
+          const double* py = wy + (rel0 + q);
+          const double* pz = wz + (rel0 + q);
+          double c[R + 3];
+#pragma unroll
+          for (int k = 0; k < R + 3; ++k) c[k] = py[k];
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            yh[r] = fma(t.B[0], c[r], fma(t.B[1], c[r + 1], fma(t.B[2], c[r + 2], t.B[3] * c[r + 3])));
+#pragma unroll
+          for (int k = 0; k < R + 3; ++k) c[k] = pz[k];
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            zh[r] = fma(t.B[0], c[r], fma(t.B[1], c[r + 1], fma(t.B[2], c[r + 2], t.B[3] * c[r + 3])));
+        } else {
+          if (!active) continue;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            double Bc[4];
+            const int cell = lo + li0 + r + q;
+            int cc = (int)clamp_cell(cell, P, t.B, Bc) - wbase;
+            cc = cc < 0 ? 0 : (cc > nwin - 4 ? nwin - 4 : cc);      // lanes past the grid end
+            yh[r] = fma(Bc[0], wy[cc], fma(Bc[1], wy[cc + 1], fma(Bc[2], wy[cc + 2], Bc[3] * wy[cc + 3])));
+            zh[r] = fma(Bc[0], wz[cc], fma(Bc[1], wz[cc + 1], fma(Bc[2], wz[cc + 2], Bc[3] * wz[cc + 3])));
+          }
+        }
+        const double wcz = t.wcz, wgz = t.wgz, wgy = t.wgy;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double f = drv(yh[r], &zh[r]);
+          Az[r] = fma(wcz, zh[r], fma(wgz, f, Az[r]));
+          Af[r] = fma(wgy, f, Af[r]);
+        }
+        if (yj) {
+          const double wy_ = t.wy;
+#pragma unroll
+          for (int r = 0; r < R; ++r) Ay[r] = fma(wy_, yh[r], Ay[r]);
+        }
+      }
+    };
+
+    // ---------------- (2)+(3) levels K, ..., 2
+    for (int j = K; j >= 2; --j) {
+      const int b = (K - j) & 1;
+      level(j, b);
+      if (j <= 6) PHASE_STAMP(7 + j);
+      if (j - 2 >= 2) {                     // refill this buffer with level j-2
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (warp == 0) issue_level(j - 2, b);
+      }
+    }
+
+    // ---------------- (1) this CTA's tile of the level-(n+1) spline -> ring slot of level n+1
+    // the CTAs within D[0] finished step it-1 (their level-(n+1) values exist, and they have
+    // read the value buffer this step overwrites); the CTAs within DK finished step it-3
+    // (nobody still reads the old content of ring slot n+1, level n+1+RS, RS = K+2)
+    fence_proxy_async();
+    if (warp == 0) {
+      if (it > 0) wait_neighbours_warp(pp.done_flag, bid, pp.D[0], nb, (unsigned)it);
+      if (it > 2) wait_neighbours_warp(pp.done_flag, bid, pp.DK, nb, (unsigned)(it - 2));
+    }
+    __syncthreads();
+    const int off0 = (base - 1) & 1;
+    const int off1 = (int)(((int64_t)P + base - 1) & 1);
+    if (tid == 0 && fastA) {
+      const uint32_t n0b = (uint32_t)((((Wa + 2 + off0) + 1) & ~1) * sizeof(double));
+      const uint32_t n1b = (uint32_t)((((Wa + 2 + off1) + 1) & ~1) * sizeof(double));
+      mbar_expect_tx(&bar[2], n0b + n1b);
+      bulk_g2s(Fs, vin + (base - 1 - off0), n0b, &bar[2]);
+      bulk_g2s(Fs + (WP + 4), vin + ((int64_t)P + base - 1 - off1), n1b, &bar[2]);
+    }
+    {
+      const double* F0 = vin;
+      const double* F1 = vin + P;
+      const double m1_0 = __ldcg(F0) - 2.0 * __ldcg(F0 + 1) + __ldcg(F0 + 2);
+      const double mP2_0 = __ldcg(F0 + P - 3) - 2.0 * __ldcg(F0 + P - 2) + __ldcg(F0 + P - 1);
+      const double m1_1 = __ldcg(F1) - 2.0 * __ldcg(F1 + 1) + __ldcg(F1 + 2);
+      const double mP2_1 = __ldcg(F1 + P - 3) - 2.0 * __ldcg(F1 + P - 2) + __ldcg(F1 + P - 1);
+      const double* Fw0 = Fs + off0 + 1 - base;      // Fw0[k] = F0[k] for k in [base-1, base+Wa]
+      const double* Fw1 = Fs + (WP + 4) + off1 + 1 - base;
+      if (fastA) {
+        mbar_wait(&bar[2], ph[2]);
+        ph[2] ^= 1u;
+        for (int p = tid; p < Wa; p += NT) {
+          const int k = base + p;
+          double r0 = 6.0 * (Fw0[k - 1] - 2.0 * Fw0[k] + Fw0[k + 1]);
+          double r1 = 6.0 * (Fw1[k - 1] - 2.0 * Fw1[k] + Fw1[k + 1]);
+          if (k == 2) { r0 -= m1_0; r1 -= m1_1; }
+          if (k == P - 3) { r0 -= mP2_0; r1 -= mP2_1; }
+          T0[p] = r0;
+          T0[WP + p] = r1;
+        }
+      } else {
+        for (int p = tid; p < Wa; p += NT) {
+          T0[p] = rhs_tilde(F0, 1, P, (int64_t)base + p, m1_0, mP2_0);
+          T0[WP + p] = rhs_tilde(F1, 1, P, (int64_t)base + p, m1_1, mP2_1);
+        }
+      }
+      __syncthreads();
+      PHASE_STAMP(5);
+      // constant-coefficient PCR, both fields, two levels per pass where possible:
+      //   u = r - a1 (r[-s] + r[+s]),   v = u - a2 (u[-2s] + u[+2s])
+      const double* A = T0;
+      double* B = T1;
+#pragma unroll
+      for (int l = 0; l < kPcrLevels; l += 2) {
+        const int sh = 1 << l;
+        const double a1 = fz.alpha[l];
+        if (l + 1 < kPcrLevels) {
+          const double a2 = fz.alpha[l + 1];
+          for (int p = tid; p < Wa; p += NT) {
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+              const double* Af_ = A + f * WP;
+              auto at = [&](int q) { return (q >= 0 && q < Wa) ? Af_[q] : 0.0; };
+              const double c0 = Af_[p];
+              const double cm1 = at(p - sh), cp1 = at(p + sh), cm2 = at(p - 2 * sh), cp2 = at(p + 2 * sh);
+              const double cm3 = at(p - 3 * sh), cp3 = at(p + 3 * sh);
+              const double u0 = c0 - a1 * (cm1 + cp1);
+              const double um = cm2 - a1 * (cm3 + cm1);
+              const double up = cp2 - a1 * (cp1 + cp3);
+              B[f * WP + p] = u0 - a2 * (um + up);
+            }
+          }
+        } else {
+          for (int p = tid; p < Wa; p += NT) {
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+              const double* Af_ = A + f * WP;
+              const double lft = p - sh >= 0 ? Af_[p - sh] : 0.0;
+              const double rgt = p + sh < Wa ? Af_[p + sh] : 0.0;
+              B[f * WP + p] = Af_[p] - a1 * (lft + rgt);
+            }
+          }
+        }
+        __syncthreads();
+        const double* t = A;
+        A = B;
+        B = const_cast<double*>(t);
+      }
+      PHASE_STAMP(6);
+      const double ib = fz.inv_b;
+      double* ring1 = const_cast<double*>(s.ring) + (int64_t)slot[0] * s.slot_elems;
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const double* F = f ? F1 : F0;
+        const double* Fw = f ? Fw1 : Fw0;
+        const double m1 = f ? m1_1 : m1_0, mP2 = f ? mP2_1 : mP2_0;
+        const double* Am = A + f * WP;
+        auto mt = [&](int k) { return Am[k - base] * ib; };
+        auto mk = [&](int k) -> double {
+          if (k == 1) return m1;
+          if (k == P - 2) return mP2;
+          if (k == 0) return 2.0 * m1 - (P - 2 == 2 ? mP2 : mt(2));
+          if (k == P - 1) return 2.0 * mP2 - (P - 3 == 1 ? m1 : mt(P - 3));
+          return mt(k);
+        };
+        double* rf = ring1 + (int64_t)f * g.cfield;
+        for (int k = k0 + tid; k < k1; k += NT) {
+          double c;
+          if (fastA) c = Fw[k] - mt(k) * (1.0 / 6.0);
+          else if (k >= 0 && k < P) c = __ldcg(F + k) - mk(k) * (1.0 / 6.0);
+          else if (k < 0) {
+            const double c0 = __ldcg(F) - mk(0) * (1.0 / 6.0), c1 = __ldcg(F + 1) - m1 * (1.0 / 6.0);
+            c = 6.0 * __ldcg(F) - 4.0 * c0 - c1;
+          } else {
+            const double cl = __ldcg(F + P - 1) - mk(P - 1) * (1.0 / 6.0);
+            const double cm = __ldcg(F + P - 2) - mP2 * (1.0 / 6.0);
+            c = 6.0 * __ldcg(F + P - 1) - 4.0 * cl - cm;
+          }
+          rf[k + 1] = c;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {                         // publish the CTA's ring stores (gpu-scope release)
+      __threadfence();
+      st_release(pp.ring_flag + bid, (unsigned)it + 1);
+    }
+    PHASE_STAMP(7);
+
+    // ---------------- level 1: the neighbours' coefficients of level n+1 from the ring
+    {
+      const int b = (K - 1) & 1;
+      if (warp == 0) issue_level(1, b);
+      level(1, b);
+      PHASE_STAMP(8);
+    }
+    __syncthreads();
+    PHASE_STAMP(3);
+
+    // ---------------- (4) reduction over node chunks (fixed order) and epilogue
+    double* red = buf0;
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double* q = red + (chunk * TP + li0 + r) * 3;
+        q[0] = Az[r];
+        q[1] = Af[r];
+        q[2] = Ay[r];
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < hi - lo; t += NT) {
+      double az = 0.0, af = 0.0, ay = 0.0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const double* q = red + (c * TP + t) * 3;
+        az += q[0];
+        af += q[1];
+        ay += q[2];
+      }
+      // z: Eq. 20 line 2 (explicit); y: Eq. 20 line 1 by Picard from E[y^{n+Ky}]
+      Driver<DRV, 1> dn(pb.dp);
+      dn.at(tn);
+      const double z = az * inv_gz0;
+      const double rhs = fma(s.ky_dt, af, ay);
+      double y = ay;
+      int itp;
+      for (itp = 1; itp <= s.picard_max; ++itp) {
+        const double yn = fma(s.ky_dt_gy0, dn(y, &z), rhs);
+        const double dy = fabs(yn - y);
+        const bool fixed = (yn == y);     // exact fixed point: the remaining iterations are identities
+        y = yn;
+        if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
+        if (fixed) { itp = s.picard_max; break; }
+      }
+      if (itp > s.picard_max) itp = s.picard_max;
+      const int p = lo + t;
+      vout[p] = y;
+      vout[P + p] = z;
+      s.picard[p] = itp;
+      if (!isfinite(y) || !isfinite(z)) atomicMin(s.bad, (unsigned long long)p);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(pp.done_flag + bid, (unsigned)it + 1);
+    }
+    PHASE_STAMP(4);
+  }
+}
+
+// instantiated (R, C, NT, MB = CTAs per SM) variants of the fused kernel; index 0 is the default
+struct FusedVariant { int R, C, NT, MB; };
+#define BSDE_FUSED_VARIANTS(X) X(0, 7, 8, 256, 2) X(1, 7, 8, 512, 1) X(2, 5, 4, 384, 1) X(3, 3, 4, 640, 1) X(4, 7, 4, 256, 1) X(5, 5, 4, 256, 2)
+static const FusedVariant kVariants[] = {
+#define BSDE_V_ROW(i, R, C, NT, MB) {R, C, NT, MB},
+    BSDE_FUSED_VARIANTS(BSDE_V_ROW)
+#undef BSDE_V_ROW
+};
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+int fused1d_num_variants() { return kNumVariants; }
+
+bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int qspan1, int nsm, int variant, Fused1D& fz,
+                      int& threads, int& blocks, size_t& smem) {
+  if (variant < 0 || variant >= kNumVariants) return false;
+  const FusedVariant v = kVariants[variant];
+  const int64_t P = g.P[0];
+  if (P >= (1ll << 30) || P < 8) return false;
+  const int nwpg = v.NT / (32 * v.C);
+  fz.variant = variant;
+  fz.TP = 32 * nwpg * v.R;
+  threads = v.NT;
+  blocks = (int)((P + fz.TP - 1) / fz.TP);
+  int wm = fz.TP + qspan_max + 4 + 2;
+  const int wr = (3 * v.C * fz.TP + 3) / 4;               // reduction reuses buf0/buf1
+  if (wr > wm) wm = wr;
+  wm = (wm + 1) & ~1;
+  fz.WMAX = wm;
+  fz.WP = ((fz.TP + 1 + 8 + 2 * kPcrHalo + 4) + 1) & ~1;      // PCR extent of the own tile
+  smem = 128 + ((size_t)4 * wm + 2 * (size_t)(fz.WP + 4) + 4 * (size_t)fz.WP) * sizeof(double);
+  (void)K; (void)L; (void)nsm;
+  return smem <= (v.MB == 1 ? 220 * 1024 : 112 * 1024);
+}
+
+void pcr_constants(double* alpha, double* inv_b);
+
+template <int DRV, int R, int C, int NT, int MB>
+static cudaError_t launch_fused1d(const StepArgs& s, const Grid& g, const Problem& pb, const Fused1D& fz0,
+                                  const Persist1D& pp, int threads, int blocks, size_t smem, cudaStream_t st) {
+  Fused1D fz = fz0;
+  pcr_constants(fz.alpha, &fz.inv_b);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;     // neighbour flags need all CTAs co-resident
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, quad1d_fused<DRV, R, C, NT, MB>, s, g, pb, fz, pp);
+}
+
+template <int DRV>
+static cudaError_t launch_fused1d_v(const StepArgs& s, const Grid& g, const Problem& pb, const Fused1D& fz,
+                                    const Persist1D& pp, int threads, int blocks, size_t smem, cudaStream_t st) {
+  switch (fz.variant) {
+#define BSDE_V_CASE(i, R, C, NT, MB) \
+    case i: return launch_fused1d<DRV, R, C, NT, MB>(s, g, pb, fz, pp, threads, blocks, smem, st);
+    BSDE_FUSED_VARIANTS(BSDE_V_CASE)
+#undef BSDE_V_CASE
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int DRV>
+static cudaError_t set_attr_drv() {
+  cudaError_t e = cudaSuccess;
+#define BSDE_V_ATTR(i, R, C, NT, MB)                                                                   \
+  if (e == cudaSuccess)                                                                               \
+    e = cudaFuncSetAttribute(quad1d_fused<DRV, R, C, NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             MB == 1 ? 220 * 1024 : 112 * 1024);
+  BSDE_FUSED_VARIANTS(BSDE_V_ATTR)
+#undef BSDE_V_ATTR
+  return e;
+}
+
+// blocks per SM the fused kernel can keep resident (for the cooperative launch)
+int fused1d_blocks_per_sm(int variant, size_t smem) {
+  int nb = 0;
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (variant) {
+#define BSDE_V_OCC(i, R, C, NT, MB) \
+    case i: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, quad1d_fused<DRV_DIFF, R, C, NT, MB>, NT, smem); break;
+    BSDE_FUSED_VARIANTS(BSDE_V_OCC)
+#undef BSDE_V_OCC
+  }
+  return e == cudaSuccess ? nb : 0;
+}
+
+// nsteps consecutive steps (ring_mode 1: levels n0, n0-1, ...) or one step with StepArgs'
+// fields (ring_mode 0); one cooperative launch either way
+cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem& pb, const Fused1D& fz, int n0,
+                                 int nsteps, int ring_mode, int cur, double t0, double dt, double* v0, double* v1,
+                                 unsigned* flags, const int* D, int DK, int threads, int blocks, size_t smem,
+                                 cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(unsigned) * 2 * (size_t)blocks, st);
+  if (e != cudaSuccess) return e;
+  Persist1D pp{};
+  pp.n0 = n0;
+  pp.nsteps = nsteps;
+  pp.ring_mode = ring_mode;
+  pp.cur = cur;
+  pp.t0 = t0;
+  pp.dt = dt;
+  pp.vbuf[0] = v0;
+  pp.vbuf[1] = v1;
+  pp.ring_flag = flags;
+  pp.done_flag = flags + blocks;
+  for (int j = 0; j <= kMaxK; ++j) pp.D[j] = D[j];
+  pp.DK = DK;
+  switch (pb.driver_id) {
+    case DRV_ZERO: return launch_fused1d_v<DRV_ZERO>(s, g, pb, fz, pp, threads, blocks, smem, st);
+    case DRV_AFFINE: return launch_fused1d_v<DRV_AFFINE>(s, g, pb, fz, pp, threads, blocks, smem, st);
+    case DRV_EX1: return launch_fused1d_v<DRV_EX1>(s, g, pb, fz, pp, threads, blocks, smem, st);
+    case DRV_EX2: return launch_fused1d_v<DRV_EX2>(s, g, pb, fz, pp, threads, blocks, smem, st);
+    case DRV_DIFF: return launch_fused1d_v<DRV_DIFF>(s, g, pb, fz, pp, threads, blocks, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}

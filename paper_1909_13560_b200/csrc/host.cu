@@ -1,0 +1,884 @@
+// host.cu -- C ABI (include/bsde.h) and host runtime of the B200 multistep BSDE solver.
+//
+// Setup (steps 1-2 of the algorithm) runs on the host: grids and the
+// balance rule, the Gauss-Hermite rule (Eq. 21), the weight rows (Tables 1-2), the
+// translation-invariant tap tables uploaded to constant memory.
+// Everything that touches grid data (terminal/initial layers, spline builds, the
+// backward sweep of Eq. 20) runs in the kernels of kernels.cu.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/bsde.h"
+#include "bsde_internal.h"
+
+namespace bsde {
+cudaError_t upload_arena(const void* data, int bytes, int offset, cudaStream_t st);
+int arena_capacity_bytes();
+cudaError_t upload_gl(const double* x, const double* w, cudaStream_t st);
+cudaError_t launch_layer(const Problem& pb, const Grid& g, double t, bool terminal, double* values, cudaStream_t st);
+cudaError_t launch_spline(const Grid& g, const double* values, int F, double* slot, double* tmp0, double* tmp1,
+                          cudaStream_t st, int64_t* launches);
+cudaError_t launch_generic_step(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st);
+bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int qspan1, int nsm, int variant, Fused1D& fz,
+                      int& threads, int& blocks, size_t& smem);
+int fused1d_num_variants();
+cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem& pb, const Fused1D& fz, int n0,
+                                 int nsteps, int ring_mode, int cur, double t0, double dt, double* v0, double* v1,
+                                 unsigned* flags, const int* D, int DK, int threads, int blocks, size_t smem,
+                                 cudaStream_t st);
+int fused1d_blocks_per_sm(int variant, size_t smem);
+cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
+cudaError_t init_device_attributes();
+}  // namespace bsde
+
+using namespace bsde;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_setup_error;
+
+struct bsde_ctx {
+  bsde_config cfg{};
+  Problem pb{};
+  Grid g{};
+  int d = 1, F = 2, K = 1, Ky = 1, Kz = 1, L = 1, N = 1;
+  double dt = 0;
+  int level = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  bool own_ws = false;
+  double* vbuf[2] = {nullptr, nullptr};   // ping-pong value buffers, F * npts each
+  int cur = 0;                  // vbuf[cur] holds the newest level
+  int fused_variant = 0;        // fused 1-D kernel variant (kernel_variant >= 10 selects variant - 10)
+  int nsm = 148;
+  double* ring = nullptr;       // (RS + 1) * F * cfield ; slot RS = scratch
+  int RS = 3;                   // ring slots: K + 2 (level m in slot m % RS; the 2 spare slots let the
+                                // fused kernel's CTAs run up to 2 steps apart without write-after-read hazards)
+  double* tmp0 = nullptr;       // cfield
+  double* tmp1 = nullptr;       // cfield
+  int32_t* picard = nullptr;    // npts
+  unsigned long long* bad = nullptr;
+  unsigned* barrier = nullptr;  // grid-barrier counter of the persistent fused kernel
+  double* dres = nullptr;       // 8 doubles
+  int tap_off = -1, tap1_off = -1, tap_count = 0;        // byte offsets in the constant arena
+  int boot_tap_off = -1, boot_tap1_off = -1;
+  int qspan = 0, qspan1 = 0, boot_qspan = 0, boot_qspan1 = 0;
+  struct Geo {
+    bool ok = false;
+    Fused1D fz{};
+    int threads = 0, blocks = 0;
+    int D[kMaxK + 1] = {};        // D[j]: CTA distance of level j's window; D[0]: values halo
+    int DK = 1;                   // max over levels
+    size_t smem = 0;
+  } geo, boot_geo;
+  double gy[7]{}, gz[7]{};
+  double gh_a[kMaxL]{}, gh_w[kMaxL]{};
+  std::vector<AxisTap> taps;    // host copy of the main table (K * d * L)
+  int64_t launches = 0;
+  unsigned long long* phase_ns = nullptr;   // debug: BSDE_PHASE_TIMING=1
+  std::string err;
+  bool closed_form = true;
+};
+
+static bsde_status set_err(bsde_ctx* c, bsde_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  else g_setup_error = buf;
+  return st;
+}
+
+#define CU(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t _e = (call);                                                                  \
+    if (_e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "%s: %s (%s:%d)", #call,         \
+                                          cudaGetErrorString(_e), __FILE__, __LINE__);        \
+  } while (0)
+
+// ------------------------------------------------------------------ constant-arena allocator
+namespace {
+struct Arena {
+  std::mutex mu;
+  std::vector<std::pair<int, int>> used;   // (offset, count)
+};
+Arena g_arena[64];
+
+int arena_alloc(int dev, int count) {        // count in bytes, 16-byte granularity
+  count = (count + 15) & ~15;
+  if (dev < 0 || dev >= 64) return -1;
+  Arena& a = g_arena[dev];
+  std::lock_guard<std::mutex> lk(a.mu);
+  std::sort(a.used.begin(), a.used.end());
+  int pos = 0;
+  for (auto& u : a.used) {
+    if (u.first - pos >= count) break;
+    pos = (u.first + u.second + 15) & ~15;
+  }
+  if (pos + count > arena_capacity_bytes()) return -1;
+  a.used.push_back({pos, count});
+  return pos;
+}
+void arena_free(int dev, int off) {
+  if (dev < 0 || dev >= 64 || off < 0) return;
+  Arena& a = g_arena[dev];
+  std::lock_guard<std::mutex> lk(a.mu);
+  for (size_t i = 0; i < a.used.size(); ++i)
+    if (a.used[i].first == off) { a.used.erase(a.used.begin() + i); return; }
+}
+
+// ------------------------------------------------------------------ numerics of the setup
+// Weight rows as printed: Table 1 (y, gamma^{Ky}_{Ky,j}) and Table 2 (z, gamma^1_{Kz,j}),
+// PAPER.md:235-269; Eq. 20's b is read as gamma (R1).
+const long double kTab1[6][7] = {
+    {1.0L / 2, 1.0L / 2},
+    {1.0L / 6, 2.0L / 3, 1.0L / 6},
+    {1.0L / 8, 3.0L / 8, 3.0L / 8, 1.0L / 8},
+    {1.0L / 12, 1.0L / 3, 1.0L / 6, 1.0L / 3, 1.0L / 12},
+    {41.0L / 600, 19.0L / 75, 107.0L / 600, 107.0L / 600, 19.0L / 75, 41.0L / 600},
+    {19.0L / 336, 3.0L / 14, 15.0L / 112, 4.0L / 21, 15.0L / 112, 3.0L / 14, 19.0L / 336}};
+const long double kTab2[6][7] = {
+    {1.0L / 2, 1.0L / 2},
+    {5.0L / 12, 2.0L / 3, -1.0L / 12},
+    {3.0L / 8, 19.0L / 24, -5.0L / 24, 1.0L / 24},
+    {35.0L / 96, 5.0L / 6, -13.0L / 48, 1.0L / 12, -1.0L / 96},
+    {131.0L / 360, 151.0L / 180, -103.0L / 360, 37.0L / 360, -1.0L / 45, 1.0L / 360},
+    {163.0L / 448, 47.0L / 56, -129.0L / 448, 3.0L / 28, -37.0L / 1344, 1.0L / 168, -1.0L / 1344}};
+
+// Gauss-Hermite rule (Eq. 21): nodes are the eigenvalues of the Jacobi matrix of the
+// Hermite weight e^{-x^2} (diagonal 0, off-diagonal sqrt(k/2)), found by Sturm-sequence
+// bisection in long double; weights by the Christoffel function 1 / sum_k p_k(a)^2 of
+// the orthonormal Hermite polynomials.
+int sturm_count(int L, long double x) {   // eigenvalues < x
+  int cnt = 0;
+  long double q = -x;                     // d_1 - x, d = 0
+  if (q < 0) ++cnt;
+  for (int k = 1; k < L; ++k) {
+    const long double b2 = (long double)k / 2.0L;
+    if (q == 0) q = 1e-4000L;
+    q = -x - b2 / q;
+    if (q < 0) ++cnt;
+  }
+  return cnt;
+}
+
+void hermite_rule(int L, double* a, double* w) {
+  const long double bound = sqrtl(2.0L * L) + 2.0L;
+  for (int i = 0; i < L; ++i) {           // i-th smallest eigenvalue
+    long double lo = -bound, hi = bound;
+    for (int it = 0; it < 200; ++it) {
+      const long double mid = 0.5L * (lo + hi);
+      if (mid == lo || mid == hi) break;
+      if (sturm_count(L, mid) > i) hi = mid; else lo = mid;
+    }
+    long double x = 0.5L * (lo + hi);
+    if (L % 2 == 1 && i == L / 2) x = 0.0L;
+    // Christoffel weight
+    const long double pim4 = 0.75112554446494248285870300477622L;   // pi^{-1/4}
+    long double pm = 0.0L, p = pim4, sum = p * p;
+    for (int k = 1; k < L; ++k) {
+      const long double pn = (sqrtl(2.0L) * x * p - sqrtl((long double)(k - 1)) * pm) / sqrtl((long double)k);
+      pm = p; p = pn;
+      sum += p * p;
+    }
+    a[i] = (double)x;
+    w[i] = (double)(1.0L / sum);
+  }
+  // exact symmetry
+  for (int i = 0; i < L / 2; ++i) {
+    const double m = 0.5 * (a[L - 1 - i] - a[i]);
+    a[i] = -m; a[L - 1 - i] = m;
+    const double ww = 0.5 * (w[i] + w[L - 1 - i]);
+    w[i] = ww; w[L - 1 - i] = ww;
+  }
+}
+
+// Gauss-Legendre rule on [-1, 1] for the d >= 2 smoothing (R11): Newton on
+// P_n from Tricomi's initial guesses, long double.
+void legendre_rule(int n, double* x, double* w) {
+  for (int i = 0; i < n; ++i) {
+    long double z = -cosl(3.14159265358979323846264338327950288L * (4.0L * (i + 1) - 1.0L) / (4.0L * n + 2.0L));
+    long double dp = 1.0L;
+    for (int it = 0; it < 60; ++it) {
+      long double p0 = 1.0L, p1 = z;
+      for (int k = 2; k <= n; ++k) {
+        const long double p2 = ((2.0L * k - 1.0L) * z * p1 - (k - 1.0L) * p0) / k;
+        p0 = p1; p1 = p2;
+      }
+      dp = n * (z * p1 - p0) / (z * z - 1.0L);
+      const long double dz = p1 / dp;
+      z -= dz;
+      if (fabsl(dz) < 1e-20L) break;
+    }
+    x[i] = (double)z;
+    w[i] = (double)(2.0L / ((1.0L - z * z) * dp * dp));
+  }
+}
+
+// balance rule with reading R3: q = min(Ky+1, Kz, 3), M = 2 ceil(X/dx)
+int64_t balanced_points(double width, double dt, int Ky, int Kz, int r) {
+  const int q = std::min(std::min(Ky + 1, Kz), 3);
+  const long double dxs = powl((long double)dt, (long double)(q + 1) / (long double)r);
+  const long double cnt = 0.5L * (long double)width / dxs;
+  const int64_t half = (int64_t)ceill(cnt * (1.0L - 1e-12L));
+  return 2 * half + 1;
+}
+
+// B-spline basis of a shift theta in [0, 1)
+void bspline_basis(long double t, double* B) {
+  const long double u = 1.0L - t;
+  B[0] = (double)(u * u * u / 6.0L);
+  B[1] = (double)((3.0L * t * t * t - 6.0L * t * t + 4.0L) / 6.0L);
+  B[2] = (double)((-3.0L * t * t * t + 3.0L * t * t + 3.0L * t + 1.0L) / 6.0L);
+  B[3] = (double)(t * t * t / 6.0L);
+}
+
+// tap table of levels 1..K for step dt: X = x_i + s, s = sqrt(2 j dt) a_l
+void build_taps(const bsde_ctx* c, int K, double dt, std::vector<AxisTap>& out, int* qspan, int* qspan1) {
+  const int d = c->d, L = c->L;
+  out.assign((size_t)K * d * L, AxisTap{});
+  const long double rpi = 1.0L / sqrtl(3.14159265358979323846264338327950288L);
+  int span = 0;
+  for (int j = 1; j <= K; ++j)
+    for (int a = 0; a < d; ++a) {
+      for (int l = 0; l < L; ++l) {
+        AxisTap& t = out[((size_t)(j - 1) * d + a) * L + l];
+        const long double s = sqrtl(2.0L * j * (long double)dt) * (long double)c->gh_a[l];
+        const long double u = s / (long double)c->g.dx[a];
+        const long double q = floorl(u);
+        t.q = (int32_t)q;
+        bspline_basis(u - q, t.B);
+        t.w = (double)((long double)c->gh_w[l] * rpi);
+        t.s = (double)s;
+      }
+      span = std::max(span, out[((size_t)(j - 1) * d + a) * L + L - 1].q - out[((size_t)(j - 1) * d + a) * L].q);
+    }
+  if (qspan) *qspan = span;
+  if (qspan1) *qspan1 = out[(size_t)(L - 1)].q - out[0].q;    // level 1, axis 0
+}
+
+// fused 1-D records: stencil of level j / node l with the scheme weights folded in
+std::vector<Tap1D> build_tap1d(const std::vector<AxisTap>& t, int K, int L, int Ky, int Kz, const double* gy,
+                               const double* gz) {
+  std::vector<Tap1D> out((size_t)K * L);
+  for (int j = 1; j <= K; ++j) {
+    const long double gzj = j <= Kz ? gz[j] : 0.0L, gyj = j <= Ky ? gy[j] : 0.0L;
+    const long double czj = (j == 1 ? 1.0L : 0.0L) - gzj;
+    for (int l = 0; l < L; ++l) {
+      const AxisTap& a = t[(size_t)(j - 1) * L + l];
+      Tap1D& r = out[(size_t)(j - 1) * L + l];
+      r.q = a.q;
+      r.pad = 0;
+      for (int k = 0; k < 4; ++k) r.B[k] = a.B[k];
+      const long double w = a.w;
+      r.wcz = (double)(w * czj);
+      r.wgz = (double)(w * gzj * (long double)a.s);
+      r.wgy = (double)(w * gyj);
+      r.wy = j == Ky ? a.w : 0.0;
+    }
+  }
+  return out;
+}
+
+// CTA distances of the fused kernel's neighbour waits; the fused path needs all CTAs
+// co-resident (one per SM) and <= 8192 CTAs of flags
+void set_distances(bsde_ctx* c, const std::vector<AxisTap>& t, int K, bsde_ctx::Geo& geo) {
+  if (!geo.ok) return;
+  const int L = c->L, TP = geo.fz.TP;
+  auto reach = [&](int j) {
+    const int qa = -t[(size_t)(j - 1) * L].q, qb = t[(size_t)(j - 1) * L + L - 1].q;
+    return std::max(qa, qb) + 4;
+  };
+  geo.D[0] = (kPcrHalo + 6 + TP - 1) / TP;
+  int dk = geo.D[0];
+  for (int j = 1; j <= K; ++j) {
+    geo.D[j] = (reach(j) + TP - 1) / TP;
+    dk = std::max(dk, geo.D[j]);
+  }
+  geo.DK = dk;
+  const int per_sm = fused1d_blocks_per_sm(geo.fz.variant, geo.smem);
+  if (geo.blocks > c->nsm * per_sm || geo.blocks > 8192) geo.ok = false;
+}
+
+bool closed_form_supported(const bsde_config& cfg) {
+  const int t = cfg.terminal_id, f = cfg.driver_id, d = cfg.d;
+  const double* q = cfg.driver_params;
+  if (t == BSDE_TERM_CONST) return f == BSDE_DRV_ZERO || (f == BSDE_DRV_AFFINE && q[1] == 0 && q[2] == 0 && q[3] == 0);
+  if (t == BSDE_TERM_POLY)
+    return f == BSDE_DRV_ZERO || (f == BSDE_DRV_AFFINE && q[1] == 0 && q[2] == 0 && q[3] == 0 && q[4] == 0);
+  if (t == BSDE_TERM_LOGISTIC) return f == BSDE_DRV_EX1;
+  if (t == BSDE_TERM_EX2) return f == BSDE_DRV_EX2 && d == 1;
+  if (t == BSDE_TERM_CALL_W) return (f == BSDE_DRV_AFFINE || f == BSDE_DRV_DIFF_RATES) && d == 1;
+  if (t == BSDE_TERM_SIN_SUM) return f == BSDE_DRV_AFFINE;
+  if (t == BSDE_TERM_EXCHANGE_W) return f == BSDE_DRV_AFFINE && d == 2;
+  if (t == BSDE_TERM_GEO_BASKET_W) return f == BSDE_DRV_DIFF_RATES;
+  return false;
+}
+
+bsde_status validate(const bsde_config* cfg, bsde_ctx* c) {
+  if (!cfg) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "cfg is NULL");
+  if (cfg->struct_size != sizeof(bsde_config))
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "struct_size %u != sizeof(bsde_config) %zu", cfg->struct_size,
+                   sizeof(bsde_config));
+  if (cfg->d < 1 || cfg->d > 3) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "d=%d outside 1..3", cfg->d);
+  if (cfg->m != 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "m=%d: only m=1 is supported", cfg->m);
+  if (cfg->Ky < 1 || cfg->Ky > 6 || cfg->Kz < 1 || cfg->Kz > 6)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "Ky=%d Kz=%d outside 1..6 (Tables 1-2)", cfg->Ky, cfg->Kz);
+  if (cfg->L < 1 || cfg->L > kMaxL) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "L=%d outside 1..64", cfg->L);
+  if (!(cfg->T > cfg->t0)) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "T <= t0");
+  const int K = std::max(cfg->Ky, cfg->Kz);
+  if (cfg->N < K) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "N=%d < K=%d", cfg->N, K);
+  if (cfg->picard_max < 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "picard_max < 1");
+  if (cfg->driver_id < 0 || cfg->driver_id > 4) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "driver_id");
+  if (cfg->terminal_id < 0 || cfg->terminal_id > 7) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "terminal_id");
+  if (cfg->driver_id == BSDE_DRV_EX2 && cfg->d != 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "EX2 driver is 1-D");
+  if (cfg->terminal_id == BSDE_TERM_EXCHANGE_W && cfg->d != 2)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "exchange payoff needs d=2");
+  if (cfg->nranks > 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "nranks > 1 not supported by this build");
+  for (int a = 0; a < cfg->d; ++a) {
+    if (!(cfg->xhi[a] > cfg->xlo[a])) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "empty box on axis %d", a);
+    if (cfg->npts[a] != 0 && cfg->npts[a] < 4)
+      return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "npts[%d]=%lld < 4 (not-a-knot needs 4 points)", a,
+                     (long long)cfg->npts[a]);
+  }
+  if (cfg->bootstrap == 0 && K > 1 && !closed_form_supported(*cfg))
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT,
+                   "no closed form for terminal %d with driver %d: use bootstrap=1", cfg->terminal_id, cfg->driver_id);
+  return BSDE_OK;
+}
+
+void fill_grid(const bsde_config* cfg, Grid& g, double dt) {
+  g.d = cfg->d;
+  g.npts = 1;
+  for (int a = 0; a < 3; ++a) { g.P[a] = 1; g.xlo[a] = 0; g.xhi[a] = 0; g.dx[a] = 0; }
+  for (int a = 0; a < cfg->d; ++a) {
+    int64_t P = cfg->npts[a];
+    if (P == 0) P = balanced_points(cfg->xhi[a] - cfg->xlo[a], dt, cfg->Ky, cfg->Kz, cfg->r > 0 ? cfg->r : 4);
+    g.P[a] = P;
+    g.xlo[a] = cfg->xlo[a];
+    g.xhi[a] = cfg->xhi[a];
+    g.dx[a] = (cfg->xhi[a] - cfg->xlo[a]) / (double)(P - 1);
+    g.npts *= P;
+  }
+  const int d = cfg->d;
+  g.vstride[d - 1] = 1;
+  for (int a = d - 2; a >= 0; --a) g.vstride[a] = g.vstride[a + 1] * g.P[a + 1];
+  // coefficient layout: extent P+3 per axis (c_{-1} .. c_{P+1}); last axis padded to 4
+  const int64_t lastQ = ((g.P[d - 1] + 3 + 3) / 4) * 4;
+  g.cstride[d - 1] = 1;
+  int64_t ext = lastQ;
+  for (int a = d - 2; a >= 0; --a) { g.cstride[a] = ext; ext *= g.P[a] + 3; }
+  g.cfield = ext;
+  for (int a = d; a < 3; ++a) { g.vstride[a] = 0; g.cstride[a] = 0; }
+}
+
+struct Layout {
+  size_t values, ring, tmp0, tmp1, picard, bad, barrier, dres, total;
+};
+// values: 2 ping-pong buffers of F * npts (the fused 1-D step reads level n+1 while
+// other CTAs write level n)
+
+Layout layout(const Grid& g, int F, int K) {
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  Layout L{};
+  size_t off = 0;
+  L.values = off; off += 2 * al(sizeof(double) * F * g.npts);
+  L.ring = off; off += al(sizeof(double) * (size_t)(K + 3) * F * g.cfield);
+  L.tmp0 = off; off += g.d >= 2 ? al(sizeof(double) * g.cfield) : 0;
+  L.tmp1 = off; off += g.d >= 3 ? al(sizeof(double) * g.cfield) : 0;
+  L.picard = off; off += al(sizeof(int32_t) * g.npts);
+  L.bad = off; off += 256;
+  L.barrier = off; off += al(sizeof(unsigned) * 2 * 8192);      // fused-kernel progress flags
+  L.dres = off; off += 256;
+  L.total = off;
+  return L;
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// One step of the scheme (Eq. 20) from the newest values (level n+1) and the ring slots of
+// levels n+2..n+K: slots[0] receives the spline of the newest values.  Output -> the other
+// value buffer, which becomes the newest.
+bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, const double* gzl, double dtl,
+                     double tn, const int* slots, int tap_off, int tap1_off, const bsde_ctx::Geo& geo, int variant) {
+  StepArgs s{};
+  s.ring = c->ring;
+  s.slot_elems = (int64_t)c->F * c->g.cfield;
+  for (int j = 1; j <= Kl; ++j) {
+    s.slot[j - 1] = slots[j - 1];
+    s.t_level[j - 1] = tn + j * dtl;
+    const double gzj = j <= Kzl ? gzl[j] : 0.0;
+    s.gzj[j - 1] = gzj;
+    s.czj[j - 1] = (j == 1 ? 1.0 : 0.0) - gzj;
+    s.gyj[j - 1] = j <= Kyl ? gyl[j] : 0.0;
+  }
+  s.K = Kl; s.Ky = Kyl; s.Kz = Kzl; s.L = c->L;
+  s.ring_slots = c->RS;
+  s.tap_off = tap_off;
+  s.tap1_off = tap1_off;
+  s.gz0 = gzl[0];
+  s.ky_dt = Kyl * dtl;
+  s.ky_dt_gy0 = Kyl * dtl * gyl[0];
+  s.tn = tn;
+  s.picard_max = c->cfg.picard_max;
+  s.picard_tol = c->cfg.picard_tol;
+  s.values_in = c->vbuf[c->cur];
+  s.values = c->vbuf[c->cur ^ 1];
+  s.picard = c->picard;
+  s.bad = c->bad;
+  s.phase_ns = c->phase_ns;
+  cudaError_t e;
+  if (c->d == 1 && (variant == 0 || variant >= 10) && geo.ok && tap1_off >= 0) {
+    e = launch_fused1d_steps(s, c->g, c->pb, geo.fz, 0, 1, 0, c->cur, 0.0, 0.0, c->vbuf[0], c->vbuf[1], c->barrier,
+                             geo.D, geo.DK, geo.threads, geo.blocks, geo.smem, c->stream);
+    ++c->launches;
+  } else {
+    e = launch_spline(c->g, c->vbuf[c->cur], c->F, c->ring + (int64_t)slots[0] * c->F * c->g.cfield, c->tmp0,
+                      c->tmp1, c->stream, &c->launches);
+    if (e == cudaSuccess) {
+      e = launch_generic_step(s, c->g, c->pb, c->stream);
+      ++c->launches;
+    }
+  }
+  if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "step kernels: %s", cudaGetErrorString(e));
+  c->cur ^= 1;
+  return BSDE_OK;
+}
+
+bsde_status spline_into(bsde_ctx* c, int slot) {
+  cudaError_t e = launch_spline(c->g, c->vbuf[c->cur], c->F, c->ring + (int64_t)slot * c->F * c->g.cfield, c->tmp0,
+                                c->tmp1, c->stream, &c->launches);
+  if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "spline kernel: %s", cudaGetErrorString(e));
+  return BSDE_OK;
+}
+
+void release(bsde_ctx* c) {
+  if (!c) return;
+  int dev = c->cfg.device;
+  if (c->tap_off >= 0) arena_free(dev, c->tap_off);
+  if (c->tap1_off >= 0) arena_free(dev, c->tap1_off);
+  if (c->boot_tap_off >= 0) arena_free(dev, c->boot_tap_off);
+  if (c->boot_tap1_off >= 0) arena_free(dev, c->boot_tap1_off);
+  if (c->own_ws && c->ws) cudaFree(c->ws);
+  if (c->phase_ns) cudaFree(c->phase_ns);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ ABI
+extern "C" {
+
+bsde_status bsde_query_workspace(const bsde_config* cfg, size_t* bytes) {
+  bsde_ctx* c = nullptr;
+  bsde_status st = validate(cfg, c);
+  if (st) return st;
+  const int K = std::max(cfg->Ky, cfg->Kz);
+  Grid g{};
+  fill_grid(cfg, g, (cfg->T - cfg->t0) / cfg->N);
+  *bytes = layout(g, 1 + cfg->d, K).total;
+  return BSDE_OK;
+}
+
+bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, bsde_ctx** out) {
+  const double t_start = now_s();
+  if (out) *out = nullptr;
+  if (!out) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "out is NULL");
+  bsde_status st = validate(cfg, nullptr);
+  if (st) return st;
+  bsde_ctx* c = new (std::nothrow) bsde_ctx();
+  if (!c) return set_err(nullptr, BSDE_ERR_RESOURCE_LIMIT, "host allocation failed");
+  c->cfg = *cfg;
+  c->d = cfg->d;
+  c->F = 1 + cfg->d;
+  c->Ky = cfg->Ky;
+  c->Kz = cfg->Kz;
+  c->K = std::max(cfg->Ky, cfg->Kz);
+  c->RS = c->K + 2;
+  c->L = cfg->L;
+  c->N = cfg->N;
+  c->dt = (cfg->T - cfg->t0) / cfg->N;
+  fill_grid(cfg, c->g, c->dt);
+  c->pb.d = c->d;
+  c->pb.driver_id = cfg->driver_id;
+  c->pb.terminal_id = cfg->terminal_id;
+  c->pb.smoothing = cfg->smoothing;
+  for (int k = 0; k < 12; ++k) { c->pb.dp[k] = cfg->driver_params[k]; c->pb.tp[k] = cfg->terminal_params[k]; }
+  c->pb.T = cfg->T;
+  c->pb.t0 = cfg->t0;
+  c->pb.dt = c->dt;
+  c->pb.N = cfg->N;
+  for (int j = 0; j <= c->Ky; ++j) c->gy[j] = (double)kTab1[c->Ky - 1][j];
+  for (int j = 0; j <= c->Kz; ++j) c->gz[j] = (double)kTab2[c->Kz - 1][j];
+  hermite_rule(c->L, c->gh_a, c->gh_w);
+
+  auto fail = [&](bsde_status s) {
+    g_setup_error = c->err;
+    release(c);
+    return s;
+  };
+  cudaError_t ce = cudaSetDevice(cfg->device);
+  if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "cudaSetDevice(%d): %s", cfg->device, cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
+  ce = init_device_attributes();
+  if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "kernel attributes: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
+  if (cfg->stream) c->stream = (cudaStream_t)cfg->stream;
+  else {
+    ce = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "stream: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
+    c->own_stream = true;
+  }
+  // memory
+  Layout lay = layout(c->g, c->F, c->K);
+  if (d_workspace) {
+    if (bytes < lay.total) {
+      set_err(c, BSDE_ERR_RESOURCE_LIMIT, "workspace of %zu bytes < required %zu", bytes, lay.total);
+      return fail(BSDE_ERR_RESOURCE_LIMIT);
+    }
+    c->ws = (char*)d_workspace;
+    c->ws_bytes = bytes;
+  } else {
+    ce = cudaMalloc((void**)&c->ws, lay.total);
+    if (ce != cudaSuccess) {
+      set_err(c, BSDE_ERR_RESOURCE_LIMIT, "cudaMalloc(%zu) failed: %s (grid %lld points)", lay.total,
+              cudaGetErrorString(ce), (long long)c->g.npts);
+      cudaGetLastError();
+      return fail(BSDE_ERR_RESOURCE_LIMIT);
+    }
+    c->own_ws = true;
+    c->ws_bytes = lay.total;
+  }
+  c->vbuf[0] = (double*)(c->ws + lay.values);
+  c->vbuf[1] = c->vbuf[0] + (lay.ring - lay.values) / (2 * sizeof(double));
+  c->ring = (double*)(c->ws + lay.ring);
+  c->tmp0 = (double*)(c->ws + lay.tmp0);
+  c->tmp1 = (double*)(c->ws + lay.tmp1);
+  c->picard = (int32_t*)(c->ws + lay.picard);
+  c->bad = (unsigned long long*)(c->ws + lay.bad);
+  c->barrier = (unsigned*)(c->ws + lay.barrier);
+  c->dres = (double*)(c->ws + lay.dres);
+  if (getenv("BSDE_PHASE_TIMING") && cudaMalloc((void**)&c->phase_ns, (size_t)8 * 16 * 600 * 1100) != cudaSuccess) c->phase_ns = nullptr;
+  // zero the whole ring once: the padding entry c_{P+1} of every line is read with weight 0
+  ce = cudaMemsetAsync(c->ring, 0, sizeof(double) * (size_t)(c->RS + 1) * c->F * c->g.cfield, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->picard, 0, sizeof(int32_t) * c->g.npts, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->bad, 0xff, sizeof(unsigned long long), c->stream);
+  if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "memset: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
+
+  // tap tables -> constant arena
+  build_taps(c, c->K, c->dt, c->taps, &c->qspan, &c->qspan1);
+  if (cfg->kernel_variant >= 10) c->fused_variant = cfg->kernel_variant - 10;
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
+  if (c->d == 1) {
+    c->geo.ok = fused1d_geometry(c->g, c->K, c->L, c->qspan, c->qspan1, c->nsm, c->fused_variant, c->geo.fz,
+                                 c->geo.threads, c->geo.blocks, c->geo.smem);
+    set_distances(c, c->taps, c->K, c->geo);
+  }
+  c->tap_count = (int)c->taps.size();
+  {
+    const int bytes = (int)(sizeof(AxisTap) * c->taps.size());
+    c->tap_off = arena_alloc(cfg->device, bytes);
+    if (c->tap_off < 0) {
+      set_err(c, BSDE_ERR_RESOURCE_LIMIT, "constant tap arena full (%d bytes needed)", bytes);
+      return fail(BSDE_ERR_RESOURCE_LIMIT);
+    }
+    ce = upload_arena(c->taps.data(), bytes, c->tap_off, c->stream);
+    if (ce == cudaSuccess && c->d == 1) {
+      std::vector<Tap1D> t1 = build_tap1d(c->taps, c->K, c->L, c->Ky, c->Kz, c->gy, c->gz);
+      const int b1 = (int)(sizeof(Tap1D) * t1.size());
+      c->tap1_off = arena_alloc(cfg->device, b1);
+      if (c->tap1_off >= 0) ce = upload_arena(t1.data(), b1, c->tap1_off, c->stream);
+      else c->geo.ok = false;               // no room: generic kernel
+    }
+    if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "taps: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
+  }
+  {
+    double gx[kSmoothGL], gw[kSmoothGL];
+    legendre_rule(kSmoothGL, gx, gw);
+    ce = upload_gl(gx, gw, c->stream);
+    if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "GL: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
+  }
+
+  // K initial layers N, N-1, ..., N-K+1
+  const int K = c->K, N = c->N;
+  ce = launch_layer(c->pb, c->g, cfg->T, true, c->vbuf[c->cur], c->stream);
+  ++c->launches;
+  if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "layer: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
+  if ((st = spline_into(c, N % c->RS))) return fail(st);
+  c->level = N;
+  if (K > 1 && cfg->bootstrap == 1) {
+    // one-step scheme (K = 1) on S_b sub-steps per coarse interval (reading R9)
+    const int Sb = cfg->bootstrap_substeps > 0 ? cfg->bootstrap_substeps : 1;
+    const double db = c->dt / Sb;
+    std::vector<AxisTap> bt;
+    build_taps(c, 1, db, bt, &c->boot_qspan, &c->boot_qspan1);
+    if (c->d == 1)
+      c->boot_geo.ok = fused1d_geometry(c->g, 1, c->L, c->boot_qspan, c->boot_qspan1, c->nsm, c->fused_variant,
+                                        c->boot_geo.fz, c->boot_geo.threads, c->boot_geo.blocks, c->boot_geo.smem);
+      set_distances(c, bt, 1, c->boot_geo);
+    const double g1[2] = {0.5, 0.5};
+    {
+      const int bytes = (int)(sizeof(AxisTap) * bt.size());
+      c->boot_tap_off = arena_alloc(cfg->device, bytes);
+      if (c->boot_tap_off < 0) {
+        set_err(c, BSDE_ERR_RESOURCE_LIMIT, "constant tap arena full (bootstrap)");
+        return fail(BSDE_ERR_RESOURCE_LIMIT);
+      }
+      ce = upload_arena(bt.data(), bytes, c->boot_tap_off, c->stream);
+      if (ce == cudaSuccess && c->d == 1) {
+        std::vector<Tap1D> t1 = build_tap1d(bt, 1, c->L, 1, 1, g1, g1);
+        const int b1 = (int)(sizeof(Tap1D) * t1.size());
+        c->boot_tap1_off = arena_alloc(cfg->device, b1);
+        if (c->boot_tap1_off >= 0) ce = upload_arena(t1.data(), b1, c->boot_tap1_off, c->stream);
+      }
+      if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "taps: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
+    }
+    for (int m = N - 1; m >= N - K + 1; --m) {
+      for (int s = Sb - 1; s >= 0; --s) {
+        const double tn = cfg->t0 + m * c->dt + s * db;
+        const int slots[1] = {c->RS};                        // scratch slot
+        if ((st = run_step(c, 1, 1, 1, g1, g1, db, tn, slots, c->boot_tap_off, c->boot_tap1_off, c->boot_geo,
+                           cfg->kernel_variant)))
+          return fail(st);
+      }
+      if ((st = spline_into(c, m % c->RS))) return fail(st);
+      c->level = m;
+    }
+  } else {
+    for (int m = N - 1; m >= N - K + 1; --m) {
+      ce = launch_layer(c->pb, c->g, cfg->t0 + m * c->dt, false, c->vbuf[c->cur], c->stream);
+      ++c->launches;
+      if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "layer: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
+      if ((st = spline_into(c, m % c->RS))) return fail(st);
+      c->level = m;
+    }
+  }
+  ce = cudaMemsetAsync(c->picard, 0, sizeof(int32_t) * c->g.npts, c->stream);
+  if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "memset: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
+  (void)t_start;
+  *out = c;
+  return BSDE_OK;
+}
+
+bsde_status bsde_step(bsde_ctx* c) {
+  if (!c) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (c->level <= 0) return set_err(c, BSDE_ERR_STATE, "already at n = 0");
+  cudaSetDevice(c->cfg.device);
+  const int n = c->level - 1;
+  int slots[kMaxK];
+  for (int j = 1; j <= c->K; ++j) slots[j - 1] = (n + j) % c->RS;   // ring slot of level n+j
+  bsde_status st = run_step(c, c->K, c->Ky, c->Kz, c->gy, c->gz, c->dt, c->cfg.t0 + n * c->dt, slots, c->tap_off,
+                            c->tap1_off, c->geo, c->cfg.kernel_variant);
+  if (st) return st;
+  c->level = n;
+  return BSDE_OK;
+}
+
+static bsde_status check_bad(bsde_ctx* c) {
+  unsigned long long bad = 0;
+  cudaError_t e = cudaMemcpyAsync(&bad, c->bad, sizeof bad, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
+  if (bad != ~0ULL)
+    return set_err(c, BSDE_ERR_NUMERICAL_DOMAIN, "non-finite y or z at point %llu (level <= %d)", bad, c->level + 1);
+  return BSDE_OK;
+}
+
+bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
+  if (!c) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  cudaSetDevice(c->cfg.device);
+  const double t0 = now_s();
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+    return set_err(c, BSDE_ERR_CUDA, "event create");
+  cudaEventRecord(e0, c->stream);
+  int64_t steps = 0;
+  bsde_status st = BSDE_OK;
+  // d = 1 fused path: all remaining steps in one cooperative (persistent) launch
+  const bool fused = c->d == 1 && (c->cfg.kernel_variant == 0 || c->cfg.kernel_variant >= 10) && c->geo.ok &&
+                     c->tap1_off >= 0 && getenv("BSDE_NO_PERSISTENT") == nullptr;
+  if (fused && c->level >= 2) {
+    StepArgs s{};
+    s.ring = c->ring;
+    s.slot_elems = (int64_t)c->F * c->g.cfield;
+    s.K = c->K; s.Ky = c->Ky; s.Kz = c->Kz; s.L = c->L;
+    s.ring_slots = c->RS;
+    s.tap_off = c->tap_off;
+    s.tap1_off = c->tap1_off;
+    s.gz0 = c->gz[0];
+    s.ky_dt = c->Ky * c->dt;
+    s.ky_dt_gy0 = c->Ky * c->dt * c->gy[0];
+    s.picard_max = c->cfg.picard_max;
+    s.picard_tol = c->cfg.picard_tol;
+    s.picard = c->picard;
+    s.bad = c->bad;
+    s.phase_ns = c->phase_ns;
+    const int ns = c->level;
+    cudaError_t e = launch_fused1d_steps(s, c->g, c->pb, c->geo.fz, c->level - 1, ns, 1, c->cur, c->cfg.t0, c->dt, c->vbuf[0],
+                               c->vbuf[1], c->barrier, c->geo.D, c->geo.DK, c->geo.threads, c->geo.blocks,
+                               c->geo.smem, c->stream);
+    ++c->launches;
+    if (e != cudaSuccess) st = set_err(c, BSDE_ERR_CUDA, "persistent step kernel: %s", cudaGetErrorString(e));
+    else {
+      c->cur ^= (ns & 1);
+      c->level = 0;
+      steps = ns;
+    }
+  }
+  while (st == BSDE_OK && c->level > 0) {
+    if ((st = bsde_step(c))) break;
+    ++steps;
+  }
+  cudaEventRecord(e1, c->stream);
+  if (st) { cudaEventDestroy(e0); cudaEventDestroy(e1); return st; }
+  if ((st = check_bad(c))) { cudaEventDestroy(e0); cudaEventDestroy(e1); return st; }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (res) {
+    memset(res, 0, sizeof *res);
+    // evaluation point x = 0 (reading R4): grid value if 0 is a grid point, else the spline
+    bool on_grid = true;
+    int64_t idx = 0;
+    for (int a = 0; a < c->d; ++a) {
+      if (!(c->g.xlo[a] == -c->g.xhi[a] && (c->g.P[a] % 2) == 1)) on_grid = false;
+      idx += ((c->g.P[a] - 1) / 2) * c->g.vstride[a];
+    }
+    double out[4] = {0, 0, 0, 0};
+    if (on_grid) {
+      for (int f = 0; f < c->F; ++f) {
+        cudaError_t e = cudaMemcpyAsync(&out[f], c->vbuf[c->cur] + (int64_t)f * c->g.npts + idx, sizeof(double),
+                                        cudaMemcpyDeviceToHost, c->stream);
+        if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "read-back: %s", cudaGetErrorString(e));
+      }
+    } else {
+      const double x[3] = {0, 0, 0};
+      if ((st = spline_into(c, c->RS))) return st;              // newest level -> scratch slot
+      cudaError_t e = launch_eval(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, x, c->dres, c->stream);
+      ++c->launches;
+      if (e == cudaSuccess) e = cudaMemcpyAsync(out, c->dres, sizeof(double) * c->F, cudaMemcpyDeviceToHost, c->stream);
+      if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "eval: %s", cudaGetErrorString(e));
+    }
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
+    res->y0 = out[0];
+    for (int a = 0; a < c->d; ++a) res->z0[a] = out[1 + a];
+    res->t_sweep_s = ms * 1e-3;
+    res->t_total_s = now_s() - t0;
+    res->updates = c->g.npts * steps;
+    res->picard_max_used = c->cfg.picard_max;
+  }
+  return BSDE_OK;
+}
+
+bsde_status bsde_level(const bsde_ctx* c, int32_t* n_out) {
+  if (!c || !n_out) return BSDE_ERR_INVALID_ARGUMENT;
+  *n_out = c->level;
+  return BSDE_OK;
+}
+
+bsde_status bsde_get_layer(const bsde_ctx* cc, int32_t field, double* host_dst, int64_t count) {
+  bsde_ctx* c = const_cast<bsde_ctx*>(cc);
+  if (!c || !host_dst) return BSDE_ERR_INVALID_ARGUMENT;
+  if (field < 0 || field >= c->F) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "field %d outside 0..%d", field, c->F - 1);
+  if (count != c->g.npts) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "count %lld != %lld", (long long)count, (long long)c->g.npts);
+  cudaSetDevice(c->cfg.device);
+  CU(cudaMemcpyAsync(host_dst, c->vbuf[c->cur] + (int64_t)field * c->g.npts, sizeof(double) * count, cudaMemcpyDeviceToHost,
+                     c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return BSDE_OK;
+}
+
+bsde_status bsde_get_picard_counts(const bsde_ctx* cc, int32_t* host_dst, int64_t count) {
+  bsde_ctx* c = const_cast<bsde_ctx*>(cc);
+  if (!c || !host_dst) return BSDE_ERR_INVALID_ARGUMENT;
+  if (count != c->g.npts) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "count mismatch");
+  cudaSetDevice(c->cfg.device);
+  CU(cudaMemcpyAsync(host_dst, c->picard, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return BSDE_OK;
+}
+
+bsde_status bsde_query_grid(const bsde_ctx* c, int64_t npts[3], double dx[3]) {
+  if (!c) return BSDE_ERR_INVALID_ARGUMENT;
+  for (int a = 0; a < 3; ++a) {
+    npts[a] = a < c->d ? c->g.P[a] : 1;
+    dx[a] = a < c->d ? c->g.dx[a] : 0.0;
+  }
+  return BSDE_OK;
+}
+
+bsde_status bsde_query_taps(const bsde_ctx* cc, int32_t level, int32_t axis, int32_t* q, double* basis4, double* w,
+                            double* dw) {
+  bsde_ctx* c = const_cast<bsde_ctx*>(cc);
+  if (!c) return BSDE_ERR_INVALID_ARGUMENT;
+  if (level < 1 || level > c->K || axis < 0 || axis >= c->d)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "level %d / axis %d out of range", level, axis);
+  for (int l = 0; l < c->L; ++l) {
+    const AxisTap& t = c->taps[((size_t)(level - 1) * c->d + axis) * c->L + l];
+    if (q) q[l] = t.q;
+    if (basis4) for (int k = 0; k < 4; ++k) basis4[4 * l + k] = t.B[k];
+    if (w) w[l] = t.w;
+    if (dw) dw[l] = t.s;
+  }
+  return BSDE_OK;
+}
+
+bsde_status bsde_eval(bsde_ctx* c, const double* x, double* out) {
+  if (!c || !x || !out) return BSDE_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->cfg.device);
+  double xx[3] = {0, 0, 0};
+  for (int a = 0; a < c->d; ++a) xx[a] = x[a];
+  bsde_status st = spline_into(c, c->RS);                        // newest level -> scratch slot
+  if (st) return st;
+  CU(launch_eval(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, xx, c->dres, c->stream));
+  ++c->launches;
+  CU(cudaMemcpyAsync(out, c->dres, sizeof(double) * c->F, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return BSDE_OK;
+}
+
+bsde_status bsde_layer_device_ptr(const bsde_ctx* c, int32_t field, const double** dptr) {
+  if (!c || !dptr || field < 0 || field >= c->F) return BSDE_ERR_INVALID_ARGUMENT;
+  *dptr = c->vbuf[c->cur] + (int64_t)field * c->g.npts;
+  return BSDE_OK;
+}
+
+bsde_status bsde_kernel_launches(const bsde_ctx* c, int64_t* count) {
+  if (!c || !count) return BSDE_ERR_INVALID_ARGUMENT;
+  *count = c->launches;
+  return BSDE_OK;
+}
+
+// debug only (not in bsde.h): per-CTA phase stamps of the last fused step
+int bsde_internal_phase_times(const bsde_ctx* c, unsigned long long* host, int n) {
+  if (!c || !c->phase_ns) return 1;
+  cudaStreamSynchronize(c->stream);
+  return cudaMemcpy(host, c->phase_ns, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess;
+}
+
+const char* bsde_last_error(const bsde_ctx* c) { return c ? c->err.c_str() : g_setup_error.c_str(); }
+
+void bsde_destroy(bsde_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->cfg.device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  release(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,539 @@
+// kernels.cu -- sm_100a fp64 kernels of the multistep BSDE solver.
+//
+//   layer_kernel      terminal layer y^N = g, z^N = grad g (+ smoothing, R11)
+//                     and closed-form initial layers (R9)
+//   spline_pass       not-a-knot cubic spline -> B-spline coefficients along one axis,
+//                     batched constant-matrix tridiagonal solve by PCR in shared memory
+//                     ("two linear systems", north_star (1))
+//   quad_generic      fused Gauss-Hermite quadrature (Eq. 21) of spline-interpolated
+//                     values + z (Eq. 20 line 2) + Picard y (Eq. 20 line 1), any d
+//   quad1d_fused      d = 1: level-1 spline (PCR) + quadrature on shared-memory windows
+//                     streamed by cp.async.bulk + z + Picard, one kernel per step (cfg 2)
+//   eval_kernel       spline of the newest level at one point (the evaluation point)
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "bsde_internal.h"
+#include "problems.cuh"
+
+namespace bsde {
+
+// ------------------------------------------------------------------ constant arena
+// Byte arena of tap tables (AxisTap for the generic kernel, Tap1D for the fused 1-D
+// kernel); each context owns 16-byte aligned ranges (host.cu allocator).
+constexpr int kArenaBytes = 63 * 1024;
+__constant__ __align__(16) unsigned char c_arena[kArenaBytes];
+__constant__ double c_gl_x[kSmoothGL], c_gl_w[kSmoothGL];
+
+cudaError_t upload_arena(const void* data, int bytes, int offset, cudaStream_t st) {
+  if (offset < 0 || offset + bytes > kArenaBytes) return cudaErrorInvalidValue;
+  return cudaMemcpyToSymbolAsync(c_arena, data, bytes, offset, cudaMemcpyHostToDevice, st);
+}
+int arena_capacity_bytes() { return kArenaBytes; }
+__device__ __forceinline__ const AxisTap* axis_taps(int off) { return reinterpret_cast<const AxisTap*>(c_arena + off); }
+__device__ __forceinline__ const Tap1D* taps1d(int off) { return reinterpret_cast<const Tap1D*>(c_arena + off); }
+cudaError_t upload_gl(const double* x, const double* w, cudaStream_t st) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_gl_x, x, sizeof(double) * kSmoothGL, 0, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbolAsync(c_gl_w, w, sizeof(double) * kSmoothGL, 0, cudaMemcpyHostToDevice, st);
+}
+
+// ------------------------------------------------------------------ layers
+__device__ inline void grid_coords(const Grid& g, int64_t p, double* x) {
+  for (int a = g.d - 1; a >= 0; --a) {
+    const int64_t i = p % g.P[a];
+    p /= g.P[a];
+    x[a] = g.xlo[a] + (double)i * g.dx[a];
+  }
+}
+
+// cell average of g over prod [lo_a, hi_a], axis `fixed` pinned at lo (GL16 tensor rule)
+__device__ double smooth_box(const Problem& pb, const double* lo, const double* hi, int fixed) {
+  const int d = pb.d;
+  int n[kMaxD];
+  int tot = 1;
+  for (int a = 0; a < d; ++a) { n[a] = a == fixed ? 1 : kSmoothGL; tot *= n[a]; }
+  double acc = 0.0;
+  for (int m = 0; m < tot; ++m) {
+    int rem = m;
+    double w[kMaxD], wt = 1.0;
+    for (int a = d - 1; a >= 0; --a) {
+      const int k = rem % n[a];
+      rem /= n[a];
+      if (a == fixed) w[a] = lo[a];
+      else {
+        w[a] = 0.5 * (lo[a] + hi[a]) + 0.5 * (hi[a] - lo[a]) * c_gl_x[k];
+        wt *= 0.5 * c_gl_w[k];
+      }
+    }
+    double y, z[kMaxD];
+    terminal_eval(pb, w, y, z);
+    acc += wt * y;
+  }
+  return acc;
+}
+
+__global__ void layer_kernel(Problem pb, Grid g, double t, int terminal, double* values) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= g.npts) return;
+  const int d = g.d;
+  double x[kMaxD], y, z[kMaxD];
+  grid_coords(g, p, x);
+  if (terminal) {
+    terminal_eval(pb, x, y, z);
+    const int kinked = pb.terminal_id == TRM_CALL || pb.terminal_id == TRM_EXCHANGE || pb.terminal_id == TRM_GEO;
+    if (pb.smoothing && kinked) {
+      int pos = 0, neg = 0;
+      for (int m = 0; m < (1 << d); ++m) {
+        double c[kMaxD];
+        for (int a = 0; a < d; ++a) c[a] = x[a] + (((m >> a) & 1) ? 0.5 : -0.5) * g.dx[a];
+        const double v = payoff_argument(pb, c);
+        if (v > 0.0) pos = 1;
+        else if (v < 0.0) neg = 1;
+        else { pos = 1; neg = 1; }
+      }
+      if (pos && neg) {
+        if (d == 1 && pb.terminal_id == TRM_CALL) {
+          // closed-form average of (S0 e^{a + s w} - K)^+ over the cell
+          const double* q = pb.tp;
+          const double a = (q[2] - 0.5 * q[3] * q[3]) * pb.T, s = q[3];
+          const double lo = x[0] - 0.5 * g.dx[0], hi = x[0] + 0.5 * g.dx[0];
+          const double wk = (log(q[1] / q[0]) - a) / s;
+          const double l = lo > wk ? lo : wk;
+          y = hi <= wk ? 0.0 : (q[0] * exp(a) * (exp(s * hi) - exp(s * l)) / s - q[1] * (hi - l)) / (hi - lo);
+          double yp, ym, zz[kMaxD];
+          double wp = hi, wm = lo;
+          terminal_eval(pb, &wp, yp, zz);
+          terminal_eval(pb, &wm, ym, zz);
+          z[0] = (yp - ym) / g.dx[0];
+        } else {
+          double lo[kMaxD], hi[kMaxD];
+          for (int a = 0; a < d; ++a) { lo[a] = x[a] - 0.5 * g.dx[a]; hi[a] = x[a] + 0.5 * g.dx[a]; }
+          y = smooth_box(pb, lo, hi, -1);
+          for (int a = 0; a < d; ++a) {
+            double lo2[kMaxD], hi2[kMaxD];
+            for (int b = 0; b < d; ++b) { lo2[b] = lo[b]; hi2[b] = hi[b]; }
+            lo2[a] = hi[a];
+            const double up = smooth_box(pb, lo2, hi2, a);
+            lo2[a] = lo[a];
+            const double dn = smooth_box(pb, lo2, hi2, a);
+            z[a] = (up - dn) / g.dx[a];
+          }
+        }
+      }
+    }
+  } else {
+    exact_eval(pb, t, x, y, z);
+  }
+  values[p] = y;
+  for (int a = 0; a < d; ++a) values[(int64_t)(1 + a) * g.npts + p] = z[a];
+}
+
+cudaError_t launch_layer(const Problem& pb, const Grid& g, double t, bool terminal, double* values, cudaStream_t st) {
+  const int T = 256;
+  const int64_t nb = (g.npts + T - 1) / T;
+  layer_kernel<<<(unsigned)nb, T, 0, st>>>(pb, g, t, terminal ? 1 : 0, values);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ spline pass (PCR)
+struct PassArgs {
+  const double* src;   // value index 0 of batch (0,0)
+  double* dst;         // storage index 0 (k = -1) of batch (0,0)
+  int64_t P;           // line length
+  int64_t s_line, d_line;
+  int64_t nb0, nb1;    // batch extents (nb1 inner)
+  int64_t s_b0, s_b1, d_b0, d_b1;
+  int32_t TS;          // outputs per tile
+  double alpha[kPcrLevels];
+  double inv_b;
+};
+
+// odd periodic extension of the reduced right-hand side about nodes 1 and P-2
+// (Dirichlet nodes after m_1 and m_{P-2} are known): exact by the method of images.
+__device__ inline double rhs_tilde(const double* F, int64_t sl, int64_t P, int64_t k, double m1, double mP2) {
+  const int64_t period = 2 * (P - 3);
+  int64_t u = (k - 1) % period;
+  if (u < 0) u += period;
+  if (u == 0 || u == P - 3) return 0.0;
+  int64_t i;
+  double sgn;
+  if (u < P - 3) { i = 1 + u; sgn = 1.0; }
+  else { i = 1 + period - u; sgn = -1.0; }
+  double r = 6.0 * (F[(i - 1) * sl] - 2.0 * F[i * sl] + F[(i + 1) * sl]);
+  if (i == 2) r -= m1;
+  if (i == P - 3) r -= mP2;
+  return sgn * r;
+}
+
+template <bool STRIDED>
+__global__ void spline_pass(PassArgs a) {
+  extern __shared__ double sm[];
+  const int H = kPcrHalo;
+  int lane, worker, nworkers, nlanes;
+  int64_t b1;
+  bool valid;
+  if (STRIDED) {
+    lane = threadIdx.x; worker = threadIdx.y; nworkers = blockDim.y; nlanes = 32;
+    b1 = (int64_t)blockIdx.y * 32 + lane;
+    valid = b1 < a.nb1;
+  } else {
+    lane = 0; worker = threadIdx.x; nworkers = blockDim.x; nlanes = 1;
+    b1 = blockIdx.y;
+    valid = true;
+  }
+  const int64_t b0 = blockIdx.z;
+  const int64_t P = a.P;
+  const double* F = a.src + b0 * a.s_b0 + (valid ? b1 : 0) * a.s_b1;
+  double* out = a.dst + b0 * a.d_b0 + (valid ? b1 : 0) * a.d_b1;
+  const int64_t sl = a.s_line;
+  const int64_t k0 = -1 + (int64_t)blockIdx.x * a.TS;
+  const int64_t k1 = min(k0 + (int64_t)a.TS, P + 1);
+  const int64_t base = k0 - 3 - H;
+  const int W = a.TS + 6 + 2 * H;
+  double* A = sm;
+  double* B = sm + (size_t)W * nlanes;
+  double m1 = 0.0, mP2 = 0.0;
+  if (valid) {
+    m1 = F[0] - 2.0 * F[sl] + F[2 * sl];
+    mP2 = F[(P - 3) * sl] - 2.0 * F[(P - 2) * sl] + F[(P - 1) * sl];
+  }
+  for (int p = worker; p < W; p += nworkers)
+    A[p * nlanes + lane] = valid ? rhs_tilde(F, sl, P, base + p, m1, mP2) : 0.0;
+  __syncthreads();
+  // constant-coefficient PCR on the (1,4,1) system: r_i <- r_i - (a/b)(r_{i-s} + r_{i+s})
+#pragma unroll
+  for (int l = 0; l < kPcrLevels; ++l) {
+    const int s = 1 << l;
+    const double al = a.alpha[l];
+    for (int p = worker; p < W; p += nworkers) {
+      const double lft = p - s >= 0 ? A[(p - s) * nlanes + lane] : 0.0;
+      const double rgt = p + s < W ? A[(p + s) * nlanes + lane] : 0.0;
+      B[p * nlanes + lane] = A[p * nlanes + lane] - al * (lft + rgt);
+    }
+    __syncthreads();
+    double* t = A; A = B; B = t;
+  }
+  if (!valid) return;
+  const double ib = a.inv_b;
+  auto mt = [&](int64_t k) { return A[(k - base) * nlanes + lane] * ib; };
+  auto mk = [&](int64_t k) -> double {
+    if (k == 1) return m1;
+    if (k == P - 2) return mP2;
+    if (k == 0) return 2.0 * m1 - (P - 2 == 2 ? mP2 : mt(2));
+    if (k == P - 1) return 2.0 * mP2 - (P - 3 == 1 ? m1 : mt(P - 3));
+    return mt(k);
+  };
+  for (int64_t k = k0 + worker; k < k1; k += nworkers) {
+    double c;
+    if (k >= 0 && k < P) c = F[k * sl] - mk(k) * (1.0 / 6.0);
+    else if (k < 0) {
+      const double c0 = F[0] - mk(0) * (1.0 / 6.0), c1 = F[sl] - m1 * (1.0 / 6.0);
+      c = 6.0 * F[0] - 4.0 * c0 - c1;
+    } else {
+      const double cl = F[(P - 1) * sl] - mk(P - 1) * (1.0 / 6.0), cm = F[(P - 2) * sl] - mP2 * (1.0 / 6.0);
+      c = 6.0 * F[(P - 1) * sl] - 4.0 * cl - cm;
+    }
+    out[(k + 1) * a.d_line] = c;
+  }
+}
+
+// PCR constants of the infinite (1,4,1) Toeplitz system, long double on the host
+void pcr_constants(double* alpha, double* inv_b) {
+  long double av = 1.0L, bv = 4.0L;
+  for (int l = 0; l < kPcrLevels; ++l) {
+    alpha[l] = (double)(av / bv);
+    const long double an = -av * av / bv, bn = bv - 2.0L * av * av / bv;
+    av = an; bv = bn;
+  }
+  *inv_b = (double)(1.0L / bv);
+}
+
+static cudaError_t run_pass(PassArgs pa, bool strided, cudaStream_t st, int64_t* launches) {
+  const int H = kPcrHalo;
+  pcr_constants(pa.alpha, &pa.inv_b);
+  if (strided) {
+    pa.TS = 64;
+    const int W = pa.TS + 6 + 2 * H;
+    const size_t smem = (size_t)W * 32 * 2 * sizeof(double);
+    dim3 grid((unsigned)((pa.P + 2 + pa.TS - 1) / pa.TS), (unsigned)((pa.nb1 + 31) / 32), (unsigned)pa.nb0);
+    spline_pass<true><<<grid, dim3(32, 8), smem, st>>>(pa);
+  } else {
+    pa.TS = pa.P + 2 <= 4096 ? (int)(pa.P + 2) : 1024;
+    if (pa.P + 2 > 4096 && pa.nb0 * pa.nb1 == 1) pa.TS = 512;   // one long line: spread over SMs
+    const int W = pa.TS + 6 + 2 * H;
+    const size_t smem = (size_t)W * 2 * sizeof(double);
+    dim3 grid((unsigned)((pa.P + 2 + pa.TS - 1) / pa.TS), (unsigned)pa.nb1, (unsigned)pa.nb0);
+    spline_pass<false><<<grid, 256, smem, st>>>(pa);
+  }
+  ++*launches;
+  return cudaGetLastError();
+}
+
+// Tensor-product spline of F fields of `values` (value layout) into a ring slot
+// (coefficient layout): pass along axis 0, then 1, ....
+cudaError_t launch_spline(const Grid& g, const double* values, int F, double* slot, double* tmp0, double* tmp1,
+                          cudaStream_t st, int64_t* launches) {
+  const int d = g.d;
+  for (int f = 0; f < F; ++f) {
+    const double* vsrc = values + (int64_t)f * g.npts;
+    double* cdst = slot + (int64_t)f * g.cfield;
+    const double* src = vsrc;
+    bool src_is_values = true;
+    for (int ax = 0; ax < d; ++ax) {
+      double* dst = (ax == d - 1) ? cdst : (ax % 2 == 0 ? tmp0 : tmp1);
+      PassArgs pa{};
+      pa.P = g.P[ax];
+      // batch axes: all axes except ax, at most two; the last remaining one is "inner"
+      int bax[2], nbx = 0;
+      for (int b = 0; b < d; ++b) if (b != ax) bax[nbx++] = b;
+      int64_t n[2] = {1, 1}, ss[2] = {0, 0}, ds[2] = {0, 0};
+      int64_t soff = 0, doff = 0;
+      for (int t = 0; t < nbx; ++t) {
+        const int b = bax[t];
+        const bool done = b < ax;                 // already spline-transformed -> ghosts included
+        n[t] = done ? g.P[b] + 2 : g.P[b];
+        ss[t] = src_is_values ? g.vstride[b] : g.cstride[b];
+        ds[t] = g.cstride[b];
+        if (!done) {
+          if (!src_is_values) soff += g.cstride[b];   // value index 0 -> storage index 1
+          doff += g.cstride[b];
+        }
+      }
+      // line axis offsets: source value index 0 (storage 1 in coefficient layout)
+      if (!src_is_values) soff += g.cstride[ax];
+      pa.src = src + soff;
+      pa.dst = dst + doff;
+      pa.s_line = src_is_values ? g.vstride[ax] : g.cstride[ax];
+      pa.d_line = g.cstride[ax];
+      if (nbx == 0) { pa.nb0 = 1; pa.nb1 = 1; }
+      else if (nbx == 1) { pa.nb0 = 1; pa.nb1 = n[0]; pa.s_b1 = ss[0]; pa.d_b1 = ds[0]; }
+      else { pa.nb0 = n[0]; pa.s_b0 = ss[0]; pa.d_b0 = ds[0]; pa.nb1 = n[1]; pa.s_b1 = ss[1]; pa.d_b1 = ds[1]; }
+      const bool strided = ax != d - 1;
+      cudaError_t e = run_pass(pa, strided, st, launches);
+      if (e != cudaSuccess) return e;
+      src = dst;
+      src_is_values = false;
+    }
+  }
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ interpolation helpers
+// per-axis cell and basis with boundary clamping (R6):
+// outside the box the coordinate is clamped, i.e. the spline is evaluated at the
+// boundary knot: cell 0 / P-1 with theta = 0 -> B = (1/6, 2/3, 1/6, 0).
+__device__ inline int64_t clamp_cell(int64_t c, int64_t P, const double* Bin, double* B) {
+  if (c < 0 || c >= P - 1) {
+    B[0] = 1.0 / 6.0; B[1] = 2.0 / 3.0; B[2] = 1.0 / 6.0; B[3] = 0.0;
+    return c < 0 ? 0 : P - 1;
+  }
+  B[0] = Bin[0]; B[1] = Bin[1]; B[2] = Bin[2]; B[3] = Bin[3];
+  return c;
+}
+
+template <int D>
+__device__ inline double gather(const double* __restrict__ C, const int64_t* cs, const int64_t* cell,
+                                const double (*B)[4]) {
+  if (D == 1) {
+    const double* c = C + cell[0];
+    return B[0][0] * __ldg(c) + B[0][1] * __ldg(c + 1) + B[0][2] * __ldg(c + 2) + B[0][3] * __ldg(c + 3);
+  } else if (D == 2) {
+    double v = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < 4; ++k0) {
+      const double* c = C + (cell[0] + k0) * cs[0] + cell[1];
+      const double row = B[1][0] * __ldg(c) + B[1][1] * __ldg(c + 1) + B[1][2] * __ldg(c + 2) + B[1][3] * __ldg(c + 3);
+      v = fma(B[0][k0], row, v);
+    }
+    return v;
+  } else {
+    double v = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < 4; ++k0) {
+      double pl = 0.0;
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) {
+        const double* c = C + (cell[0] + k0) * cs[0] + (cell[1] + k1) * cs[1] + cell[2];
+        const double row = B[2][0] * __ldg(c) + B[2][1] * __ldg(c + 1) + B[2][2] * __ldg(c + 2) + B[2][3] * __ldg(c + 3);
+        pl = fma(B[1][k1], row, pl);
+      }
+      v = fma(B[0][k0], pl, v);
+    }
+    return v;
+  }
+}
+
+// Epilogue shared by all quadrature kernels: z (Eq. 20 line 2, explicit) then y by
+// Picard iteration on Eq. 20 line 1 starting from E[y^{n+Ky}] (R8, R18).
+template <int DRV, int D>
+__device__ inline void epilogue(const StepArgs& s, int64_t p, int64_t npts, double Ay, double Af, const double* Az,
+                                const double* dp) {
+  Driver<DRV, D> drv(dp);
+  drv.at(s.tn);
+  double z[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) z[a] = Az[a] / s.gz0;
+  const double rhs = fma(s.ky_dt, Af, Ay);
+  double y = Ay;
+  int it;
+  for (it = 1; it <= s.picard_max; ++it) {
+    const double yn = fma(s.ky_dt_gy0, drv(y, z), rhs);
+    const double dy = fabs(yn - y);
+    const bool fixed = (yn == y);    // exact fixed point: the remaining iterations are identities
+    y = yn;
+    if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
+    if (fixed) { it = s.picard_max; break; }
+  }
+  if (it > s.picard_max) it = s.picard_max;
+  s.values[p] = y;
+  bool bad = !isfinite(y);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    s.values[(int64_t)(1 + a) * npts + p] = z[a];
+    bad |= !isfinite(z[a]);
+  }
+  s.picard[p] = it;
+  if (bad) atomicMin(s.bad, (unsigned long long)p);
+}
+
+// ------------------------------------------------------------------ generic fused kernel
+// One thread per grid point; for level j and node tuple Lambda the tap is the
+// translation-invariant stencil (q_Lambda, theta_Lambda) of PAPER.md:391-392.
+template <int D, int DRV>
+__global__ void __launch_bounds__(256) quad_generic(StepArgs s, Grid g, Problem pb) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= g.npts) return;
+  int64_t idx[D];
+  {
+    int64_t r = p;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) { idx[a] = r % g.P[a]; r /= g.P[a]; }
+  }
+  Driver<DRV, D> drv(pb.dp);
+  const int L = s.L;
+  double Az[D], Af = 0.0, Ay = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) Az[a] = 0.0;
+  int ntap = 1;
+#pragma unroll
+  for (int a = 0; a < D; ++a) ntap *= L;
+  for (int j = 1; j <= s.K; ++j) {
+    drv.at(s.t_level[j - 1]);
+    const double* C = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
+    const double czj = s.czj[j - 1], gzj = s.gzj[j - 1], gyj = s.gyj[j - 1];
+    const bool yj = (j == s.Ky);
+    const AxisTap* tj = axis_taps(s.tap_off) + (j - 1) * D * L;
+    for (int tap = 0; tap < ntap; ++tap) {
+      int lam[D];
+      {
+        int r = tap;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) { lam[a] = r % L; r /= L; }
+      }
+      int64_t cell[D];
+      double B[D][4];
+      double w = 1.0, sa[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const AxisTap& t = tj[a * L + lam[a]];
+        cell[a] = clamp_cell(idx[a] + t.q, g.P[a], t.B, B[a]);
+        w *= t.w;
+        sa[a] = t.s;
+      }
+      const double yh = gather<D>(C, g.cstride, cell, B);
+      double zh[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) zh[a] = gather<D>(C + (int64_t)(1 + a) * g.cfield, g.cstride, cell, B);
+      const double f = drv(yh, zh);
+      const double wf = w * f;
+#pragma unroll
+      for (int a = 0; a < D; ++a) Az[a] += w * czj * zh[a] + gzj * sa[a] * wf;
+      Af = fma(gyj, wf, Af);
+      if (yj) Ay = fma(w, yh, Ay);
+    }
+  }
+  epilogue<DRV, D>(s, p, g.npts, Ay, Af, Az, pb.dp);
+}
+
+// ------------------------------------------------------------------ 1-D fused step kernel
+#include "fused1d.cuh"
+
+template <int D, int DRV>
+static cudaError_t launch_generic(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st) {
+  const int T = 256;
+  const int64_t nb = (g.npts + T - 1) / T;
+  quad_generic<D, DRV><<<(unsigned)nb, T, 0, st>>>(s, g, pb);
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t dispatch_generic(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st) {
+  switch (pb.driver_id) {
+    case DRV_ZERO: return launch_generic<D, DRV_ZERO>(s, g, pb, st);
+    case DRV_AFFINE: return launch_generic<D, DRV_AFFINE>(s, g, pb, st);
+    case DRV_EX1: return launch_generic<D, DRV_EX1>(s, g, pb, st);
+    case DRV_EX2: return launch_generic<D, DRV_EX2>(s, g, pb, st);
+    case DRV_DIFF: return launch_generic<D, DRV_DIFF>(s, g, pb, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// generic fused quadrature kernel (any d); the spline of level n+1 is built by
+// launch_spline before it
+cudaError_t launch_generic_step(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st) {
+  switch (g.d) {
+    case 1: return dispatch_generic<1>(s, g, pb, st);
+    case 2: return dispatch_generic<2>(s, g, pb, st);
+    case 3: return dispatch_generic<3>(s, g, pb, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// opt in to > 48 KB dynamic shared memory on the current device (called per context)
+cudaError_t init_device_attributes() {
+  const int lim = 200 * 1024;
+  cudaError_t e = cudaFuncSetAttribute(spline_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  if (e == cudaSuccess) e = set_attr_drv<DRV_ZERO>();
+  if (e == cudaSuccess) e = set_attr_drv<DRV_AFFINE>();
+  if (e == cudaSuccess) e = set_attr_drv<DRV_EX1>();
+  if (e == cudaSuccess) e = set_attr_drv<DRV_EX2>();
+  if (e == cudaSuccess) e = set_attr_drv<DRV_DIFF>();
+  return e;
+}
+
+// ------------------------------------------------------------------ evaluation point
+__global__ void eval_kernel(Grid g, const double* slot, int F, double x0, double x1, double x2, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double x[3] = {x0, x1, x2};
+  int64_t cell[kMaxD];
+  double B[kMaxD][4];
+  for (int a = 0; a < g.d; ++a) {
+    double X = fmin(fmax(x[a], g.xlo[a]), g.xhi[a]);
+    const double u = (X - g.xlo[a]) / g.dx[a];
+    int64_t c = (int64_t)floor(u);
+    if (c > g.P[a] - 2) c = g.P[a] - 2;
+    if (c < 0) c = 0;
+    const double t = u - (double)c;
+    B[a][0] = (1.0 - t) * (1.0 - t) * (1.0 - t) / 6.0;
+    B[a][1] = (3.0 * t * t * t - 6.0 * t * t + 4.0) / 6.0;
+    B[a][2] = (-3.0 * t * t * t + 3.0 * t * t + 3.0 * t + 1.0) / 6.0;
+    B[a][3] = t * t * t / 6.0;
+    cell[a] = c;
+  }
+  for (int f = 0; f < F; ++f) {
+    const double* C = slot + (int64_t)f * g.cfield;
+    double v = 0.0;
+    if (g.d == 1) v = gather<1>(C, g.cstride, cell, B);
+    else if (g.d == 2) v = gather<2>(C, g.cstride, cell, B);
+    else v = gather<3>(C, g.cstride, cell, B);
+    out[f] = v;
+  }
+}
+
+cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st) {
+  eval_kernel<<<1, 32, 0, st>>>(g, slot, F, x[0], g.d > 1 ? x[1] : 0.0, g.d > 2 ? x[2] : 0.0, out);
+  return cudaGetLastError();
+}
+
+}  // namespace bsde

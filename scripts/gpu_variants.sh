@@ -1,0 +1,2 @@
+python scripts/variants.py 6 2>&1
+timeout 900 python -m pytest tests/ -m gpu -q -x 2>&1 | tail -5
