@@ -121,7 +121,7 @@ def run_ours(args):
     ws = {K: torch.empty(query_workspace(specs[K]), dtype=torch.uint8, device="cuda") for K in KS}
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    k6 = [0.0, 0]
+    k6 = [0.0, 0, 0]
 
     def one_step(timed=True):
         tot, upd, launches, y0 = 0.0, 0, 0, {}
@@ -136,6 +136,7 @@ def run_ours(args):
             if K == 6 and timed:
                 k6[0] += r.t_sweep_s
                 k6[1] += r.updates // 65536
+                k6[2] += 1
             launches += s.kernel_launches - n0
             y0[K] = (r.y0, r.z0[0])
             s.close()
@@ -160,19 +161,28 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         elapsed = float(tt.item())
     value = upds * world / elapsed
-    k6_time, k6_launches = k6
 
-    # ---- average launch duration of the dominant kernel (quad1d_fused, K = 6): the sweep is
-    # one kernel per step back to back, so the CUDA-event time of the K = 6 sweeps of the
-    # timed region divided by their launches (gaps included, so a lower bound on the rate)
-    launch_s = k6_time / k6_launches
-    fl = flops_per_point_step(6) * 65536
+    # ---- the dominant kernel is quad1d_fused: one persistent launch per sweep (all N-K+1
+    # steps).  Its average launch duration is the CUDA-event time of the K = 6 sweeps of the
+    # timed region (recorded on `stream` inside bsde_solve) divided by their number.
+    k6_time, k6_steps, k6_sweeps = k6
+    launch_s = k6_time / k6_sweeps
+    fl = flops_per_point_step(6) * 65536 * (k6_steps // k6_sweeps)
     clocks = clk.summary()
     peak = peak_fp64_tflops(1965.0)
     achieved = fl / launch_s / 1e12
+    traffic = None
+    try:   # dram__bytes_read.sum + dram__bytes_write.sum (MB) per launch, from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "round1", "ncu_quad1d_fused_K6_summary.json")) as fh:
+            prof = json.load(fh)
+        traffic = (float(prof["dram__bytes_read.sum"]) + float(prof["dram__bytes_write.sum"])) * 1e6
+    except (OSError, KeyError, ValueError):
+        pass
     roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "quad1d_fused<DRV_DIFF> (K=6)", "flops_per_launch": fl, "launch_us": round(launch_s * 1e6, 3),
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_note": "DRAM bytes per launch (one 251-step sweep; state is L2-resident) from ncu --set full",
+            "kernel": "quad1d_fused<DRV_DIFF> (K=6, one launch = one 251-step sweep)", "flops_per_launch": fl,
+            "launch_us": round(launch_s * 1e6, 3),
             "peak_note": "FP64 pipe: 148 SM x 64 DFMA/clk x 2 x 1965 MHz (derived; DESIGN.md Roofline)"}
 
     # ---- e2e: setup (host config -> device) + sweep + final layers device -> host, host clock

@@ -72,6 +72,14 @@ __device__ __forceinline__ void level_window(int qmin, int qmax, int64_t lo, int
   nwin = (int)(chi - clo + 4);
 }
 
+// span [wv, we] (storage indices, wv even) of the window of a level whose node offsets
+// are [qmin, qmax], for the tile [lo, hi): cells lo+qmin .. hi-1+qmax, 4 coefficients each
+__device__ __forceinline__ void level_span(int qmin, int qmax, int lo, int hi, int& wv, int& we) {
+  const int a = lo + qmin;
+  wv = a - (a & 1);
+  we = hi - 1 + qmax + 3;
+}
+
 // Launch parameters of the fused kernel.  All CTAs of a launch are co-resident
 // (cooperative launch); CTAs synchronise only with the neighbours they exchange data
 // with, through per-CTA progress flags:
@@ -114,8 +122,8 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
   const int WM = fz.WMAX, WP = fz.WP;
   double* const buf0 = reinterpret_cast<double*>(smem_raw + 128);
   double* const buf1 = buf0 + 2 * WM;
-  double* const Fs = buf1 + 2 * WM;                 // 2 x (WP + 4): values of the tile + PCR halo
-  double* const T0 = Fs + 2 * (WP + 4);             // 2 x WP
+  double* const Fs = buf1 + 2 * WM;                 // 2 x (WP + 8): values of the tile + PCR halo
+  double* const T0 = Fs + 2 * (WP + 8);             // 2 x WP
   double* const T1 = T0 + 2 * WP;                   // 2 x WP
   constexpr int NWPG = NT / (32 * C);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -136,7 +144,6 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
   const int k0 = lo == 0 ? -1 : lo, k1 = hi == P ? P + 1 : hi;
   const int base = k0 - 4 - H;
   const int Wa = (k1 - k0) + 8 + 2 * H;
-  const bool fastA = base >= 2 && base + Wa - 1 <= P - 3;        // no end rows in the PCR window
 
   int it_stamp = 0;
   PHASE_STAMP(0);
@@ -182,21 +189,18 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
       if (j == 1) wait_neighbours_warp(pp.ring_flag, bid, pp.D[1], nb, (unsigned)it + 1);
       if (lane != 0) return;
       const Tap1D* tj = tap0 + (j - 1) * L;
-      int64_t clo;
-      int nwin;
-      level_window(tj[0].q, tj[L - 1].q, lo, hi, P, clo, nwin);
-      const int64_t s0 = clo & ~(int64_t)1;
-      const int64_t s1 = (clo + nwin + 1) & ~(int64_t)1;
+      int wv, we;
+      level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
+      // real part [s0, s1) of the window (storage 0..P+2), even-aligned for the bulk copy
+      const int s0 = max(wv, 0);
+      const int s1 = (min(we, P + 2) + 2) & ~1;
       const uint32_t bytes = (uint32_t)((s1 - s0) * sizeof(double));
       const double* Cf = s.ring + (int64_t)slot[j - 1] * s.slot_elems;
-      double* dst = b ? buf1 : buf0;
+      double* dst = (b ? buf1 : buf0) + (s0 - wv);
       mbar_expect_tx(&bar[b], 2 * bytes);
       bulk_g2s(dst, Cf + s0, bytes, &bar[b]);
       bulk_g2s(dst + WM, Cf + g.cfield + s0, bytes, &bar[b]);
     };
-    // Levels are processed K, K-1, ..., 2, then 1: levels >= 2 only need ring slots written
-    // in earlier steps, so they run before this step's spline (phase A) and hide the wait
-    // for the neighbours' level-(n+1) values; level j uses buffer (K - j) & 1.
     // Slots of levels n+2..n+K were written in phase A of earlier steps by CTAs up to DK
     // away: their ring flags of step it-1 cover all of them.
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -212,30 +216,48 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
     double Az[R], Af[R], Ay[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) { Az[r] = 0.0; Af[r] = 0.0; Ay[r] = 0.0; }
-    // one level of taps on the window in buffer b
+    // one level of taps on the window in buffer b.  The window spans storage indices
+    // [wv, we] (wv even); entries outside the real range [0, P+2] are filled with the
+    // clamped boundary values F_0 / F_{P-1}, so every tap uses the same
+    // 4-term B-spline stencil; the cells whose stencil straddles the boundary
+    // ([-3, -1] and [P-1, P+2]) are clamped cells and get the boundary value directly.
     auto level = [&](int j, int b) {
       const Tap1D* tj = tap0 + (j - 1) * L;
-      int wbase, nwin;
-      {
-        int64_t clo;
-        level_window(tj[0].q, tj[L - 1].q, lo, hi, P, clo, nwin);
-        wbase = (int)(clo & ~(int64_t)1);
-        nwin += (int)clo - wbase;
-      }
+      int wv, we;
+      level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
       mbar_wait(&bar[b], ph[b]);
       ph[b] ^= 1u;
-      const double* const wy = b ? buf1 : buf0;
-      const double* const wz = wy + WM;
+      double* const wy = b ? buf1 : buf0;
+      double* const wz = wy + WM;
+      // clamped boundary values: s(x_0) = (c_{-1} + 4 c_0 + c_1)/6, s(x_{P-1}) likewise
+      double fy0 = 0, fz0 = 0, fy1 = 0, fz1 = 0;
+      const bool left = wv < 0, right = we > P + 2;
+      if (left || right) {                      // edge CTAs only (CTA-uniform)
+        if (left) {
+          const double* cy = wy - wv;
+          const double* cz = wz - wv;
+          fy0 = (1.0 / 6.0) * cy[0] + (2.0 / 3.0) * cy[1] + (1.0 / 6.0) * cy[2];
+          fz0 = (1.0 / 6.0) * cz[0] + (2.0 / 3.0) * cz[1] + (1.0 / 6.0) * cz[2];
+          for (int k = tid; k < -wv; k += NT) { wy[k] = fy0; wz[k] = fz0; }
+        }
+        if (right) {
+          const double* cy = wy + (P - 1 - wv);
+          const double* cz = wz + (P - 1 - wv);
+          fy1 = (1.0 / 6.0) * cy[0] + (2.0 / 3.0) * cy[1] + (1.0 / 6.0) * cy[2];
+          fz1 = (1.0 / 6.0) * cz[0] + (2.0 / 3.0) * cz[1] + (1.0 / 6.0) * cz[2];
+          for (int k = P + 3 - wv + tid; k <= we - wv; k += NT) { wy[k] = fy1; wz[k] = fz1; }
+        }
+        __syncthreads();
+      }
       drv.at(tlev[j - 1]);
       const bool yj = (j == s.Ky);
-      const int rel0 = lo - wbase + li0;               // lane's first cell relative to the window (q = 0)
-      // taps whose cells stay inside [0, P-2] for the whole tile (q ascending in lambda)
-      const int qlo = -lo, qhi = P - 2 - tile_last;
+      const int cl0 = lo + li0;                      // lane's first point
+      const int rel0 = cl0 - wv;                     // ... relative to the window (q = 0)
       for (int l = chunk; l < L; l += C) {
         const Tap1D& t = tj[l];
         const int q = t.q;
         double yh[R], zh[R];
-        if (q >= qlo && q <= qhi) {
+        {
           const double* py = wy + (rel0 + q);
           const double* pz = wz + (rel0 + q);
           double c[R + 3];
@@ -249,18 +271,17 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
 #pragma unroll
           for (int r = 0; r < R; ++r)
             zh[r] = fma(t.B[0], c[r], fma(t.B[1], c[r + 1], fma(t.B[2], c[r + 2], t.B[3] * c[r + 3])));
-        } else {
-          if (!active) continue;
+        }
+        const int cb = cl0 + q, ce = cb + R - 1;     // lane's cells
+        if ((left && cb <= -1 && ce >= -3) || (right && cb <= P + 2 && ce >= P - 1)) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            double Bc[4];
-            const int cell = lo + li0 + r + q;
-            int cc = (int)clamp_cell(cell, P, t.B, Bc) - wbase;
-            cc = cc < 0 ? 0 : (cc > nwin - 4 ? nwin - 4 : cc);      // lanes past the grid end
-            yh[r] = fma(Bc[0], wy[cc], fma(Bc[1], wy[cc + 1], fma(Bc[2], wy[cc + 2], Bc[3] * wy[cc + 3])));
-            zh[r] = fma(Bc[0], wz[cc], fma(Bc[1], wz[cc + 1], fma(Bc[2], wz[cc + 2], Bc[3] * wz[cc + 3])));
+            const int cell = cb + r;
+            if (cell >= -3 && cell <= -1) { yh[r] = fy0; zh[r] = fz0; }
+            if (cell >= P - 1 && cell <= P + 2) { yh[r] = fy1; zh[r] = fz1; }
           }
         }
+        if (!active) continue;
         const double wcz = t.wcz, wgz = t.wgz, wgy = t.wgy;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -298,41 +319,52 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
       if (it > 2) wait_neighbours_warp(pp.done_flag, bid, pp.DK, nb, (unsigned)(it - 2));
     }
     __syncthreads();
-    const int off0 = (base - 1) & 1;
-    const int off1 = (int)(((int64_t)P + base - 1) & 1);
-    if (tid == 0 && fastA) {
-      const uint32_t n0b = (uint32_t)((((Wa + 2 + off0) + 1) & ~1) * sizeof(double));
-      const uint32_t n1b = (uint32_t)((((Wa + 2 + off1) + 1) & ~1) * sizeof(double));
+    // values window [va, vb] of both fields (clamped to the grid); when the grid is long
+    // enough (smemA) every folded index of the odd extension lands inside it
+    const int va = max(base - 3, 0), vb = min(base + Wa + 2, P - 1);
+    const bool smemA = P >= Wa + 2 * kPcrHalo + 96;
+    const int va0 = va & ~1;                                   // field 0 start, even
+    const int va1 = (int)((((int64_t)P + va) & ~(int64_t)1) - P);  // field 1 start (P + va1 even)
+    if (tid == 0 && smemA) {
+      const uint32_t n0b = (uint32_t)((((vb + 1 - va0) + 1) & ~1) * sizeof(double));
+      const uint32_t n1b = (uint32_t)((((vb + 1 - va1) + 1) & ~1) * sizeof(double));
       mbar_expect_tx(&bar[2], n0b + n1b);
-      bulk_g2s(Fs, vin + (base - 1 - off0), n0b, &bar[2]);
-      bulk_g2s(Fs + (WP + 4), vin + ((int64_t)P + base - 1 - off1), n1b, &bar[2]);
+      bulk_g2s(Fs, vin + va0, n0b, &bar[2]);
+      bulk_g2s(Fs + (WP + 8), vin + ((int64_t)P + va1), n1b, &bar[2]);
     }
     {
       const double* F0 = vin;
       const double* F1 = vin + P;
-      const double m1_0 = __ldcg(F0) - 2.0 * __ldcg(F0 + 1) + __ldcg(F0 + 2);
-      const double mP2_0 = __ldcg(F0 + P - 3) - 2.0 * __ldcg(F0 + P - 2) + __ldcg(F0 + P - 1);
-      const double m1_1 = __ldcg(F1) - 2.0 * __ldcg(F1 + 1) + __ldcg(F1 + 2);
-      const double mP2_1 = __ldcg(F1 + P - 3) - 2.0 * __ldcg(F1 + P - 2) + __ldcg(F1 + P - 1);
-      const double* Fw0 = Fs + off0 + 1 - base;      // Fw0[k] = F0[k] for k in [base-1, base+Wa]
-      const double* Fw1 = Fs + (WP + 4) + off1 + 1 - base;
-      if (fastA) {
+      const double* Fw0 = smemA ? Fs - va0 : F0;                // Fw[k] = F[k] for k in [va, vb]
+      const double* Fw1 = smemA ? Fs + (WP + 8) - va1 : F1;
+      if (smemA) {
         mbar_wait(&bar[2], ph[2]);
         ph[2] ^= 1u;
-        for (int p = tid; p < Wa; p += NT) {
-          const int k = base + p;
-          double r0 = 6.0 * (Fw0[k - 1] - 2.0 * Fw0[k] + Fw0[k + 1]);
-          double r1 = 6.0 * (Fw1[k - 1] - 2.0 * Fw1[k] + Fw1[k + 1]);
+      }
+      // m_1 and m_{P-2} (not-a-knot end rows), only where the window reaches the ends
+      double m1_0 = 0.0, m1_1 = 0.0, mP2_0 = 0.0, mP2_1 = 0.0;
+      if (!smemA || va == 0) {
+        m1_0 = Fw0[0] - 2.0 * Fw0[1] + Fw0[2];
+        m1_1 = Fw1[0] - 2.0 * Fw1[1] + Fw1[2];
+      }
+      if (!smemA || vb == P - 1) {
+        mP2_0 = Fw0[P - 3] - 2.0 * Fw0[P - 2] + Fw0[P - 1];
+        mP2_1 = Fw1[P - 3] - 2.0 * Fw1[P - 2] + Fw1[P - 1];
+      }
+      for (int p = tid; p < Wa; p += NT) {
+        const int k = base + p;
+        double r0, r1;
+        if (k >= 2 && k <= P - 3) {
+          r0 = 6.0 * (Fw0[k - 1] - 2.0 * Fw0[k] + Fw0[k + 1]);
+          r1 = 6.0 * (Fw1[k - 1] - 2.0 * Fw1[k] + Fw1[k + 1]);
           if (k == 2) { r0 -= m1_0; r1 -= m1_1; }
           if (k == P - 3) { r0 -= mP2_0; r1 -= mP2_1; }
-          T0[p] = r0;
-          T0[WP + p] = r1;
+        } else {
+          r0 = rhs_tilde(Fw0, 1, P, (int64_t)k, m1_0, mP2_0);
+          r1 = rhs_tilde(Fw1, 1, P, (int64_t)k, m1_1, mP2_1);
         }
-      } else {
-        for (int p = tid; p < Wa; p += NT) {
-          T0[p] = rhs_tilde(F0, 1, P, (int64_t)base + p, m1_0, mP2_0);
-          T0[WP + p] = rhs_tilde(F1, 1, P, (int64_t)base + p, m1_1, mP2_1);
-        }
+        T0[p] = r0;
+        T0[WP + p] = r1;
       }
       __syncthreads();
       PHASE_STAMP(5);
@@ -381,7 +413,6 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
       double* ring1 = const_cast<double*>(s.ring) + (int64_t)slot[0] * s.slot_elems;
 #pragma unroll
       for (int f = 0; f < 2; ++f) {
-        const double* F = f ? F1 : F0;
         const double* Fw = f ? Fw1 : Fw0;
         const double m1 = f ? m1_1 : m1_0, mP2 = f ? mP2_1 : mP2_0;
         const double* Am = A + f * WP;
@@ -396,15 +427,15 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
         double* rf = ring1 + (int64_t)f * g.cfield;
         for (int k = k0 + tid; k < k1; k += NT) {
           double c;
-          if (fastA) c = Fw[k] - mt(k) * (1.0 / 6.0);
-          else if (k >= 0 && k < P) c = __ldcg(F + k) - mk(k) * (1.0 / 6.0);
+          if (k >= 2 && k <= P - 3) c = Fw[k] - mt(k) * (1.0 / 6.0);
+          else if (k >= 0 && k < P) c = Fw[k] - mk(k) * (1.0 / 6.0);
           else if (k < 0) {
-            const double c0 = __ldcg(F) - mk(0) * (1.0 / 6.0), c1 = __ldcg(F + 1) - m1 * (1.0 / 6.0);
-            c = 6.0 * __ldcg(F) - 4.0 * c0 - c1;
+            const double c0 = Fw[0] - mk(0) * (1.0 / 6.0), c1 = Fw[1] - m1 * (1.0 / 6.0);
+            c = 6.0 * Fw[0] - 4.0 * c0 - c1;
           } else {
-            const double cl = __ldcg(F + P - 1) - mk(P - 1) * (1.0 / 6.0);
-            const double cm = __ldcg(F + P - 2) - mP2 * (1.0 / 6.0);
-            c = 6.0 * __ldcg(F + P - 1) - 4.0 * cl - cm;
+            const double cl = Fw[P - 1] - mk(P - 1) * (1.0 / 6.0);
+            const double cm = Fw[P - 2] - mP2 * (1.0 / 6.0);
+            c = 6.0 * Fw[P - 1] - 4.0 * cl - cm;
           }
           rf[k + 1] = c;
         }
@@ -499,6 +530,7 @@ bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int qspan1, in
   const int nwpg = v.NT / (32 * v.C);
   fz.variant = variant;
   fz.TP = 32 * nwpg * v.R;
+  if (P < 2 * fz.TP + 2 * kPcrHalo + 256) return false;     // small grids: generic kernel (smemA below)
   threads = v.NT;
   blocks = (int)((P + fz.TP - 1) / fz.TP);
   int wm = fz.TP + qspan_max + 4 + 2;
@@ -506,8 +538,8 @@ bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int qspan1, in
   if (wr > wm) wm = wr;
   wm = (wm + 1) & ~1;
   fz.WMAX = wm;
-  fz.WP = ((fz.TP + 1 + 8 + 2 * kPcrHalo + 4) + 1) & ~1;      // PCR extent of the own tile
-  smem = 128 + ((size_t)4 * wm + 2 * (size_t)(fz.WP + 4) + 4 * (size_t)fz.WP) * sizeof(double);
+  fz.WP = ((fz.TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;      // PCR extent of the own tile (+ window slack)
+  smem = 128 + ((size_t)4 * wm + 2 * (size_t)(fz.WP + 8) + 4 * (size_t)fz.WP) * sizeof(double);
   (void)K; (void)L; (void)nsm;
   return smem <= (v.MB == 1 ? 220 * 1024 : 112 * 1024);
 }
