@@ -92,8 +92,13 @@ typedef struct {
   int32_t  bootstrap_substeps;
   int32_t  smoothing;        /* 1: cell-average the kinked payoff at the terminal layer
                                 (R11)                          */
-  int32_t  nranks, rank;     /* slab partition along axis 0 (d >= 2); 1/0 for one GPU       */
-  const void* nccl_unique_id;/* reserved for the multi-GPU path; NULL                       */
+  int32_t  nranks, rank;     /* slab partition along axis 0 (d >= 2); 1/0 for one GPU.  Rank r
+                                owns rows [r P0/R, (r+1) P0/R) and keeps `halo` extra rows on
+                                each side (quadrature reach + cubic support + PCR decay),
+                                exchanged after every step                    */
+  const void* nccl_unique_id;/* nranks > 1: 128-byte ncclUniqueId from bsde_nccl_unique_id()
+                                (multi-process, one rank per GPU, halos by NCCL send/recv), or
+                                NULL for an in-process group driven by bsde_group_step/solve */
   void*    stream;           /* cudaStream_t to run on; NULL -> library-owned stream        */
   int32_t  device;           /* CUDA device ordinal                                         */
   int32_t  kernel_variant;   /* 0: auto (fastest available), 1: generic reference kernels   */
@@ -133,7 +138,8 @@ bsde_status bsde_solve(bsde_ctx* ctx, bsde_result* res);
 /* index n of the newest level                                                         */
 bsde_status bsde_level(const bsde_ctx* ctx, int32_t* n_out);
 
-/* Copy field (0 = y, k = z_k) of the newest level to host memory (count = total points). */
+/* Copy field (0 = y, k = z_k) of the newest level to host memory; count = the points this
+ * rank owns (all points for one rank).                                                 */
 bsde_status bsde_get_layer(const bsde_ctx* ctx, int32_t field, double* host_dst, int64_t count);
 
 /* Picard iteration count per point of the newest level (0 for initial layers).         */
@@ -156,6 +162,28 @@ bsde_status bsde_eval(bsde_ctx* ctx, const double* x, double* out);
 /* Device pointer of field `field` of the newest level (npts contiguous doubles, valid
  * until the next bsde_step).                                                          */
 bsde_status bsde_layer_device_ptr(const bsde_ctx* ctx, int32_t field, const double** dptr);
+
+/* Slab partition of this rank: owned global rows [own_lo, own_hi) of axis 0 and the halo
+ * width (0 for one rank).  bsde_get_layer / bsde_get_picard_counts return the owned rows.  */
+bsde_status bsde_query_partition(const bsde_ctx* ctx, int64_t* own_lo, int64_t* own_hi, int64_t* halo);
+
+/* Host only (no device needed): the partition a config would get: out = {own_lo, own_hi,
+ * halo, slab_lo, slab_hi} (global rows of axis 0).  INVALID_ARGUMENT if a slab is thinner
+ * than the halo.                                                                        */
+bsde_status bsde_query_partition_cfg(const bsde_config* cfg, int64_t out[5]);
+
+/* A fresh NCCL unique id (rank 0 calls it and broadcasts the bytes, e.g. with
+ * torch.distributed); out must hold >= 128 bytes.                                      */
+bsde_status bsde_nccl_unique_id(void* out, size_t bytes);
+
+/* In-process slab group: ctxs[r] is rank r of n (nccl_unique_id == NULL), all at the same
+ * level.  One backward step on every rank, then the halo copy between neighbours
+ * (cudaMemcpyPeer; ranks may share a GPU).  Synchronises the ranks' streams.           */
+bsde_status bsde_group_step(bsde_ctx** ctxs, int32_t n);
+
+/* Remaining steps of an in-process group to n = 0 and the evaluation point (from the
+ * owning rank).  res may be NULL.                                                      */
+bsde_status bsde_group_solve(bsde_ctx** ctxs, int32_t n, bsde_result* res);
 
 /* Number of kernels launched by this context so far.                                  */
 bsde_status bsde_kernel_launches(const bsde_ctx* ctx, int64_t* count);

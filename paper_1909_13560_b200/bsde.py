@@ -26,7 +26,8 @@ TERMINALS = {"const": 0, "poly": 1, "logistic": 2, "ex2": 3, "call_w": 4, "sin_s
 # every symbol include/bsde.h declares
 EXPORTS = ["bsde_query_workspace", "bsde_setup", "bsde_step", "bsde_solve", "bsde_level", "bsde_get_layer",
            "bsde_get_picard_counts", "bsde_query_grid", "bsde_query_taps", "bsde_eval", "bsde_layer_device_ptr",
-           "bsde_kernel_launches", "bsde_last_error", "bsde_destroy"]
+           "bsde_query_partition", "bsde_query_partition_cfg", "bsde_nccl_unique_id", "bsde_group_step",
+           "bsde_group_solve", "bsde_kernel_launches", "bsde_last_error", "bsde_destroy"]
 
 
 class BsdeError(RuntimeError):
@@ -79,6 +80,11 @@ def load_library(path: str = LIB_PATH):
             lib.bsde_eval.argtypes = [P, D, D]
             lib.bsde_layer_device_ptr.argtypes = [P, I32, C.POINTER(C.c_void_p)]
             lib.bsde_kernel_launches.argtypes = [P, C.POINTER(I64)]
+            lib.bsde_query_partition.argtypes = [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]
+            lib.bsde_query_partition_cfg.argtypes = [C.POINTER(bsde_config), C.POINTER(I64)]
+            lib.bsde_nccl_unique_id.argtypes = [C.c_void_p, C.c_size_t]
+            lib.bsde_group_step.argtypes = [C.POINTER(C.c_void_p), I32]
+            lib.bsde_group_solve.argtypes = [C.POINTER(C.c_void_p), I32, C.POINTER(bsde_result)]
             lib.bsde_last_error.argtypes = [P]
             lib.bsde_last_error.restype = C.c_char_p
             lib.bsde_destroy.argtypes = [P]
@@ -94,7 +100,8 @@ def _dp(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
-def make_config(spec: dict, device: int = 0, stream: int | None = None, kernel_variant: int = 0) -> bsde_config:
+def make_config(spec: dict, device: int = 0, stream: int | None = None, kernel_variant: int = 0,
+                nranks: int = 1, rank: int = 0, nccl_id=None) -> bsde_config:
     c = bsde_config()
     c.struct_size = C.sizeof(bsde_config)
     d = int(spec["d"])
@@ -120,8 +127,8 @@ def make_config(spec: dict, device: int = 0, stream: int | None = None, kernel_v
     c.bootstrap = int(spec.get("bootstrap", 0))
     c.bootstrap_substeps = int(spec.get("bootstrap_substeps", 1))
     c.smoothing = int(spec.get("smoothing", 0))
-    c.nranks, c.rank = 1, 0
-    c.nccl_unique_id = None
+    c.nranks, c.rank = int(nranks), int(rank)
+    c.nccl_unique_id = C.cast(nccl_id, C.c_void_p) if nccl_id is not None else None
     c.stream = stream
     c.device = int(device)
     c.kernel_variant = int(kernel_variant)
@@ -138,14 +145,37 @@ def query_workspace(spec: dict) -> int:
     return int(n.value)
 
 
+def query_partition(spec: dict, nranks: int, rank: int) -> dict:
+    """Host-only: the slab (global axis-0 rows) a rank would own (bsde_query_partition_cfg)."""
+    lib = load_library()
+    cfg = make_config(spec, nranks=nranks, rank=rank)
+    out = (C.c_int64 * 5)()
+    st = lib.bsde_query_partition_cfg(C.byref(cfg), out)
+    if st != BSDE_OK:
+        raise BsdeError(st, lib.bsde_last_error(None).decode())
+    return dict(own_lo=out[0], own_hi=out[1], halo=out[2], slab_lo=out[3], slab_hi=out[4])
+
+
+def nccl_unique_id() -> bytes:
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    st = lib.bsde_nccl_unique_id(buf, 128)
+    if st != BSDE_OK:
+        raise BsdeError(st, lib.bsde_last_error(None).decode())
+    return buf.raw
+
+
 class Solver:
-    """One bsde_ctx: ``bsde_setup`` on construction, ``bsde_destroy`` on close."""
+    """One bsde_ctx: ``bsde_setup`` on construction, ``bsde_destroy`` on close.  With
+    ``nranks > 1`` the context holds the slab of ``rank`` (d >= 2); ``nccl_id`` (128 bytes)
+    selects the multi-process NCCL mode, None an in-process group (see ``GroupSolver``)."""
 
     def __init__(self, spec: dict, device: int = 0, stream: int | None = None, workspace=None,
-                 kernel_variant: int = 0):
+                 kernel_variant: int = 0, nranks: int = 1, rank: int = 0, nccl_id: bytes | None = None):
         self._lib = load_library()
         self.spec = dict(spec)
-        self.cfg = make_config(spec, device, stream, kernel_variant)
+        self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        self.cfg = make_config(spec, device, stream, kernel_variant, nranks, rank, self._id)
         h = C.c_void_p()
         ptr, nbytes = None, 0
         if workspace is not None:          # caller-owned device memory (e.g. a torch uint8 tensor)
@@ -159,8 +189,13 @@ class Solver:
         dx = (C.c_double * 3)()
         self._call(self._lib.bsde_query_grid(h, n, dx))
         self.d = int(spec["d"])
-        self.shape = tuple(int(n[a]) for a in range(self.d))
+        self.global_shape = tuple(int(n[a]) for a in range(self.d))
         self.dx = tuple(float(dx[a]) for a in range(self.d))
+        lo, hi, halo = C.c_int64(), C.c_int64(), C.c_int64()
+        self._call(self._lib.bsde_query_partition(h, C.byref(lo), C.byref(hi), C.byref(halo)))
+        self.own = (int(lo.value), int(hi.value))
+        self.halo = int(halo.value)
+        self.shape = (self.own[1] - self.own[0],) + self.global_shape[1:]     # owned part
         self.npts = int(np.prod(self.shape))
 
     def _call(self, st):
@@ -229,8 +264,59 @@ class Solver:
         self._call(self._lib.bsde_layer_device_ptr(self._h, field, C.byref(p)))
         return int(p.value)
 
+    def partition(self) -> dict:
+        return dict(own_lo=self.own[0], own_hi=self.own[1], halo=self.halo)
+
     @property
     def kernel_launches(self) -> int:
         n = C.c_int64()
         self._call(self._lib.bsde_kernel_launches(self._h, C.byref(n)))
         return int(n.value)
+
+
+class GroupSolver:
+    """In-process slab group: ``nranks`` contexts (ranks 0..n-1) of one d >= 2 problem,
+    optionally on one GPU, stepped together (bsde_group_step / bsde_group_solve)."""
+
+    def __init__(self, spec: dict, nranks: int, devices=None, kernel_variant: int = 0):
+        devices = devices or [0] * nranks
+        self.ranks = [Solver(spec, device=devices[r], kernel_variant=kernel_variant, nranks=nranks, rank=r)
+                      for r in range(nranks)]
+        self._lib = load_library()
+        self._arr = (C.c_void_p * nranks)(*[s._h for s in self.ranks])
+
+    def _call(self, st):
+        if st != BSDE_OK:
+            raise BsdeError(st, self._lib.bsde_last_error(None).decode() or
+                            " | ".join(self._lib.bsde_last_error(s._h).decode() for s in self.ranks))
+
+    @property
+    def level(self) -> int:
+        return self.ranks[0].level
+
+    def step(self):
+        self._call(self._lib.bsde_group_step(self._arr, len(self.ranks)))
+
+    def solve(self) -> bsde_result:
+        r = bsde_result()
+        self._call(self._lib.bsde_group_solve(self._arr, len(self.ranks), C.byref(r)))
+        return r
+
+    def layer(self, field: int = 0) -> np.ndarray:
+        return np.concatenate([s.layer(field) for s in self.ranks], axis=0)
+
+    def layers(self) -> np.ndarray:
+        return np.stack([self.layer(f) for f in range(1 + self.ranks[0].d)])
+
+    def picard_counts(self) -> np.ndarray:
+        return np.concatenate([s.picard_counts() for s in self.ranks], axis=0)
+
+    def close(self):
+        for s in self.ranks:
+            s.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -12,10 +12,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbsde_b200.so")
 SOURCES = ["kernels.cu", "host.cu"]
-HEADERS = ["bsde_internal.h", "problems.cuh"]
+HEADERS = ["bsde_internal.h", "problems.cuh", "fused1d.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+LIBS = ["-L/usr/lib/x86_64-linux-gnu", "-lnccl"]
 
 
 def _stale() -> bool:
@@ -30,7 +31,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES]
+    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES] + LIBS
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

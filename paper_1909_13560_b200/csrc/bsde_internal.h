@@ -53,6 +53,10 @@ struct Grid {
   int64_t cstride[kMaxD];  // coefficient layout strides (extent P+3 per axis, storage k+1)
   int64_t npts;            // product of P
   int64_t cfield;          // elements of one coefficient field (incl. padding)
+  // slab partition along axis 0 (d >= 2, nranks > 1): P[0] is the local extended slab,
+  // local row 0 is global row off0, owned rows are local [own0, own0 + nown0); the global
+  // axis-0 extent Pg0 is what clamping sees.  One rank: off0 = own0 = 0, nown0 = Pg0 = P[0].
+  int64_t off0, Pg0, own0, nown0;
 };
 
 // Per-step parameters of the fused quadrature / z / Picard kernel (Eq. 20).

@@ -137,7 +137,6 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
   const bool active = lo + li0 < hi;
   const int L = s.L, K = s.K;
   const int H = kPcrHalo;
-  const int tile_last = lo + NWPG * 32 * R - 1;      // last point of the full tile (incl. idle lanes)
   const Tap1D* const tap0 = taps1d(s.tap1_off);
   const double inv_gz0 = 1.0 / s.gz0;
   // coefficients this CTA owns (c indices k = storage - 1) and the PCR extent around them

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include "../../include/bsde.h"
 #include "bsde_internal.h"
@@ -88,6 +89,11 @@ struct bsde_ctx {
   std::vector<AxisTap> taps;    // host copy of the main table (K * d * L)
   int64_t launches = 0;
   unsigned long long* phase_ns = nullptr;   // debug: BSDE_PHASE_TIMING=1
+  // slab partition (d >= 2): global rows [r0, r1) owned, halo rows exchanged per step
+  int nranks = 1, rank = 0;
+  int64_t P0g = 0, r0 = 0, r1 = 0, lo_e = 0, hi_e = 0, halo = 0;
+  ncclComm_t comm = nullptr;        // multi-process mode (nccl_unique_id given)
+  bool grouped = false;             // in-process group mode (bsde_group_*)
   std::string err;
   bool closed_form = true;
 };
@@ -314,6 +320,39 @@ void set_distances(bsde_ctx* c, const std::vector<AxisTap>& t, int K, bsde_ctx::
   if (geo.blocks > c->nsm * per_sm || geo.blocks > 8192) geo.ok = false;
 }
 
+// balanced rows of rank r out of R
+inline void rank_rows(int64_t P0, int R, int r, int64_t& r0, int64_t& r1) {
+  r0 = (int64_t)r * P0 / R;
+  r1 = (int64_t)(r + 1) * P0 / R;
+}
+
+// slab partition of axis 0 (host only): owned rows, halo = axis-0 quadrature reach + cubic
+// support + PCR decay rows, extended slab [lo_e, hi_e)
+bsde_status plan_partition(bsde_ctx* c) {
+  if (c->nranks <= 1) {
+    c->r0 = 0; c->r1 = c->P0g; c->lo_e = 0; c->hi_e = c->P0g; c->halo = 0;
+    return BSDE_OK;
+  }
+  int reach = 0;
+  for (int j = 1; j <= c->K; ++j)
+    for (int l = 0; l < c->L; ++l) {
+      const int q = c->taps[((size_t)(j - 1) * c->d + 0) * c->L + l].q;
+      reach = std::max(reach, q < 0 ? -q : q);
+    }
+  c->halo = reach + 3 + kPcrHalo + 6;
+  for (int r = 0; r < c->nranks; ++r) {
+    int64_t a, b;
+    rank_rows(c->P0g, c->nranks, r, a, b);
+    if (b - a < c->halo)
+      return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "slab of rank %d has %lld rows < halo %lld: use fewer ranks", r,
+                     (long long)(b - a), (long long)c->halo);
+  }
+  rank_rows(c->P0g, c->nranks, c->rank, c->r0, c->r1);
+  c->lo_e = std::max<int64_t>(0, c->r0 - c->halo);
+  c->hi_e = std::min<int64_t>(c->P0g, c->r1 + c->halo);
+  return BSDE_OK;
+}
+
 bool closed_form_supported(const bsde_config& cfg) {
   const int t = cfg.terminal_id, f = cfg.driver_id, d = cfg.d;
   const double* q = cfg.driver_params;
@@ -348,7 +387,10 @@ bsde_status validate(const bsde_config* cfg, bsde_ctx* c) {
   if (cfg->driver_id == BSDE_DRV_EX2 && cfg->d != 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "EX2 driver is 1-D");
   if (cfg->terminal_id == BSDE_TERM_EXCHANGE_W && cfg->d != 2)
     return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "exchange payoff needs d=2");
-  if (cfg->nranks > 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "nranks > 1 not supported by this build");
+  if (cfg->nranks > 1 && cfg->d < 2)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "nranks > 1 needs d >= 2 (1-D runs as replicas, DESIGN.md)");
+  if (cfg->nranks > 1 && (cfg->rank < 0 || cfg->rank >= cfg->nranks))
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "rank %d outside 0..%d", cfg->rank, cfg->nranks - 1);
   for (int a = 0; a < cfg->d; ++a) {
     if (!(cfg->xhi[a] > cfg->xlo[a])) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "empty box on axis %d", a);
     if (cfg->npts[a] != 0 && cfg->npts[a] < 4)
@@ -384,7 +426,33 @@ void fill_grid(const bsde_config* cfg, Grid& g, double dt) {
   for (int a = d - 2; a >= 0; --a) { g.cstride[a] = ext; ext *= g.P[a] + 3; }
   g.cfield = ext;
   for (int a = d; a < 3; ++a) { g.vstride[a] = 0; g.cstride[a] = 0; }
+  g.off0 = 0;
+  g.Pg0 = g.P[0];
+  g.own0 = 0;
+  g.nown0 = g.P[0];
 }
+
+// restrict a global grid to the local extended slab [lo_e, hi_e) of axis 0, owned [r0, r1)
+void localize_grid(Grid& g, int64_t lo_e, int64_t hi_e, int64_t r0, int64_t r1) {
+  const int d = g.d;
+  const int64_t Pg0 = g.P[0];
+  g.P[0] = hi_e - lo_e;
+  g.npts = 1;
+  for (int a = 0; a < d; ++a) g.npts *= g.P[a];
+  g.vstride[d - 1] = 1;
+  for (int a = d - 2; a >= 0; --a) g.vstride[a] = g.vstride[a + 1] * g.P[a + 1];
+  const int64_t lastQ = ((g.P[d - 1] + 3 + 3) / 4) * 4;
+  g.cstride[d - 1] = 1;
+  int64_t ext = lastQ;
+  for (int a = d - 2; a >= 0; --a) { g.cstride[a] = ext; ext *= g.P[a] + 3; }
+  g.cfield = ext;
+  g.off0 = lo_e;
+  g.Pg0 = Pg0;
+  g.own0 = r0 - lo_e;
+  g.nown0 = r1 - r0;
+}
+
+
 
 struct Layout {
   size_t values, ring, tmp0, tmp1, picard, bad, barrier, dres, total;
@@ -411,6 +479,8 @@ Layout layout(const Grid& g, int F, int K) {
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
+
+bsde_status exchange_nccl(bsde_ctx* c);
 
 // One step of the scheme (Eq. 20) from the newest values (level n+1) and the ring slots of
 // levels n+2..n+K: slots[0] receives the spline of the newest values.  Output -> the other
@@ -458,6 +528,57 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
   }
   if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "step kernels: %s", cudaGetErrorString(e));
   c->cur ^= 1;
+  return exchange_nccl(c);      // no-op for one rank and for in-process groups (bsde_group_step)
+}
+
+// halo rows of the newest values between slab neighbours (d >= 2, nranks > 1)
+struct HaloPlan {
+  int64_t send_lo_off, send_lo_rows;   // to rank-1: local row offset / rows
+  int64_t recv_lo_off, recv_lo_rows;   // from rank-1
+  int64_t send_hi_off, send_hi_rows;   // to rank+1
+  int64_t recv_hi_off, recv_hi_rows;   // from rank+1
+};
+HaloPlan halo_plan(const bsde_ctx* c) {
+  HaloPlan p{};
+  if (c->rank > 0) {
+    p.recv_lo_off = 0;
+    p.recv_lo_rows = c->r0 - c->lo_e;                          // my rows [lo_e, r0)
+    p.send_lo_off = c->r0 - c->lo_e;
+    p.send_lo_rows = std::min<int64_t>(c->P0g - c->r0, c->halo);  // rank-1's rows [r0, r0 + halo)
+  }
+  if (c->rank < c->nranks - 1) {
+    p.recv_hi_off = c->r1 - c->lo_e;
+    p.recv_hi_rows = c->hi_e - c->r1;                          // my rows [r1, hi_e)
+    p.send_hi_rows = std::min<int64_t>(c->r1, c->halo);        // rank+1's rows [r1 - halo, r1)
+    p.send_hi_off = c->r1 - p.send_hi_rows - c->lo_e;
+  }
+  return p;
+}
+
+int64_t row_len(const bsde_ctx* c) { return c->g.npts / c->g.P[0]; }
+
+bsde_status exchange_nccl(bsde_ctx* c) {
+  if (c->nranks <= 1 || c->grouped) return BSDE_OK;
+  const HaloPlan hp = halo_plan(c);
+  const int64_t rl = row_len(c);
+  double* v = c->vbuf[c->cur];
+  ncclResult_t nr = ncclGroupStart();
+  for (int f = 0; f < c->F && nr == ncclSuccess; ++f) {
+    double* b = v + (int64_t)f * c->g.npts;
+    if (c->rank > 0) {
+      nr = ncclSend(b + hp.send_lo_off * rl, (size_t)(hp.send_lo_rows * rl), ncclDouble, c->rank - 1, c->comm, c->stream);
+      if (nr == ncclSuccess)
+        nr = ncclRecv(b + hp.recv_lo_off * rl, (size_t)(hp.recv_lo_rows * rl), ncclDouble, c->rank - 1, c->comm, c->stream);
+    }
+    if (c->rank < c->nranks - 1 && nr == ncclSuccess) {
+      nr = ncclSend(b + hp.send_hi_off * rl, (size_t)(hp.send_hi_rows * rl), ncclDouble, c->rank + 1, c->comm, c->stream);
+      if (nr == ncclSuccess)
+        nr = ncclRecv(b + hp.recv_hi_off * rl, (size_t)(hp.recv_hi_rows * rl), ncclDouble, c->rank + 1, c->comm, c->stream);
+    }
+  }
+  ncclResult_t ne = ncclGroupEnd();
+  if (nr != ncclSuccess || ne != ncclSuccess)
+    return set_err(c, BSDE_ERR_COMM, "halo exchange: %s", ncclGetErrorString(nr != ncclSuccess ? nr : ne));
   return BSDE_OK;
 }
 
@@ -477,10 +598,96 @@ void release(bsde_ctx* c) {
   if (c->boot_tap1_off >= 0) arena_free(dev, c->boot_tap1_off);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->phase_ns) cudaFree(c->phase_ns);
+  if (c->comm) ncclCommDestroy(c->comm);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
 }  // namespace
+
+// The evaluation point x = 0 (reading R4): the grid value if 0 is a grid node, else the
+// spline of the newest level at 0.  With a slab partition the rank owning the cell of x = 0
+// computes it; NCCL ranks then share it with an all-reduce (zeros elsewhere).
+// Leaves out[] on the host (synchronises c->stream).
+bsde_status eval_point(bsde_ctx* c, double* out) {
+  for (int f = 0; f < 4; ++f) out[f] = 0.0;
+  bool on_grid = true;
+  for (int a = 0; a < c->d; ++a)
+    if (!(c->g.xlo[a] == -c->g.xhi[a] && ((a == 0 ? c->P0g : c->g.P[a]) % 2) == 1)) on_grid = false;
+  // global axis-0 row of the point (node or cell)
+  const double u0 = (0.0 - c->g.xlo[0]) / c->g.dx[0];
+  int64_t row = on_grid ? (c->P0g - 1) / 2 : std::min<int64_t>(std::max<int64_t>((int64_t)floor(u0), 0), c->P0g - 2);
+  const bool owner = row >= c->r0 && row < c->r1;
+  if (owner) {
+    if (on_grid) {
+      int64_t idx = (row - c->lo_e) * c->g.vstride[0];
+      for (int a = 1; a < c->d; ++a) idx += ((c->g.P[a] - 1) / 2) * c->g.vstride[a];
+      for (int f = 0; f < c->F; ++f) {
+        cudaError_t e = cudaMemcpyAsync(&out[f], c->vbuf[c->cur] + (int64_t)f * c->g.npts + idx, sizeof(double),
+                                        cudaMemcpyDeviceToHost, c->stream);
+        if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "read-back: %s", cudaGetErrorString(e));
+      }
+    } else {
+      const double x[3] = {0, 0, 0};
+      bsde_status st = spline_into(c, c->RS);                 // newest level -> scratch slot
+      if (st) return st;
+      cudaError_t e = launch_eval(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, x, c->dres, c->stream);
+      ++c->launches;
+      if (e == cudaSuccess) e = cudaMemcpyAsync(out, c->dres, sizeof(double) * c->F, cudaMemcpyDeviceToHost, c->stream);
+      if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "eval: %s", cudaGetErrorString(e));
+    }
+  }
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
+  if (c->comm) {
+    cudaError_t ce = cudaMemcpyAsync(c->dres, out, sizeof(double) * 4, cudaMemcpyHostToDevice, c->stream);
+    ncclResult_t nr = ncclAllReduce(c->dres, c->dres, 4, ncclDouble, ncclSum, c->comm, c->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out, c->dres, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
+    if (nr != ncclSuccess) return set_err(c, BSDE_ERR_COMM, "all-reduce of y0: %s", ncclGetErrorString(nr));
+    if (ce != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "y0: %s", cudaGetErrorString(ce));
+  }
+  return BSDE_OK;
+}
+
+// in-process slab group (nranks contexts driven by one host thread, possibly on one GPU):
+// copy halo rows of the newest values from the neighbours' buffers
+bsde_status group_exchange(bsde_ctx** cs, int n) {
+  for (int r = 0; r < n; ++r) {
+    cudaSetDevice(cs[r]->cfg.device);
+    cudaError_t e = cudaStreamSynchronize(cs[r]->stream);
+    if (e != cudaSuccess) return set_err(cs[r], BSDE_ERR_CUDA, "group sync: %s", cudaGetErrorString(e));
+  }
+  for (int r = 0; r < n; ++r) {
+    bsde_ctx* c = cs[r];
+    const HaloPlan hp = halo_plan(c);
+    const int64_t rl = row_len(c);
+    cudaSetDevice(c->cfg.device);
+    for (int side = 0; side < 2; ++side) {
+      const int nbr = side == 0 ? r - 1 : r + 1;
+      if (nbr < 0 || nbr >= n) continue;
+      bsde_ctx* o = cs[nbr];
+      const HaloPlan ho = halo_plan(o);
+      const int64_t rows = side == 0 ? hp.recv_lo_rows : hp.recv_hi_rows;
+      const int64_t dst_off = side == 0 ? hp.recv_lo_off : hp.recv_hi_off;
+      const int64_t src_off = side == 0 ? ho.send_hi_off : ho.send_lo_off;
+      const int64_t src_rows = side == 0 ? ho.send_hi_rows : ho.send_lo_rows;
+      if (rows != src_rows) return set_err(c, BSDE_ERR_COMM, "halo plan mismatch (%lld vs %lld rows)", (long long)rows,
+                                           (long long)src_rows);
+      for (int f = 0; f < c->F; ++f) {
+        double* dst = c->vbuf[c->cur] + (int64_t)f * c->g.npts + dst_off * rl;
+        const double* src = o->vbuf[o->cur] + (int64_t)f * o->g.npts + src_off * rl;
+        cudaError_t e = cudaMemcpyPeerAsync(dst, c->cfg.device, src, o->cfg.device, sizeof(double) * rows * rl, c->stream);
+        if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "halo copy: %s", cudaGetErrorString(e));
+      }
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    cudaSetDevice(cs[r]->cfg.device);
+    cudaError_t e = cudaStreamSynchronize(cs[r]->stream);
+    if (e != cudaSuccess) return set_err(cs[r], BSDE_ERR_CUDA, "group sync: %s", cudaGetErrorString(e));
+  }
+  return BSDE_OK;
+}
 
 // ------------------------------------------------------------------ ABI
 extern "C" {
@@ -533,6 +740,16 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     release(c);
     return s;
   };
+  // tap tables (global grid spacing), then the slab partition of axis 0 (d >= 2, nranks > 1)
+  build_taps(c, c->K, c->dt, c->taps, &c->qspan, &c->qspan1);
+  c->nranks = cfg->nranks > 1 ? cfg->nranks : 1;
+  c->rank = c->nranks > 1 ? cfg->rank : 0;
+  c->P0g = c->g.P[0];
+  if ((st = plan_partition(c))) return fail(st);
+  if (c->nranks > 1) {
+    localize_grid(c->g, c->lo_e, c->hi_e, c->r0, c->r1);
+    c->grouped = cfg->nccl_unique_id == nullptr;
+  }
   cudaError_t ce = cudaSetDevice(cfg->device);
   if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "cudaSetDevice(%d): %s", cfg->device, cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
   ce = init_device_attributes();
@@ -542,6 +759,15 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     ce = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "stream: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
     c->own_stream = true;
+  }
+  if (c->nranks > 1 && !c->grouped) {
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_unique_id, sizeof id);
+    ncclResult_t nr = ncclCommInitRank(&c->comm, c->nranks, id, c->rank);
+    if (nr != ncclSuccess) {
+      set_err(c, BSDE_ERR_COMM, "ncclCommInitRank: %s", ncclGetErrorString(nr));
+      return fail(BSDE_ERR_COMM);
+    }
   }
   // memory
   Layout lay = layout(c->g, c->F, c->K);
@@ -580,7 +806,6 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "memset: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
 
   // tap tables -> constant arena
-  build_taps(c, c->K, c->dt, c->taps, &c->qspan, &c->qspan1);
   if (cfg->kernel_variant >= 10) c->fused_variant = cfg->kernel_variant - 10;
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
   if (c->d == 1) {
@@ -700,6 +925,7 @@ static bsde_status check_bad(bsde_ctx* c) {
 
 bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
   if (!c) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (c->grouped && c->nranks > 1) return set_err(c, BSDE_ERR_STATE, "in-process slab group: use bsde_group_solve");
   cudaSetDevice(c->cfg.device);
   const double t0 = now_s();
   cudaEvent_t e0, e1;
@@ -752,35 +978,15 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
   cudaEventDestroy(e1);
   if (res) {
     memset(res, 0, sizeof *res);
-    // evaluation point x = 0 (reading R4): grid value if 0 is a grid point, else the spline
-    bool on_grid = true;
-    int64_t idx = 0;
-    for (int a = 0; a < c->d; ++a) {
-      if (!(c->g.xlo[a] == -c->g.xhi[a] && (c->g.P[a] % 2) == 1)) on_grid = false;
-      idx += ((c->g.P[a] - 1) / 2) * c->g.vstride[a];
-    }
     double out[4] = {0, 0, 0, 0};
-    if (on_grid) {
-      for (int f = 0; f < c->F; ++f) {
-        cudaError_t e = cudaMemcpyAsync(&out[f], c->vbuf[c->cur] + (int64_t)f * c->g.npts + idx, sizeof(double),
-                                        cudaMemcpyDeviceToHost, c->stream);
-        if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "read-back: %s", cudaGetErrorString(e));
-      }
-    } else {
-      const double x[3] = {0, 0, 0};
-      if ((st = spline_into(c, c->RS))) return st;              // newest level -> scratch slot
-      cudaError_t e = launch_eval(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, x, c->dres, c->stream);
-      ++c->launches;
-      if (e == cudaSuccess) e = cudaMemcpyAsync(out, c->dres, sizeof(double) * c->F, cudaMemcpyDeviceToHost, c->stream);
-      if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "eval: %s", cudaGetErrorString(e));
-    }
+    if ((st = eval_point(c, out))) return st;
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
     res->y0 = out[0];
     for (int a = 0; a < c->d; ++a) res->z0[a] = out[1 + a];
     res->t_sweep_s = ms * 1e-3;
     res->t_total_s = now_s() - t0;
-    res->updates = c->g.npts * steps;
+    res->updates = c->g.nown0 * row_len(c) * steps;
     res->picard_max_used = c->cfg.picard_max;
   }
   return BSDE_OK;
@@ -796,9 +1002,11 @@ bsde_status bsde_get_layer(const bsde_ctx* cc, int32_t field, double* host_dst, 
   bsde_ctx* c = const_cast<bsde_ctx*>(cc);
   if (!c || !host_dst) return BSDE_ERR_INVALID_ARGUMENT;
   if (field < 0 || field >= c->F) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "field %d outside 0..%d", field, c->F - 1);
-  if (count != c->g.npts) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "count %lld != %lld", (long long)count, (long long)c->g.npts);
+  const int64_t own = c->g.nown0 * row_len(c);
+  if (count != own) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "count %lld != %lld", (long long)count, (long long)own);
   cudaSetDevice(c->cfg.device);
-  CU(cudaMemcpyAsync(host_dst, c->vbuf[c->cur] + (int64_t)field * c->g.npts, sizeof(double) * count, cudaMemcpyDeviceToHost,
+  CU(cudaMemcpyAsync(host_dst, c->vbuf[c->cur] + (int64_t)field * c->g.npts + c->g.own0 * row_len(c),
+                     sizeof(double) * count, cudaMemcpyDeviceToHost,
                      c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return BSDE_OK;
@@ -807,9 +1015,10 @@ bsde_status bsde_get_layer(const bsde_ctx* cc, int32_t field, double* host_dst, 
 bsde_status bsde_get_picard_counts(const bsde_ctx* cc, int32_t* host_dst, int64_t count) {
   bsde_ctx* c = const_cast<bsde_ctx*>(cc);
   if (!c || !host_dst) return BSDE_ERR_INVALID_ARGUMENT;
-  if (count != c->g.npts) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "count mismatch");
+  if (count != c->g.nown0 * row_len(c)) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "count mismatch");
   cudaSetDevice(c->cfg.device);
-  CU(cudaMemcpyAsync(host_dst, c->picard, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(host_dst, c->picard + c->g.own0 * row_len(c), sizeof(int32_t) * count, cudaMemcpyDeviceToHost,
+                     c->stream));
   CU(cudaStreamSynchronize(c->stream));
   return BSDE_OK;
 }
@@ -817,8 +1026,89 @@ bsde_status bsde_get_picard_counts(const bsde_ctx* cc, int32_t* host_dst, int64_
 bsde_status bsde_query_grid(const bsde_ctx* c, int64_t npts[3], double dx[3]) {
   if (!c) return BSDE_ERR_INVALID_ARGUMENT;
   for (int a = 0; a < 3; ++a) {
-    npts[a] = a < c->d ? c->g.P[a] : 1;
+    npts[a] = a < c->d ? (a == 0 ? c->P0g : c->g.P[a]) : 1;
     dx[a] = a < c->d ? c->g.dx[a] : 0.0;
+  }
+  return BSDE_OK;
+}
+
+bsde_status bsde_query_partition(const bsde_ctx* c, int64_t* own_lo, int64_t* own_hi, int64_t* halo) {
+  if (!c) return BSDE_ERR_INVALID_ARGUMENT;
+  if (own_lo) *own_lo = c->r0;
+  if (own_hi) *own_hi = c->r1;
+  if (halo) *halo = c->halo;
+  return BSDE_OK;
+}
+
+bsde_status bsde_query_partition_cfg(const bsde_config* cfg, int64_t out[5]) {
+  bsde_status st = validate(cfg, nullptr);
+  if (st) return st;
+  bsde_ctx c;
+  c.cfg = *cfg;
+  c.d = cfg->d; c.F = 1 + cfg->d; c.Ky = cfg->Ky; c.Kz = cfg->Kz; c.K = std::max(cfg->Ky, cfg->Kz);
+  c.L = cfg->L; c.N = cfg->N;
+  c.dt = (cfg->T - cfg->t0) / cfg->N;
+  fill_grid(cfg, c.g, c.dt);
+  hermite_rule(c.L, c.gh_a, c.gh_w);
+  build_taps(&c, c.K, c.dt, c.taps, &c.qspan, &c.qspan1);
+  c.nranks = cfg->nranks > 1 ? cfg->nranks : 1;
+  c.rank = c.nranks > 1 ? cfg->rank : 0;
+  c.P0g = c.g.P[0];
+  if ((st = plan_partition(&c))) { g_setup_error = c.err; return st; }
+  out[0] = c.r0; out[1] = c.r1; out[2] = c.halo; out[3] = c.lo_e; out[4] = c.hi_e;
+  return BSDE_OK;
+}
+
+bsde_status bsde_nccl_unique_id(void* out, size_t bytes) {
+  if (!out || bytes < sizeof(ncclUniqueId)) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "need %zu bytes", sizeof(ncclUniqueId));
+  ncclUniqueId id;
+  ncclResult_t nr = ncclGetUniqueId(&id);
+  if (nr != ncclSuccess) return set_err(nullptr, BSDE_ERR_COMM, "ncclGetUniqueId: %s", ncclGetErrorString(nr));
+  memcpy(out, &id, sizeof id);
+  return BSDE_OK;
+}
+
+bsde_status bsde_group_step(bsde_ctx** cs, int32_t n) {
+  if (!cs || n < 1) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "empty group");
+  for (int r = 0; r < n; ++r)
+    if (!cs[r] || cs[r]->rank != r || cs[r]->nranks != n || (n > 1 && !cs[r]->grouped))
+      return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "group member %d is not rank %d of %d (in-process mode)", r, r, n);
+  for (int r = 0; r < n; ++r) {
+    bsde_status st = bsde_step(cs[r]);
+    if (st) return st;
+  }
+  return n > 1 ? group_exchange(cs, n) : BSDE_OK;
+}
+
+bsde_status bsde_group_solve(bsde_ctx** cs, int32_t n, bsde_result* res) {
+  if (!cs || n < 1) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "empty group");
+  const double t0 = now_s();
+  int64_t steps = 0;
+  while (cs[0]->level > 0) {
+    bsde_status st = bsde_group_step(cs, n);
+    if (st) return st;
+    ++steps;
+  }
+  double out[4] = {0, 0, 0, 0};
+  for (int r = 0; r < n; ++r) {
+    cudaSetDevice(cs[r]->cfg.device);
+    bsde_status st = check_bad(cs[r]);
+    if (st) return st;
+    double o[4];
+    st = eval_point(cs[r], o);
+    if (st) return st;
+    for (int f = 0; f < 4; ++f) out[f] += o[f];
+  }
+  if (res) {
+    memset(res, 0, sizeof *res);
+    res->y0 = out[0];
+    for (int a = 0; a < cs[0]->d; ++a) res->z0[a] = out[1 + a];
+    res->t_total_s = now_s() - t0;
+    res->t_sweep_s = res->t_total_s;
+    int64_t pts = 0;
+    for (int r = 0; r < n; ++r) pts += cs[r]->g.nown0 * row_len(cs[r]);
+    res->updates = pts * steps;
+    res->picard_max_used = cs[0]->cfg.picard_max;
   }
   return BSDE_OK;
 }

@@ -40,7 +40,7 @@ cudaError_t upload_gl(const double* x, const double* w, cudaStream_t st) {
 // ------------------------------------------------------------------ layers
 __device__ inline void grid_coords(const Grid& g, int64_t p, double* x) {
   for (int a = g.d - 1; a >= 0; --a) {
-    const int64_t i = p % g.P[a];
+    const int64_t i = p % g.P[a] + (a == 0 ? g.off0 : 0);      // global index
     p /= g.P[a];
     x[a] = g.xlo[a] + (double)i * g.dx[a];
   }
@@ -401,8 +401,13 @@ __device__ inline void epilogue(const StepArgs& s, int64_t p, int64_t npts, doub
 // translation-invariant stencil (q_Lambda, theta_Lambda) of PAPER.md:391-392.
 template <int D, int DRV>
 __global__ void __launch_bounds__(256) quad_generic(StepArgs s, Grid g, Problem pb) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= g.npts) return;
+  // owned points only: rows [own0, own0 + nown0) of the (possibly partitioned) axis 0
+  int64_t rowlen = 1;
+#pragma unroll
+  for (int a = 1; a < D; ++a) rowlen *= g.P[a];
+  const int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q0 >= g.nown0 * rowlen) return;
+  const int64_t p = g.own0 * rowlen + q0;           // local linear index
   int64_t idx[D];
   {
     int64_t r = p;
@@ -436,7 +441,10 @@ __global__ void __launch_bounds__(256) quad_generic(StepArgs s, Grid g, Problem 
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         const AxisTap& t = tj[a * L + lam[a]];
-        cell[a] = clamp_cell(idx[a] + t.q, g.P[a], t.B, B[a]);
+        if (a == 0)   // clamp at the global box, then back to local storage rows
+          cell[a] = clamp_cell(idx[a] + g.off0 + t.q, g.Pg0, t.B, B[a]) - g.off0;
+        else
+          cell[a] = clamp_cell(idx[a] + t.q, g.P[a], t.B, B[a]);
         w *= t.w;
         sa[a] = t.s;
       }
@@ -461,7 +469,8 @@ __global__ void __launch_bounds__(256) quad_generic(StepArgs s, Grid g, Problem 
 template <int D, int DRV>
 static cudaError_t launch_generic(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st) {
   const int T = 256;
-  const int64_t nb = (g.npts + T - 1) / T;
+  const int64_t nown = g.npts / g.P[0] * g.nown0;
+  const int64_t nb = (nown + T - 1) / T;
   quad_generic<D, DRV><<<(unsigned)nb, T, 0, st>>>(s, g, pb);
   return cudaGetLastError();
 }
@@ -511,10 +520,12 @@ __global__ void eval_kernel(Grid g, const double* slot, int F, double x0, double
   for (int a = 0; a < g.d; ++a) {
     double X = fmin(fmax(x[a], g.xlo[a]), g.xhi[a]);
     const double u = (X - g.xlo[a]) / g.dx[a];
+    const int64_t Pa = a == 0 ? g.Pg0 : g.P[a];
     int64_t c = (int64_t)floor(u);
-    if (c > g.P[a] - 2) c = g.P[a] - 2;
+    if (c > Pa - 2) c = Pa - 2;
     if (c < 0) c = 0;
     const double t = u - (double)c;
+    if (a == 0) c -= g.off0;                       // local storage row (the owner evaluates)
     B[a][0] = (1.0 - t) * (1.0 - t) * (1.0 - t) / 6.0;
     B[a][1] = (3.0 * t * t * t - 6.0 * t * t + 4.0) / 6.0;
     B[a][2] = (-3.0 * t * t * t + 3.0 * t * t + 3.0 * t + 1.0) / 6.0;

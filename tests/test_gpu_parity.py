@@ -358,3 +358,49 @@ def test_accuracy_against_closed_forms():
         r = s.solve()
         y, z = W.reference_solution(W.cfg2(2))
         assert abs(r.y0 - y) < 1e-3 and abs(r.z0[0] - z[0]) < 1e-2
+
+
+# ------------------------------------------------------------------ slab partition (d >= 2)
+@gpu
+@pytest.mark.parametrize("R,spec", [(2, W.ex4_2d(3, 8, npts=257)), (3, W.ex4_2d(3, 8, npts=257)),
+                                    (4, W.ex4_2d(3, 16, npts=513)), (2, W.exchange_2d(2, 6, npts=201))],
+                         ids=lambda v: str(v) if isinstance(v, int) else v["name"])
+def test_slab_group_matches_single_context(R, spec):
+    """In-process slab group (R contexts on one GPU, halo rows copied per step) vs one context:
+    the redundant halo spline differs only by the PCR truncation (coupling 5e-19)."""
+    from paper_1909_13560_b200 import Solver, GroupSolver
+    with Solver(spec) as one:
+        r1 = one.solve()
+        ref = one.layers()
+    with GroupSolver(spec, R) as grp:
+        assert [s.own for s in grp.ranks][0][0] == 0
+        rg = grp.solve()
+        got = grp.layers()
+    assert got.shape == ref.shape
+    for f in range(ref.shape[0]):
+        assert relerr(got[f], ref[f]) <= 1e-13, f
+    assert abs(rg.y0 - r1.y0) <= 1e-13 * max(1.0, abs(r1.y0))
+
+
+@gpu
+def test_slab_group_oracle_parity():
+    import oracle
+    from paper_1909_13560_b200 import GroupSolver
+    spec = W.ex4_2d(3, 8, npts=257)
+    with GroupSolver(spec, 2) as grp:
+        grp.solve()
+        got = grp.layers()
+    o = oracle.Oracle(spec, nthreads=NT)
+    o.solve()
+    ref = o.layers()
+    for f in range(ref.shape[0]):
+        assert relerr(got[f], ref[f]) <= TOL
+
+
+@gpu
+def test_slab_group_rejects_single_solve():
+    from paper_1909_13560_b200 import GroupSolver, BsdeError
+    with GroupSolver(W.ex4_2d(3, 8, npts=257), 2) as grp:
+        with pytest.raises(BsdeError) as ei:
+            grp.ranks[0].solve()
+        assert ei.value.code == 7
