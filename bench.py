@@ -116,7 +116,9 @@ def run_ours(args):
     dist, rank, world = _dist()
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
-    stream = torch.cuda.current_stream().cuda_stream
+    ts = torch.cuda.Stream()          # a real stream (handle 0 would make the library create its own)
+    torch.cuda.set_stream(ts)
+    stream = ts.cuda_stream
     specs = {K: W.cfg2(K) for K in KS}
     ws = {K: torch.empty(query_workspace(specs[K]), dtype=torch.uint8, device="cuda") for K in KS}
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")

@@ -1,0 +1,249 @@
+// fused2d.cuh -- the d = 2 fused quadrature kernel (included by kernels.cu, which owns
+// the constant tap arena).  The hot kernel of BASELINE cfg 4.
+//
+// The tensor-product B-spline value at a tap (lambda, mu) is separable:
+//   u(x + s) = sum_b B_b(theta_mu) Rw_lambda[c2 + b],  Rw_lambda[k] = sum_a B_a(theta_lambda) C[c1 + a][k]
+// so for every level j and axis-0 node lambda a CTA first interpolates its TY coefficient
+// rows along axis 0 once ("row pass", 4 FMA per column of the window, both fields' rows
+// read from L2 with 7 loads per 4 outputs), then evaluates the L axis-1 nodes mu on the
+// shared-memory rows (4 FMA per field per point).  Exact algebra, 2.7x fewer FMAs than the
+// direct 16-term tensor stencil at L = 8.
+//
+// Tile: TY = 4 rows x TX = 64 R columns; thread (r, lb) owns R = 5 consecutive points of
+// row r (odd stride: conflict-free LDS.64).  Axis-1 clamping uses the same
+// virtual extension as the 1-D kernel: window columns outside [0, P1+2] hold the clamped
+// boundary value of the row and the straddling cells take it directly.  Axis-0 clamping is
+// per row in the row pass.  Two CTAs per SM overlap one CTA's row pass loads with the
+// other's column pass.
+#pragma once
+
+constexpr int k2TY = 4;            // tile rows
+constexpr int k2R = 5;             // points per thread along axis 1
+constexpr int k2NT = 256;          // threads per CTA
+constexpr int k2TX = k2NT / k2TY * k2R;   // 320 tile columns
+
+template <int DRV>
+__global__ void __launch_bounds__(k2NT, 2) quad2d(StepArgs s, Grid g, Problem pb, int WC) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* const Rw = reinterpret_cast<double*>(smem_raw);     // [3 fields][TY rows][WC]
+  const int tid = threadIdx.x;
+  const int r = tid / (k2NT / k2TY), lb = tid % (k2NT / k2TY);
+  const int64_t P0g = g.Pg0, P1 = g.P[1];
+  const int x0 = blockIdx.x * k2TX;
+  const int64_t yl0 = g.own0 + (int64_t)blockIdx.y * k2TY;        // local first row of the tile
+  const int64_t yown_end = g.own0 + g.nown0;
+  const int L = s.L, K = s.K;
+  const int cx0 = x0 + lb * k2R;                                   // thread's first column
+  const int64_t yrow = yl0 + r;                                    // thread's row (local)
+  const bool rowok = yrow < yown_end;
+  const double inv_gz0 = 1.0 / s.gz0;
+
+  Driver<DRV, 2> drv(pb.dp);
+  double Az1[k2R], Az2[k2R], Af[k2R], Ay[k2R];
+#pragma unroll
+  for (int q = 0; q < k2R; ++q) { Az1[q] = 0.0; Az2[q] = 0.0; Af[q] = 0.0; Ay[q] = 0.0; }
+
+  for (int j = 1; j <= K; ++j) {
+    const AxisTap* t0 = axis_taps(s.tap_off) + (j - 1) * 2 * L;     // axis 0 nodes
+    const AxisTap* t1 = t0 + L;                                      // axis 1 nodes
+    const double* Cb = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
+    drv.at(s.t_level[j - 1]);
+    const double czj = s.czj[j - 1], gzj = s.gzj[j - 1], gyj = s.gyj[j - 1];
+    const bool yj = (j == s.Ky);
+    // column window of this level: storage columns [wv, we] (wv even)
+    const int qmin2 = t1[0].q, qmax2 = t1[L - 1].q;
+    const int wa = x0 + qmin2;
+    const int wv = wa - (wa & 1);
+    const int we = x0 + k2TX - 1 + qmax2 + 3;
+    const int nwin = we - wv + 1;
+    const int s0 = max(wv, 0), s1 = min(we, (int)P1 + 2);          // real columns
+    const bool left = wv < 0, right = we > P1 + 2;
+    for (int l = 0; l < L; ++l) {
+      const AxisTap& ta = t0[l];
+      // ---- row pass: Rw[f][r'][k] = sum_a B_a C[f][row(r') + a][wv + k], r' < TY
+      {
+        // per tile row: clamped axis-0 cell (global), local storage row, basis
+        int64_t crow[k2TY];
+        double Bt[k2TY][4];
+        bool consecutive = true;
+#pragma unroll
+        for (int rr = 0; rr < k2TY; ++rr) {
+          const int64_t gcell = yl0 + rr + g.off0 + ta.q;
+          crow[rr] = clamp_cell(gcell, P0g, ta.B, Bt[rr]) - g.off0;    // local storage row of a = 0
+          if (gcell < 0 || gcell > P0g - 2) consecutive = false;        // clamped row (cell P0-1 too)
+        }
+        const int64_t cs0 = g.cstride[0];
+        for (int k = s0 - wv + tid; k <= s1 - wv; k += k2NT) {
+#pragma unroll
+          for (int f = 0; f < 3; ++f) {
+            const double* Cf = Cb + (int64_t)f * g.cfield + wv + k;
+            if (consecutive) {
+              double cin[k2TY + 3];
+#pragma unroll
+              for (int a = 0; a < k2TY + 3; ++a) cin[a] = __ldcg(Cf + (crow[0] + a) * cs0);
+#pragma unroll
+              for (int rr = 0; rr < k2TY; ++rr)
+                Rw[(f * k2TY + rr) * WC + k] =
+                    fma(ta.B[0], cin[rr], fma(ta.B[1], cin[rr + 1], fma(ta.B[2], cin[rr + 2], ta.B[3] * cin[rr + 3])));
+            } else {
+#pragma unroll
+              for (int rr = 0; rr < k2TY; ++rr) {
+                const double* Cr = Cf + crow[rr] * cs0;
+                Rw[(f * k2TY + rr) * WC + k] =
+                    fma(Bt[rr][0], __ldcg(Cr), fma(Bt[rr][1], __ldcg(Cr + cs0),
+                        fma(Bt[rr][2], __ldcg(Cr + 2 * cs0), Bt[rr][3] * __ldcg(Cr + 3 * cs0))));
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+      // ---- axis-1 boundary: clamped values of every row, virtual window entries
+      double bl[3] = {0, 0, 0}, br[3] = {0, 0, 0};     // this thread's row
+      if (left || right) {
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          const double* row = Rw + (f * k2TY + r) * WC;
+          if (left) bl[f] = (1.0 / 6.0) * row[-wv] + (2.0 / 3.0) * row[1 - wv] + (1.0 / 6.0) * row[2 - wv];
+          if (right)
+            br[f] = (1.0 / 6.0) * row[P1 - 1 - wv] + (2.0 / 3.0) * row[P1 - wv] + (1.0 / 6.0) * row[P1 + 1 - wv];
+        }
+        __syncthreads();                   // all boundary values read before the fill below
+        for (int idx = tid; idx < 3 * k2TY * nwin; idx += k2NT) {
+          const int k = idx % nwin, fr = idx / nwin;
+          const int sc = wv + k;
+          if (sc >= 0 && sc <= P1 + 2) continue;
+          double* row = Rw + fr * WC;
+          const double v = sc < 0 ? (1.0 / 6.0) * row[-wv] + (2.0 / 3.0) * row[1 - wv] + (1.0 / 6.0) * row[2 - wv]
+                                  : (1.0 / 6.0) * row[P1 - 1 - wv] + (2.0 / 3.0) * row[P1 - wv] +
+                                        (1.0 / 6.0) * row[P1 + 1 - wv];
+          row[k] = v;
+        }
+        __syncthreads();
+      }
+      // ---- column pass over the axis-1 nodes
+      const double wl = ta.w, sl = ta.s;
+      const double Wcz = wl * czj, Wgz1 = wl * gzj * sl, Wgz = wl * gzj, Wgy = wl * gyj;
+      const double* ry = Rw + (0 * k2TY + r) * WC;
+      const double* rz1 = Rw + (1 * k2TY + r) * WC;
+      const double* rz2 = Rw + (2 * k2TY + r) * WC;
+      const int rel0 = cx0 - wv;
+      for (int m = 0; m < L; ++m) {
+        const AxisTap& tb = t1[m];
+        const int q = tb.q;
+        double yv[k2R], z1v[k2R], z2v[k2R];
+        {
+          double c[k2R + 3];
+#pragma unroll
+          for (int k = 0; k < k2R + 3; ++k) c[k] = ry[rel0 + q + k];
+#pragma unroll
+          for (int p = 0; p < k2R; ++p)
+            yv[p] = fma(tb.B[0], c[p], fma(tb.B[1], c[p + 1], fma(tb.B[2], c[p + 2], tb.B[3] * c[p + 3])));
+#pragma unroll
+          for (int k = 0; k < k2R + 3; ++k) c[k] = rz1[rel0 + q + k];
+#pragma unroll
+          for (int p = 0; p < k2R; ++p)
+            z1v[p] = fma(tb.B[0], c[p], fma(tb.B[1], c[p + 1], fma(tb.B[2], c[p + 2], tb.B[3] * c[p + 3])));
+#pragma unroll
+          for (int k = 0; k < k2R + 3; ++k) c[k] = rz2[rel0 + q + k];
+#pragma unroll
+          for (int p = 0; p < k2R; ++p)
+            z2v[p] = fma(tb.B[0], c[p], fma(tb.B[1], c[p + 1], fma(tb.B[2], c[p + 2], tb.B[3] * c[p + 3])));
+        }
+        const int cb = cx0 + q, ce = cb + k2R - 1;
+        if ((left && cb <= -1 && ce >= -3) || (right && cb <= P1 + 2 && ce >= P1 - 1)) {
+#pragma unroll
+          for (int p = 0; p < k2R; ++p) {
+            const int cell = cb + p;
+            if (cell >= -3 && cell <= -1) { yv[p] = bl[0]; z1v[p] = bl[1]; z2v[p] = bl[2]; }
+            if (cell >= P1 - 1 && cell <= P1 + 2) { yv[p] = br[0]; z1v[p] = br[1]; z2v[p] = br[2]; }
+          }
+        }
+        const double wm = tb.w;
+        const double wcz = Wcz * wm, wgz1 = Wgz1 * wm, wgz2 = Wgz * (wm * tb.s), wgy = Wgy * wm;
+#pragma unroll
+        for (int p = 0; p < k2R; ++p) {
+          const double zz[2] = {z1v[p], z2v[p]};
+          const double f = drv(yv[p], zz);
+          Az1[p] = fma(wcz, z1v[p], fma(wgz1, f, Az1[p]));
+          Az2[p] = fma(wcz, z2v[p], fma(wgz2, f, Az2[p]));
+          Af[p] = fma(wgy, f, Af[p]);
+        }
+        if (yj) {
+          const double wy = wl * wm;
+#pragma unroll
+          for (int p = 0; p < k2R; ++p) Ay[p] = fma(wy, yv[p], Ay[p]);
+        }
+      }
+      __syncthreads();                     // Rw is rewritten by the next row pass
+    }
+  }
+  // ---- epilogue: z explicit (Eq. 20 line 2), y by Picard (Eq. 20 line 1)
+  if (!rowok) return;
+  Driver<DRV, 2> dn(pb.dp);
+  dn.at(s.tn);
+#pragma unroll
+  for (int p = 0; p < k2R; ++p) {
+    const int64_t col = cx0 + p;
+    if (col >= P1) break;
+    const double z[2] = {Az1[p] * inv_gz0, Az2[p] * inv_gz0};
+    const double rhs = fma(s.ky_dt, Af[p], Ay[p]);
+    double y = Ay[p];
+    int it;
+    for (it = 1; it <= s.picard_max; ++it) {
+      const double yn = fma(s.ky_dt_gy0, dn(y, z), rhs);
+      const double dy = fabs(yn - y);
+      const bool fixed = (yn == y);
+      y = yn;
+      if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
+      if (fixed) { it = s.picard_max; break; }
+    }
+    if (it > s.picard_max) it = s.picard_max;
+    const int64_t pidx = yrow * P1 + col;
+    s.values[pidx] = y;
+    s.values[g.npts + pidx] = z[0];
+    s.values[2 * g.npts + pidx] = z[1];
+    s.picard[pidx] = it;
+    if (!isfinite(y) || !isfinite(z[0]) || !isfinite(z[1])) atomicMin(s.bad, (unsigned long long)pidx);
+  }
+}
+
+// shared memory of quad2d for a column-window width WC (doubles)
+size_t fused2d_smem(int WC) { return (size_t)3 * k2TY * WC * sizeof(double); }
+
+// the widest column window over the levels: TX + (q_max - q_min) on axis 1 + 4 + 2
+int fused2d_window(const AxisTap* host_taps, int K, int L) {
+  int span = 0;
+  for (int j = 1; j <= K; ++j) {
+    const AxisTap* t1 = host_taps + ((size_t)(j - 1) * 2 + 1) * L;
+    span = span > t1[L - 1].q - t1[0].q ? span : t1[L - 1].q - t1[0].q;
+  }
+  return k2TX + span + 6;
+}
+
+template <int DRV>
+static cudaError_t launch_quad2d_t(const StepArgs& s, const Grid& g, const Problem& pb, int WC, cudaStream_t st) {
+  const size_t smem = fused2d_smem(WC);
+  dim3 grid((unsigned)((g.P[1] + k2TX - 1) / k2TX), (unsigned)((g.nown0 + k2TY - 1) / k2TY));
+  quad2d<DRV><<<grid, k2NT, smem, st>>>(s, g, pb, WC);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quad2d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, cudaStream_t st) {
+  if (fused2d_smem(WC) > 112 * 1024) return cudaErrorInvalidConfiguration;
+  switch (pb.driver_id) {
+    case DRV_ZERO: return launch_quad2d_t<DRV_ZERO>(s, g, pb, WC, st);
+    case DRV_AFFINE: return launch_quad2d_t<DRV_AFFINE>(s, g, pb, WC, st);
+    case DRV_EX1: return launch_quad2d_t<DRV_EX1>(s, g, pb, WC, st);
+    case DRV_DIFF: return launch_quad2d_t<DRV_DIFF>(s, g, pb, WC, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+static cudaError_t set_attr_2d() {
+  cudaError_t e = cudaFuncSetAttribute(quad2d<DRV_ZERO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad2d<DRV_AFFINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad2d<DRV_EX1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad2d<DRV_DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  return e;
+}

@@ -41,6 +41,9 @@ cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem
 int fused1d_blocks_per_sm(int variant, size_t smem);
 cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
 cudaError_t init_device_attributes();
+cudaError_t launch_quad2d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, cudaStream_t st);
+int fused2d_window(const AxisTap* host_taps, int K, int L);
+size_t fused2d_smem(int WC);
 }  // namespace bsde
 
 using namespace bsde;
@@ -63,6 +66,7 @@ struct bsde_ctx {
   double* vbuf[2] = {nullptr, nullptr};   // ping-pong value buffers, F * npts each
   int cur = 0;                  // vbuf[cur] holds the newest level
   int fused_variant = 0;        // fused 1-D kernel variant (kernel_variant >= 10 selects variant - 10)
+  int wc2 = 0, boot_wc2 = 0;    // 2-D fused kernel column window (0: use the generic kernel)
   int nsm = 148;
   double* ring = nullptr;       // (RS + 1) * F * cfield ; slot RS = scratch
   int RS = 3;                   // ring slots: K + 2 (level m in slot m % RS; the 2 spare slots let the
@@ -486,7 +490,8 @@ bsde_status exchange_nccl(bsde_ctx* c);
 // levels n+2..n+K: slots[0] receives the spline of the newest values.  Output -> the other
 // value buffer, which becomes the newest.
 bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, const double* gzl, double dtl,
-                     double tn, const int* slots, int tap_off, int tap1_off, const bsde_ctx::Geo& geo, int variant) {
+                     double tn, const int* slots, int tap_off, int tap1_off, const bsde_ctx::Geo& geo, int variant,
+                     int wc2 = 0) {
   StepArgs s{};
   s.ring = c->ring;
   s.slot_elems = (int64_t)c->F * c->g.cfield;
@@ -522,7 +527,10 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
     e = launch_spline(c->g, c->vbuf[c->cur], c->F, c->ring + (int64_t)slots[0] * c->F * c->g.cfield, c->tmp0,
                       c->tmp1, c->stream, &c->launches);
     if (e == cudaSuccess) {
-      e = launch_generic_step(s, c->g, c->pb, c->stream);
+      if (c->d == 2 && variant == 0 && wc2 > 0 && c->pb.driver_id != 3)
+        e = launch_quad2d(s, c->g, c->pb, wc2, c->stream);
+      else
+        e = launch_generic_step(s, c->g, c->pb, c->stream);
       ++c->launches;
     }
   }
@@ -808,6 +816,10 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   // tap tables -> constant arena
   if (cfg->kernel_variant >= 10) c->fused_variant = cfg->kernel_variant - 10;
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
+  if (c->d == 2) {
+    c->wc2 = fused2d_window(c->taps.data(), c->K, c->L);
+    if (fused2d_smem(c->wc2) > 112 * 1024) c->wc2 = 0;
+  }
   if (c->d == 1) {
     c->geo.ok = fused1d_geometry(c->g, c->K, c->L, c->qspan, c->qspan1, c->nsm, c->fused_variant, c->geo.fz,
                                  c->geo.threads, c->geo.blocks, c->geo.smem);
@@ -855,6 +867,10 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
       c->boot_geo.ok = fused1d_geometry(c->g, 1, c->L, c->boot_qspan, c->boot_qspan1, c->nsm, c->fused_variant,
                                         c->boot_geo.fz, c->boot_geo.threads, c->boot_geo.blocks, c->boot_geo.smem);
       set_distances(c, bt, 1, c->boot_geo);
+    if (c->d == 2) {
+      c->boot_wc2 = fused2d_window(bt.data(), 1, c->L);
+      if (fused2d_smem(c->boot_wc2) > 112 * 1024) c->boot_wc2 = 0;
+    }
     const double g1[2] = {0.5, 0.5};
     {
       const int bytes = (int)(sizeof(AxisTap) * bt.size());
@@ -877,7 +893,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
         const double tn = cfg->t0 + m * c->dt + s * db;
         const int slots[1] = {c->RS};                        // scratch slot
         if ((st = run_step(c, 1, 1, 1, g1, g1, db, tn, slots, c->boot_tap_off, c->boot_tap1_off, c->boot_geo,
-                           cfg->kernel_variant)))
+                           cfg->kernel_variant, c->boot_wc2)))
           return fail(st);
       }
       if ((st = spline_into(c, m % c->RS))) return fail(st);
@@ -907,7 +923,7 @@ bsde_status bsde_step(bsde_ctx* c) {
   int slots[kMaxK];
   for (int j = 1; j <= c->K; ++j) slots[j - 1] = (n + j) % c->RS;   // ring slot of level n+j
   bsde_status st = run_step(c, c->K, c->Ky, c->Kz, c->gy, c->gz, c->dt, c->cfg.t0 + n * c->dt, slots, c->tap_off,
-                            c->tap1_off, c->geo, c->cfg.kernel_variant);
+                            c->tap1_off, c->geo, c->cfg.kernel_variant, c->wc2);
   if (st) return st;
   c->level = n;
   return BSDE_OK;

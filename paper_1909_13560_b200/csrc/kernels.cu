@@ -466,6 +466,9 @@ __global__ void __launch_bounds__(256) quad_generic(StepArgs s, Grid g, Problem 
 // ------------------------------------------------------------------ 1-D fused step kernel
 #include "fused1d.cuh"
 
+// ------------------------------------------------------------------ 2-D fused quadrature kernel
+#include "fused2d.cuh"
+
 template <int D, int DRV>
 static cudaError_t launch_generic(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st) {
   const int T = 256;
@@ -508,6 +511,7 @@ cudaError_t init_device_attributes() {
   if (e == cudaSuccess) e = set_attr_drv<DRV_EX1>();
   if (e == cudaSuccess) e = set_attr_drv<DRV_EX2>();
   if (e == cudaSuccess) e = set_attr_drv<DRV_DIFF>();
+  if (e == cudaSuccess) e = set_attr_2d();
   return e;
 }
 

@@ -404,3 +404,17 @@ def test_slab_group_rejects_single_solve():
         with pytest.raises(BsdeError) as ei:
             grp.ranks[0].solve()
         assert ei.value.code == 7
+
+
+@gpu
+@pytest.mark.parametrize("spec", [W.ex4_2d(3, 8, npts=257), W.exchange_2d(4, 8, npts=333),
+                                  dict(W.ex4_2d(2, 6), npts=[45, 701])],
+                         ids=lambda s: s["name"] + "_" + "x".join(map(str, s["npts"])))
+def test_2d_fused_matches_generic(spec):
+    """quad2d (separable row/column passes) vs the generic direct tensor stencil."""
+    from paper_1909_13560_b200 import Solver
+    with Solver(spec, kernel_variant=0) as a, Solver(spec, kernel_variant=1) as b:
+        a.solve()
+        b.solve()
+        for f in range(3):
+            assert relerr(a.layer(f), b.layer(f)) <= 1e-13, f
