@@ -5,8 +5,9 @@ Workload (BASELINE.json configs[1], "cfg 2"): 1-D call under different borrowing
 lending rates, P = 2^16 grid points on [-16, 16] (W-space), N = 256 time steps,
 L = 16 Gauss-Hermite nodes, K = Ky = Kz = 1..6.  One bench *step* is the backward
 sweep n = N-K .. 0 (Eq. 20) of all six K; updates = P * (N - K + 1) summed over K.
-Setup (grids, tap tables, the K closed-form initial layers and their splines) is
-outside the device-timed region; the e2e number includes it.
+The six sweeps run in one persistent launch (bsde_solve_batch: CTAs execute the problems'
+steps round-robin).  Setup (grids, tap tables, the K closed-form initial layers and their
+splines) is outside the device-timed region; the e2e number includes it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -112,7 +113,7 @@ def flush_l2(torch, buf):
 def run_ours(args):
     import numpy as np
     import torch
-    from paper_1909_13560_b200 import Solver, workloads as W, query_workspace
+    from paper_1909_13560_b200 import Solver, solve_batch, workloads as W, query_workspace
     dist, rank, world = _dist()
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
@@ -123,29 +124,25 @@ def run_ours(args):
     ws = {K: torch.empty(query_workspace(specs[K]), dtype=torch.uint8, device="cuda") for K in KS}
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    k6 = [0.0, 0, 0]
-
-    def one_step(timed=True):
-        tot, upd, launches, y0 = 0.0, 0, 0, {}
-        for K in KS:
-            flush_l2(torch, flush)
-            s = Solver(specs[K], device=dev, stream=stream, workspace=ws[K])
-            n0 = s.kernel_launches
-            torch.cuda.synchronize()
-            r = s.solve()                              # device-timed sweep (CUDA events on `stream`)
-            tot += r.t_sweep_s
-            upd += r.updates
-            if K == 6 and timed:
-                k6[0] += r.t_sweep_s
-                k6[1] += r.updates // 65536
-                k6[2] += 1
-            launches += s.kernel_launches - n0
-            y0[K] = (r.y0, r.z0[0])
+    def one_step():
+        """Set up the six contexts (untimed), flush L2, then the six sweeps in ONE persistent
+        launch (bsde_solve_batch, device-timed with CUDA events on `stream`)."""
+        ss = [Solver(specs[K], device=dev, stream=stream, workspace=ws[K]) for K in KS]
+        n0 = [s.kernel_launches for s in ss]
+        flush_l2(torch, flush)
+        torch.cuda.synchronize()
+        res = solve_batch(ss)
+        t = res[0].t_sweep_s
+        upd = sum(r.updates for r in res)
+        # one batched launch is counted by every context; the rest are the y0 evaluations
+        launches = 1 + sum(s.kernel_launches - a - 1 for s, a in zip(ss, n0))
+        y0 = {K: (r.y0, r.z0[0]) for K, r in zip(KS, res)}
+        for s in ss:
             s.close()
-        return tot, upd, launches, y0
+        return t, upd, launches, y0
 
     for _ in range(args.warmup):
-        one_step(timed=False)
+        one_step()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -164,27 +161,26 @@ def run_ours(args):
         elapsed = float(tt.item())
     value = upds * world / elapsed
 
-    # ---- the dominant kernel is quad1d_fused: one persistent launch per sweep (all N-K+1
-    # steps).  Its average launch duration is the CUDA-event time of the K = 6 sweeps of the
-    # timed region (recorded on `stream` inside bsde_solve) divided by their number.
-    k6_time, k6_steps, k6_sweeps = k6
-    launch_s = k6_time / k6_sweeps
-    fl = flops_per_point_step(6) * 65536 * (k6_steps // k6_sweeps)
+    # ---- the dominant kernel is quad1d_fused: ONE persistent launch per bench step runs all
+    # six sweeps (round-robin over the problems).  Its average duration is the CUDA-event time
+    # of the launches of the timed region (recorded on `stream` inside bsde_solve_batch).
+    launch_s = elapsed / args.steps
+    fl = sum(flops_per_point_step(K) * 65536 * (256 - K + 1) for K in KS)
     clocks = clk.summary()
     peak = peak_fp64_tflops(1965.0)
     achieved = fl / launch_s / 1e12
     traffic = None
     try:   # dram__bytes_read.sum + dram__bytes_write.sum (MB) per launch, from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "round1", "ncu_quad1d_fused_K6_summary.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "round1", "ncu_quad1d_fused_batch_summary.json")) as fh:
             prof = json.load(fh)
         traffic = (float(prof["dram__bytes_read.sum"]) + float(prof["dram__bytes_write.sum"])) * 1e6
     except (OSError, KeyError, ValueError):
         pass
     roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "traffic_note": "DRAM bytes per launch (one 251-step sweep; state is L2-resident) from ncu --set full",
-            "kernel": "quad1d_fused<DRV_DIFF> (K=6, one launch = one 251-step sweep)", "flops_per_launch": fl,
-            "launch_us": round(launch_s * 1e6, 3),
+            "traffic_note": "DRAM bytes per launch (six sweeps; state is L2-resident) from ncu --set full",
+            "kernel": "quad1d_fused<DRV_DIFF>: one launch = the 6 sweeps K=1..6 (1521 steps)",
+            "flops_per_launch": fl, "launch_us": round(launch_s * 1e6, 3),
             "peak_note": "FP64 pipe: 148 SM x 64 DFMA/clk x 2 x 1965 MHz (derived; DESIGN.md Roofline)"}
 
     # ---- e2e: setup (host config -> device) + sweep + final layers device -> host, host clock
@@ -193,9 +189,9 @@ def run_ours(args):
     t0 = time.perf_counter()
     e2e_upd, h2d, d2h = 0, 0, 0
     for _ in range(args.steps):
-        for K in KS:
-            s = Solver(specs[K], device=dev, stream=stream, workspace=ws[K])
-            r = s.solve()
+        ss = [Solver(specs[K], device=dev, stream=stream, workspace=ws[K]) for K in KS]
+        res = solve_batch(ss)
+        for K, s, r in zip(KS, ss, res):
             s.layer(0, out=host)
             s.layer(1, out=host)
             e2e_upd += r.updates
@@ -210,14 +206,14 @@ def run_ours(args):
         e2e_t = float(tt.item())
     e2e = {"value": e2e_upd * world / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
            "d2h_bytes_per_step": d2h // args.steps,
-           "note": "bsde_setup + bsde_solve + bsde_get_layer(y, z) per K, host wall clock"}
+           "note": "6 x bsde_setup + bsde_solve_batch + bsde_get_layer(y, z) per K, host wall clock"}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "cfg2: 1-D differential-rates call, P=65536, N=256, L=16, K=1..6 (one step = six sweeps)",
+           "config": {"workload": "cfg2: 1-D differential-rates call, P=65536, N=256, L=16, K=1..6 (one step = the six sweeps in one bsde_solve_batch launch)",
                       "global_batch": 65536 * world, "seq_len": 256, "parallelism": f"replicas{world}",
-                      "l2": "flushed (512 MiB write) before every sweep; sweep state ~6 MiB is L2-resident by design"},
+                      "l2": "flushed (512 MiB write) before every step; the six sweeps' state (~50 MiB) is L2-resident by design"},
            "roofline": roof, "e2e": e2e, "gpu_launches": launches // max(args.steps, 1),
            "clocks": clocks,
            "accuracy": {str(K): {"y0": y0[K][0], "z0": y0[K][1]} for K in KS},
@@ -231,7 +227,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _oracle_sample(max_seconds=12.0, steps_per_K=12):
+def _oracle_sample(max_seconds=15.0, steps_per_K=120):
     """Time the oracle (as it stands) on a bounded sample of cfg 2: steps_per_K backward
     steps of each K after its (untimed) setup."""
     import oracle
@@ -254,7 +250,8 @@ def _oracle_sample(max_seconds=12.0, steps_per_K=12):
 def cpu_baseline(args):
     v, u, t, nt = _oracle_sample()
     return {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
-            "sample": f"cfg2, up to 12 backward steps per K=1..6 after untimed setup ({u} updates in {t:.2f} s)"}
+            "sample": f"cfg2, up to 120 backward steps per K=1..6 after untimed setup, capped at 15 s "
+                      f"({u} updates in {t:.2f} s)"}
 
 
 def run_reference(args):

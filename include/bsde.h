@@ -101,7 +101,10 @@ typedef struct {
                                 NULL for an in-process group driven by bsde_group_step/solve */
   void*    stream;           /* cudaStream_t to run on; NULL -> library-owned stream        */
   int32_t  device;           /* CUDA device ordinal                                         */
-  int32_t  kernel_variant;   /* 0: auto (fastest available), 1: generic reference kernels   */
+  int32_t  kernel_variant;   /* 0: auto (fastest available), 1: generic reference kernels;
+                                10 + v (d = 1): fused kernel variant v; any other value
+                                selects the generic kernels (d >= 2: fused 2-D kernel
+                                for 0 only)                                               */
 } bsde_config;
 
 typedef struct {
@@ -134,6 +137,20 @@ bsde_status bsde_step(bsde_ctx* ctx);
 /* Remaining steps to n = 0, then the evaluation point; synchronises the stream and
  * checks the device non-finite flag (NUMERICAL_DOMAIN).  res may be NULL.             */
 bsde_status bsde_solve(bsde_ctx* ctx, bsde_result* res);
+
+/* Batched solve of n (1..8) independent d = 1 problems on one device: the remaining steps
+ * of every context run in ONE persistent launch whose CTAs execute the problems' steps
+ * round-robin (step it of problems 0..n-1, then step it+1), so each problem's neighbour
+ * waits overlap the other problems' arithmetic.  Requirements (else INVALID_ARGUMENT,
+ * nothing launched): distinct contexts, one rank, d = 1, same device, grid (P, xlo, xhi)
+ * and driver id, the fused kernel available to every context with the same variant;
+ * RESOURCE_LIMIT if the combined shared-memory footprint cannot be
+ * co-resident.  The launch is issued on ctxs[0]'s stream,
+ * ordered after the other contexts' streams and before their later work (event joins).
+ * res: n results or NULL; t_sweep_s is the batch's device time (the same in every result),
+ * updates the context's own.  Synchronises ctxs[0]'s stream; NUMERICAL_DOMAIN as for
+ * bsde_solve (first failing context).                                                 */
+bsde_status bsde_solve_batch(bsde_ctx* const* ctxs, int32_t n, bsde_result* res);
 
 /* index n of the newest level                                                         */
 bsde_status bsde_level(const bsde_ctx* ctx, int32_t* n_out);

@@ -27,7 +27,7 @@ TERMINALS = {"const": 0, "poly": 1, "logistic": 2, "ex2": 3, "call_w": 4, "sin_s
 EXPORTS = ["bsde_query_workspace", "bsde_setup", "bsde_step", "bsde_solve", "bsde_level", "bsde_get_layer",
            "bsde_get_picard_counts", "bsde_query_grid", "bsde_query_taps", "bsde_eval", "bsde_layer_device_ptr",
            "bsde_query_partition", "bsde_query_partition_cfg", "bsde_nccl_unique_id", "bsde_group_step",
-           "bsde_group_solve", "bsde_kernel_launches", "bsde_last_error", "bsde_destroy"]
+           "bsde_group_solve", "bsde_solve_batch", "bsde_kernel_launches", "bsde_last_error", "bsde_destroy"]
 
 
 class BsdeError(RuntimeError):
@@ -85,6 +85,7 @@ def load_library(path: str = LIB_PATH):
             lib.bsde_nccl_unique_id.argtypes = [C.c_void_p, C.c_size_t]
             lib.bsde_group_step.argtypes = [C.POINTER(C.c_void_p), I32]
             lib.bsde_group_solve.argtypes = [C.POINTER(C.c_void_p), I32, C.POINTER(bsde_result)]
+            lib.bsde_solve_batch.argtypes = [C.POINTER(C.c_void_p), I32, C.POINTER(bsde_result)]
             lib.bsde_last_error.argtypes = [P]
             lib.bsde_last_error.restype = C.c_char_p
             lib.bsde_destroy.argtypes = [P]
@@ -272,6 +273,20 @@ class Solver:
         n = C.c_int64()
         self._call(self._lib.bsde_kernel_launches(self._h, C.byref(n)))
         return int(n.value)
+
+
+def solve_batch(solvers) -> list:
+    """``bsde_solve_batch``: the remaining steps of several independent d = 1 Solvers (same
+    grid, driver and device) in one persistent launch with round-robin steps."""
+    lib = load_library()
+    n = len(solvers)
+    arr = (C.c_void_p * n)(*[s._h for s in solvers])
+    res = (bsde_result * n)()
+    st = lib.bsde_solve_batch(arr, n, res)
+    if st != BSDE_OK:
+        raise BsdeError(st, lib.bsde_last_error(None).decode() or
+                        " | ".join(lib.bsde_last_error(s._h).decode() for s in solvers))
+    return list(res)
 
 
 class GroupSolver:

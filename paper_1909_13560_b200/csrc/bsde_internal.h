@@ -63,8 +63,10 @@ struct Grid {
 struct StepArgs {
   const double* ring;      // coefficient ring base
   int64_t slot_elems;      // elements per ring slot (F * cfield)
-  int32_t slot[kMaxK];     // ring slot of level n+j, j = 1..K (index j-1); slot[0] receives
-                           // the spline of values_in (built at the start of the step)
+  int32_t slot[kMaxK];     // ring slot of level n+j, j = 1..K (index j-1); the generic path
+                           // rebuilds slot[0] from values_in at the start of the step
+  int32_t slot_out;        // fused 1-D path: ring slot that receives the spline of the new
+                           // level n (-1: none)
   double t_level[kMaxK];   // t_{n+j}
   double czj[kMaxK];       // coefficient of E[z^{n+j}] in z^n*gz0: [j==1] - gz_j
   double gzj[kMaxK];       // gz_j (0 for j > Kz): coefficient of E[f dW]
@@ -88,9 +90,37 @@ struct Fused1D {
   int variant;               // index into the instantiated (R, C, threads, unroll) table
   int TP;                    // points per CTA
   int WMAX;                  // doubles per field buffer in shared memory
-  int WP;                    // doubles per PCR scratch array
+  int WP;                    // doubles per PCR scratch array (own-tile spline)
+  int flag_mode;             // progress-flag release: bit 0 full fence first, bit 1 by thread 0
   double alpha[kPcrLevels];  // PCR elimination ratios
   double inv_b;              // 1 / b after the last PCR level
+};
+
+// Launch parameters of the fused kernel.  All CTAs of a launch are co-resident
+// (cooperative launch); CTAs synchronise only with the neighbours they exchange data
+// with, through per-CTA progress flags:
+//   done_flag[b] = it + 1  once CTA b wrote its tile of the level-n values (pass 1 of step it)
+//   ring_flag[b] = it + 1  once CTA b wrote its tile of the level-n coefficients (pass 2)
+struct Persist1D {
+  int n0, nsteps, ring_mode, cur;
+  double t0, dt;
+  double* vbuf[2];
+  unsigned* ring_flag;
+  unsigned* done_flag;
+  int D[kMaxK + 1];  // D[j]: CTA distance of level j's window (j >= 1); D[0]: values halo of phase A
+  int DK;            // max of D
+};
+
+// One problem of a fused launch and the launch itself.  All problems of a launch share the
+// grid, the driver template and the CTA geometry; each has its own levels, taps, ring, value
+// buffers and progress flags.  CTAs run the problems' steps round-robin (step it of problem
+// 0, 1, ..., then step it + 1), so a problem's neighbour waits overlap the other problems'
+// work.  A single solve is a batch of one.
+constexpr int kMaxBatch = 8;
+struct FusedProb {
+  StepArgs s;
+  Persist1D pp;
+  double dp[12];       // driver parameters
 };
 
 }  // namespace bsde

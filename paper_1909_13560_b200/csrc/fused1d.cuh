@@ -53,10 +53,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define PHASE_STAMP(i)                                                                          \
   do {                                                                                          \
     if (s.phase_ns != nullptr && threadIdx.x == 0)                                              \
-      s.phase_ns[((size_t)it_stamp * gridDim.x + blockIdx.x) * 16 + (i)] = gtimer();              \
+      s.phase_ns[((size_t)it_stamp * gridDim.x + blockIdx.x) * 32 + (i)] = gtimer();              \
   } while (0)
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -80,19 +85,12 @@ __device__ __forceinline__ void level_span(int qmin, int qmax, int lo, int hi, i
   we = hi - 1 + qmax + 3;
 }
 
-// Launch parameters of the fused kernel.  All CTAs of a launch are co-resident
-// (cooperative launch); CTAs synchronise only with the neighbours they exchange data
-// with, through per-CTA progress flags:
-//   ring_flag[b] = it + 1  once CTA b wrote its tile of the level-(n+1) coefficients (step it)
-//   done_flag[b] = it + 1  once CTA b wrote its tile of the level-n values (end of step it)
-struct Persist1D {
-  int n0, nsteps, ring_mode, cur;
-  double t0, dt;
-  double* vbuf[2];
-  unsigned* ring_flag;
-  unsigned* done_flag;
-  int D[kMaxK + 1];  // D[j]: CTA distance of level j's window (j >= 1); D[0]: values halo of phase A
-  int DK;            // max of D
+// Persist1D, FusedProb: bsde_internal.h
+struct FusedBatch {
+  Fused1D fz;
+  Grid g;
+  int nprob, max_steps;
+  FusedProb prob[kMaxBatch];
 };
 
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
@@ -107,24 +105,29 @@ __device__ __forceinline__ void wait_neighbours_warp(const unsigned* flag, int b
     const int q = q0 + lane;
     bool ok = q > e;
     while (!__all_sync(0xffffffffu, ok)) {
-      if (!ok) ok = ld_acquire(flag + q) >= target;
+      if (!ok) ok = ld_relaxed(flag + q) >= target;      // relaxed polling (no L1 invalidation)
       if (!__all_sync(0xffffffffu, ok)) __nanosleep(32);
     }
+    if (q <= e) (void)ld_acquire(flag + q);              // synchronises with the release
   }
   __syncwarp();
   if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 template <int DRV, int R, int C, int NT, int MB>
-__global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Problem pb, Fused1D fz, Persist1D pp) {
+__global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ FusedBatch bt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);        // 0/1: level buffers, 2: values tile
+  const Fused1D& fz = bt.fz;
+  const Grid& g = bt.g;
   const int WM = fz.WMAX, WP = fz.WP;
   double* const buf0 = reinterpret_cast<double*>(smem_raw + 128);
   double* const buf1 = buf0 + 2 * WM;
-  double* const Fs = buf1 + 2 * WM;                 // 2 x (WP + 8): values of the tile + PCR halo
-  double* const T0 = Fs + 2 * (WP + 8);             // 2 x WP
-  double* const T1 = T0 + 2 * WP;                   // 2 x WP
+  // spline scratch of pass 2, overlaying the level buffers (free after the epilogue):
+  // values window Fs (2 x (WP + 8)) and the PCR arrays T0, T1 (2 x WP each)
+  double* const Fs = buf0;
+  double* const T0 = Fs + 2 * (WP + 8);
+  double* const T1 = T0 + 2 * WP;
   constexpr int NWPG = NT / (32 * C);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int chunk = warp / NWPG, pg = warp % NWPG;
@@ -135,17 +138,18 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
   const int hi = min(lo + TP, P);
   const int li0 = (pg * 32 + lane) * R;              // first local point of this lane
   const bool active = lo + li0 < hi;
-  const int L = s.L, K = s.K;
   const int H = kPcrHalo;
-  const Tap1D* const tap0 = taps1d(s.tap1_off);
-  const double inv_gz0 = 1.0 / s.gz0;
   // coefficients this CTA owns (c indices k = storage - 1) and the PCR extent around them
   const int k0 = lo == 0 ? -1 : lo, k1 = hi == P ? P + 1 : hi;
   const int base = k0 - 4 - H;
   const int Wa = (k1 - k0) + 8 + 2 * H;
+  // values window [va, vb] of both fields (clamped to the grid); the grid is long enough
+  // (fused1d_geometry) that every folded index of the odd extension lands inside it
+  const int va = max(base - 3, 0), vb = min(base + Wa + 2, P - 1);
+  const int va0 = va & ~1;                                   // field 0 start, even
+  const int va1 = (int)((((int64_t)P + va) & ~(int64_t)1) - P);  // field 1 start (P + va1 even)
+  const int publisher = fz.flag_mode & 2 ? 0 : NT - 32;     // thread that releases the flags
 
-  int it_stamp = 0;
-  PHASE_STAMP(0);
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -154,199 +158,274 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
   }
   grid_dep_wait();            // previous kernel in the stream has completed
   __syncthreads();
-  PHASE_STAMP(1);
   uint32_t ph[3] = {0, 0, 0};
 
-  for (int it = 0; it < pp.nsteps; ++it) {
-    it_stamp = it;
-    // ---------------- step parameters
-    int slot[kMaxK];
-    double tlev[kMaxK];
-    double tn;
-    const double* vin;
-    double* vout;
-    if (pp.ring_mode) {
-      const int n = pp.n0 - it;
+  for (int it = 0; it < bt.max_steps; ++it) {
+    // ================= pass 1: levels K..1, z and Picard of step it of every problem
+    for (int ip = 0; ip < bt.nprob; ++ip) {
+      const FusedProb& fp = bt.prob[ip];
+      const Persist1D& pp = fp.pp;
+      if (it >= pp.nsteps) continue;
+      const StepArgs& s = fp.s;
+      const int it_stamp = it;
+      PHASE_STAMP(0);
+      const int L = s.L, K = s.K;
+      const Tap1D* const tap0 = taps1d(s.tap1_off);
+      int slot[kMaxK];
+      double tlev[kMaxK];
+      double tn;
+      double* vout;
+      if (pp.ring_mode) {
+        const int n = pp.n0 - it;
 #pragma unroll
-      for (int j = 1; j <= kMaxK; ++j) {
-        slot[j - 1] = (n + j) % s.ring_slots;
-        tlev[j - 1] = pp.t0 + (n + j) * pp.dt;
+        for (int j = 1; j <= kMaxK; ++j) {
+          slot[j - 1] = (n + j) % s.ring_slots;
+          tlev[j - 1] = pp.t0 + (n + j) * pp.dt;
+        }
+        tn = pp.t0 + n * pp.dt;
+        vout = pp.vbuf[(pp.cur + it + 1) & 1];
+      } else {
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j) { slot[j] = s.slot[j]; tlev[j] = s.t_level[j]; }
+        tn = s.tn;
+        vout = s.values;
       }
-      tn = pp.t0 + n * pp.dt;
-      vin = pp.vbuf[(pp.cur + it) & 1];
-      vout = pp.vbuf[(pp.cur + it + 1) & 1];
-    } else {
-#pragma unroll
-      for (int j = 0; j < kMaxK; ++j) { slot[j] = s.slot[j]; tlev[j] = s.t_level[j]; }
-      tn = s.tn;
-      vin = s.values_in;
-      vout = s.values;
-    }
-    // bulk-load level j's window into buffer b (called by warp 0).  Level 1 (slot n+1) is
-    // written in phase A of this step by the CTAs within D[1]: wait for their ring flags.
-    auto issue_level = [&](int j, int b) {
-      if (j == 1) wait_neighbours_warp(pp.ring_flag, bid, pp.D[1], nb, (unsigned)it + 1);
-      if (lane != 0) return;
-      const Tap1D* tj = tap0 + (j - 1) * L;
-      int wv, we;
-      level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
-      // real part [s0, s1) of the window (storage 0..P+2), even-aligned for the bulk copy
-      const int s0 = max(wv, 0);
-      const int s1 = (min(we, P + 2) + 2) & ~1;
-      const uint32_t bytes = (uint32_t)((s1 - s0) * sizeof(double));
-      const double* Cf = s.ring + (int64_t)slot[j - 1] * s.slot_elems;
-      double* dst = (b ? buf1 : buf0) + (s0 - wv);
-      mbar_expect_tx(&bar[b], 2 * bytes);
-      bulk_g2s(dst, Cf + s0, bytes, &bar[b]);
-      bulk_g2s(dst + WM, Cf + g.cfield + s0, bytes, &bar[b]);
-    };
-    // Slots of levels n+2..n+K were written in phase A of earlier steps by CTAs up to DK
-    // away: their ring flags of step it-1 cover all of them.
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (warp == 0) {
-      if (it > 0 && K >= 2) wait_neighbours_warp(pp.ring_flag, bid, pp.DK, nb, (unsigned)it);
-      if (K >= 2) issue_level(K, 0);
-      if (K >= 3) issue_level(K - 1, 1);
-    }
-    __syncthreads();
-    PHASE_STAMP(2);
+      // bulk-load level j's window into buffer b (lane 0 of warp 0)
+      auto issue_level = [&](int j, int b) {
+        if (lane != 0) return;
+        const Tap1D* tj = tap0 + (j - 1) * L;
+        int wv, we;
+        level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
+        // real part [s0, s1) of the window (storage 0..P+2), even-aligned for the bulk copy
+        const int s0 = max(wv, 0);
+        const int s1 = (min(we, P + 2) + 2) & ~1;
+        const uint32_t bytes = (uint32_t)((s1 - s0) * sizeof(double));
+        const double* Cf = s.ring + (int64_t)slot[j - 1] * s.slot_elems;
+        double* dst = (b ? buf1 : buf0) + (s0 - wv);
+        mbar_expect_tx(&bar[b], 2 * bytes);
+        bulk_g2s(dst, Cf + s0, bytes, &bar[b]);
+        bulk_g2s(dst + WM, Cf + g.cfield + s0, bytes, &bar[b]);
+      };
+      // Level n+j was written by pass 2 of round it-j by the CTAs within D[j]: levels >= 2 are
+      // covered by the ring flags of round it-2 within DK, level 1 needs round it-1 within
+      // D[1] (waited for just before its window is issued, behind levels K..3).  (No CTA
+      // barrier here: the previous pass ended with one; the other warps wait on the mbarriers.)
+      auto ring_wait = [&](int j) {
+        if (it == 0) return;
+        if (j == 1) wait_neighbours_warp(pp.ring_flag, bid, pp.D[1], nb, (unsigned)it);
+        else if (it >= 2) wait_neighbours_warp(pp.ring_flag, bid, pp.DK, nb, (unsigned)(it - 1));
+      };
+      if (warp == 0) {
+        ring_wait(K >= 2 ? 2 : 1);
+        issue_level(K, 0);
+        if (K >= 2) {
+          if (K == 2) ring_wait(1);
+          issue_level(K - 1, 1);
+        }
+      }
+      PHASE_STAMP(1);
 
-    Driver<DRV, 1> drv(pb.dp);
-    double Az[R], Af[R], Ay[R];
+      Driver<DRV, 1> drv(fp.dp);
+      double Az[R], Af[R], Ay[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) { Az[r] = 0.0; Af[r] = 0.0; Ay[r] = 0.0; }
-    // one level of taps on the window in buffer b.  The window spans storage indices
-    // [wv, we] (wv even); entries outside the real range [0, P+2] are filled with the
-    // clamped boundary values F_0 / F_{P-1}, so every tap uses the same
-    // 4-term B-spline stencil; the cells whose stencil straddles the boundary
-    // ([-3, -1] and [P-1, P+2]) are clamped cells and get the boundary value directly.
-    auto level = [&](int j, int b) {
-      const Tap1D* tj = tap0 + (j - 1) * L;
-      int wv, we;
-      level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
-      mbar_wait(&bar[b], ph[b]);
-      ph[b] ^= 1u;
-      double* const wy = b ? buf1 : buf0;
-      double* const wz = wy + WM;
-      // clamped boundary values: s(x_0) = (c_{-1} + 4 c_0 + c_1)/6, s(x_{P-1}) likewise
-      double fy0 = 0, fz0 = 0, fy1 = 0, fz1 = 0;
-      const bool left = wv < 0, right = we > P + 2;
-      if (left || right) {                      // edge CTAs only (CTA-uniform)
-        if (left) {
-          const double* cy = wy - wv;
-          const double* cz = wz - wv;
-          fy0 = (1.0 / 6.0) * cy[0] + (2.0 / 3.0) * cy[1] + (1.0 / 6.0) * cy[2];
-          fz0 = (1.0 / 6.0) * cz[0] + (2.0 / 3.0) * cz[1] + (1.0 / 6.0) * cz[2];
-          for (int k = tid; k < -wv; k += NT) { wy[k] = fy0; wz[k] = fz0; }
+      for (int r = 0; r < R; ++r) { Az[r] = 0.0; Af[r] = 0.0; Ay[r] = 0.0; }
+      // one level of taps on the window in buffer b.  The window spans storage indices
+      // [wv, we] (wv even); entries outside the real range [0, P+2] are filled with the
+      // clamped boundary values F_0 / F_{P-1}, so every tap uses the same
+      // 4-term B-spline stencil; the cells whose stencil straddles the boundary
+      // ([-3, -1] and [P-1, P+2]) are clamped cells and get the boundary value directly.
+      auto level = [&](int j, int b) {
+        const Tap1D* tj = tap0 + (j - 1) * L;
+        int wv, we;
+        level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
+        mbar_wait(&bar[b], ph[b]);
+        ph[b] ^= 1u;
+        double* const wy = b ? buf1 : buf0;
+        double* const wz = wy + WM;
+        // clamped boundary values: s(x_0) = (c_{-1} + 4 c_0 + c_1)/6, s(x_{P-1}) likewise
+        double fy0 = 0, fz0 = 0, fy1 = 0, fz1 = 0;
+        const bool left = wv < 0, right = we > P + 2;
+        if (left || right) {                      // edge CTAs only (CTA-uniform)
+          if (left) {
+            const double* cy = wy - wv;
+            const double* cz = wz - wv;
+            fy0 = (1.0 / 6.0) * cy[0] + (2.0 / 3.0) * cy[1] + (1.0 / 6.0) * cy[2];
+            fz0 = (1.0 / 6.0) * cz[0] + (2.0 / 3.0) * cz[1] + (1.0 / 6.0) * cz[2];
+            for (int k = tid; k < -wv; k += NT) { wy[k] = fy0; wz[k] = fz0; }
+          }
+          if (right) {
+            const double* cy = wy + (P - 1 - wv);
+            const double* cz = wz + (P - 1 - wv);
+            fy1 = (1.0 / 6.0) * cy[0] + (2.0 / 3.0) * cy[1] + (1.0 / 6.0) * cy[2];
+            fz1 = (1.0 / 6.0) * cz[0] + (2.0 / 3.0) * cz[1] + (1.0 / 6.0) * cz[2];
+            for (int k = P + 3 - wv + tid; k <= we - wv; k += NT) { wy[k] = fy1; wz[k] = fz1; }
+          }
+          __syncthreads();
         }
-        if (right) {
-          const double* cy = wy + (P - 1 - wv);
-          const double* cz = wz + (P - 1 - wv);
-          fy1 = (1.0 / 6.0) * cy[0] + (2.0 / 3.0) * cy[1] + (1.0 / 6.0) * cy[2];
-          fz1 = (1.0 / 6.0) * cz[0] + (2.0 / 3.0) * cz[1] + (1.0 / 6.0) * cz[2];
-          for (int k = P + 3 - wv + tid; k <= we - wv; k += NT) { wy[k] = fy1; wz[k] = fz1; }
-        }
-        __syncthreads();
-      }
-      drv.at(tlev[j - 1]);
-      const bool yj = (j == s.Ky);
-      const int cl0 = lo + li0;                      // lane's first point
-      const int rel0 = cl0 - wv;                     // ... relative to the window (q = 0)
-      for (int l = chunk; l < L; l += C) {
-        const Tap1D& t = tj[l];
-        const int q = t.q;
-        double yh[R], zh[R];
-        {
-          const double* py = wy + (rel0 + q);
-          const double* pz = wz + (rel0 + q);
-          double c[R + 3];
+        drv.at(tlev[j - 1]);
+        const bool yj = (j == s.Ky);
+        const int cl0 = lo + li0;                      // lane's first point
+        const int rel0 = cl0 - wv;                     // ... relative to the window (q = 0)
+        for (int l = chunk; l < L; l += C) {
+          const Tap1D& t = tj[l];
+          const int q = t.q;
+          double yh[R], zh[R];
+          {
+            const double* py = wy + (rel0 + q);
+            const double* pz = wz + (rel0 + q);
+            double c[R + 3];
 #pragma unroll
-          for (int k = 0; k < R + 3; ++k) c[k] = py[k];
+            for (int k = 0; k < R + 3; ++k) c[k] = py[k];
 #pragma unroll
-          for (int r = 0; r < R; ++r)
-            yh[r] = fma(t.B[0], c[r], fma(t.B[1], c[r + 1], fma(t.B[2], c[r + 2], t.B[3] * c[r + 3])));
+            for (int r = 0; r < R; ++r)
+              yh[r] = fma(t.B[0], c[r], fma(t.B[1], c[r + 1], fma(t.B[2], c[r + 2], t.B[3] * c[r + 3])));
 #pragma unroll
-          for (int k = 0; k < R + 3; ++k) c[k] = pz[k];
+            for (int k = 0; k < R + 3; ++k) c[k] = pz[k];
 #pragma unroll
-          for (int r = 0; r < R; ++r)
-            zh[r] = fma(t.B[0], c[r], fma(t.B[1], c[r + 1], fma(t.B[2], c[r + 2], t.B[3] * c[r + 3])));
-        }
-        const int cb = cl0 + q, ce = cb + R - 1;     // lane's cells
-        if ((left && cb <= -1 && ce >= -3) || (right && cb <= P + 2 && ce >= P - 1)) {
+            for (int r = 0; r < R; ++r)
+              zh[r] = fma(t.B[0], c[r], fma(t.B[1], c[r + 1], fma(t.B[2], c[r + 2], t.B[3] * c[r + 3])));
+          }
+          const int cb = cl0 + q, ce = cb + R - 1;     // lane's cells
+          if ((left && cb <= -1 && ce >= -3) || (right && cb <= P + 2 && ce >= P - 1)) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const int cell = cb + r;
+              if (cell >= -3 && cell <= -1) { yh[r] = fy0; zh[r] = fz0; }
+              if (cell >= P - 1 && cell <= P + 2) { yh[r] = fy1; zh[r] = fz1; }
+            }
+          }
+          if (!active) continue;
+          const double wcz = t.wcz, wgz = t.wgz, wgy = t.wgy;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            const int cell = cb + r;
-            if (cell >= -3 && cell <= -1) { yh[r] = fy0; zh[r] = fz0; }
-            if (cell >= P - 1 && cell <= P + 2) { yh[r] = fy1; zh[r] = fz1; }
+            const double f = drv(yh[r], &zh[r]);
+            Az[r] = fma(wcz, zh[r], fma(wgz, f, Az[r]));
+            Af[r] = fma(wgy, f, Af[r]);
+          }
+          if (yj) {
+            const double wy_ = t.wy;
+#pragma unroll
+            for (int r = 0; r < R; ++r) Ay[r] = fma(wy_, yh[r], Ay[r]);
           }
         }
-        if (!active) continue;
-        const double wcz = t.wcz, wgz = t.wgz, wgy = t.wgy;
+      };
+
+      // levels K, ..., 1, double-buffered: level j-2 streams in while level j is computed
+      for (int j = K; j >= 1; --j) {
+        const int b = (K - j) & 1;
+        level(j, b);
+        if (j <= 6) PHASE_STAMP(1 + j);
+        if (j - 2 >= 1) {                     // refill this buffer with level j-2
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncthreads();
+          if (warp == 0) {
+            if (j - 2 == 1) ring_wait(1);
+            issue_level(j - 2, b);
+          }
+        }
+      }
+      __syncthreads();
+
+      // reduction over node chunks (fixed order) and epilogue
+      double* red = buf0;
+      if (active) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const double f = drv(yh[r], &zh[r]);
-          Az[r] = fma(wcz, zh[r], fma(wgz, f, Az[r]));
-          Af[r] = fma(wgy, f, Af[r]);
+          double* q = red + (chunk * TP + li0 + r) * 3;
+          q[0] = Az[r];
+          q[1] = Af[r];
+          q[2] = Ay[r];
         }
-        if (yj) {
-          const double wy_ = t.wy;
+      }
+      __syncthreads();
+      PHASE_STAMP(8);
+      const double inv_gz0 = 1.0 / s.gz0;
+      for (int t = tid; t < hi - lo; t += NT) {
+        double az = 0.0, af = 0.0, ay = 0.0;
 #pragma unroll
-          for (int r = 0; r < R; ++r) Ay[r] = fma(wy_, yh[r], Ay[r]);
+        for (int c = 0; c < C; ++c) {
+          const double* q = red + (c * TP + t) * 3;
+          az += q[0];
+          af += q[1];
+          ay += q[2];
         }
+        // z: Eq. 20 line 2 (explicit); y: Eq. 20 line 1 by Picard from E[y^{n+Ky}]
+        Driver<DRV, 1> dn(fp.dp);
+        dn.at(tn);
+        const double z = az * inv_gz0;
+        const double rhs = fma(s.ky_dt, af, ay);
+        double y = ay;
+        int itp;
+        for (itp = 1; itp <= s.picard_max; ++itp) {
+          const double yn = fma(s.ky_dt_gy0, dn(y, &z), rhs);
+          const double dy = fabs(yn - y);
+          const bool fixed = (yn == y);     // exact fixed point: the remaining iterations are identities
+          y = yn;
+          if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
+          if (fixed) { itp = s.picard_max; break; }
+        }
+        if (itp > s.picard_max) itp = s.picard_max;
+        const int p = lo + t;
+        vout[p] = y;
+        vout[P + p] = z;
+        s.picard[p] = itp;
+        if (!isfinite(y) || !isfinite(z)) atomicMin(s.bad, (unsigned long long)p);
       }
-    };
-
-    // ---------------- (2)+(3) levels K, ..., 2
-    for (int j = K; j >= 2; --j) {
-      const int b = (K - j) & 1;
-      level(j, b);
-      if (j <= 6) PHASE_STAMP(7 + j);
-      if (j - 2 >= 2) {                     // refill this buffer with level j-2
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (warp == 0) issue_level(j - 2, b);
+      // generic-proxy accesses of the level buffers before later bulk copies into them
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      PHASE_STAMP(9);
+      if (tid == publisher) {
+        if (fz.flag_mode & 1) __threadfence();
+        st_release(pp.done_flag + bid, (unsigned)it + 1);
       }
     }
 
-    // ---------------- (1) this CTA's tile of the level-(n+1) spline -> ring slot of level n+1
-    // the CTAs within D[0] finished step it-1 (their level-(n+1) values exist, and they have
-    // read the value buffer this step overwrites); the CTAs within DK finished step it-3
-    // (nobody still reads the old content of ring slot n+1, level n+1+RS, RS = K+2)
-    fence_proxy_async();
-    if (warp == 0) {
-      if (it > 0) wait_neighbours_warp(pp.done_flag, bid, pp.D[0], nb, (unsigned)it);
-      if (it > 2) wait_neighbours_warp(pp.done_flag, bid, pp.DK, nb, (unsigned)(it - 2));
-    }
-    __syncthreads();
-    // values window [va, vb] of both fields (clamped to the grid); when the grid is long
-    // enough (smemA) every folded index of the odd extension lands inside it
-    const int va = max(base - 3, 0), vb = min(base + Wa + 2, P - 1);
-    const bool smemA = P >= Wa + 2 * kPcrHalo + 96;
-    const int va0 = va & ~1;                                   // field 0 start, even
-    const int va1 = (int)((((int64_t)P + va) & ~(int64_t)1) - P);  // field 1 start (P + va1 even)
-    if (tid == 0 && smemA) {
-      const uint32_t n0b = (uint32_t)((((vb + 1 - va0) + 1) & ~1) * sizeof(double));
-      const uint32_t n1b = (uint32_t)((((vb + 1 - va1) + 1) & ~1) * sizeof(double));
-      mbar_expect_tx(&bar[2], n0b + n1b);
-      bulk_g2s(Fs, vin + va0, n0b, &bar[2]);
-      bulk_g2s(Fs + (WP + 8), vin + ((int64_t)P + va1), n1b, &bar[2]);
-    }
-    {
-      const double* F0 = vin;
-      const double* F1 = vin + P;
-      const double* Fw0 = smemA ? Fs - va0 : F0;                // Fw[k] = F[k] for k in [va, vb]
-      const double* Fw1 = smemA ? Fs + (WP + 8) - va1 : F1;
-      if (smemA) {
-        mbar_wait(&bar[2], ph[2]);
-        ph[2] ^= 1u;
+    // ================= pass 2: spline of every problem's new level n on this CTA's tile
+    for (int ip = 0; ip < bt.nprob; ++ip) {
+      const FusedProb& fp = bt.prob[ip];
+      const Persist1D& pp = fp.pp;
+      if (it >= pp.nsteps) continue;
+      const StepArgs& s = fp.s;
+      const int it_stamp = it;
+      int slot_out;
+      const double* vn;
+      if (pp.ring_mode) {
+        slot_out = (pp.n0 - it) % s.ring_slots;
+        vn = pp.vbuf[(pp.cur + it + 1) & 1];
+      } else {
+        slot_out = s.slot_out;
+        vn = s.values;
       }
+      if (slot_out < 0) continue;
+      PHASE_STAMP(10);
+      // the CTAs within D[0] wrote their level-n values (done flag it+1); the CTAs within DK
+      // finished pass 1 of round it-2, the last reader of ring slot n (level n + K + 2)
+      if (warp == 0) {
+        wait_neighbours_warp(pp.done_flag, bid, pp.D[0], nb, (unsigned)it + 1);
+        if (it >= 2) wait_neighbours_warp(pp.done_flag, bid, pp.DK, nb, (unsigned)(it - 1));
+      }
+      __syncthreads();
+      PHASE_STAMP(11);
+      if (tid == 0) {
+        const uint32_t n0b = (uint32_t)((((vb + 1 - va0) + 1) & ~1) * sizeof(double));
+        const uint32_t n1b = (uint32_t)((((vb + 1 - va1) + 1) & ~1) * sizeof(double));
+        mbar_expect_tx(&bar[2], n0b + n1b);
+        bulk_g2s(Fs, vn + va0, n0b, &bar[2]);
+        bulk_g2s(Fs + (WP + 8), vn + ((int64_t)P + va1), n1b, &bar[2]);
+      }
+      const double* Fw0 = Fs - va0;                 // Fw[k] = F[k] for k in [va, vb]
+      const double* Fw1 = Fs + (WP + 8) - va1;
+      mbar_wait(&bar[2], ph[2]);
+      ph[2] ^= 1u;
+      PHASE_STAMP(12);
       // m_1 and m_{P-2} (not-a-knot end rows), only where the window reaches the ends
       double m1_0 = 0.0, m1_1 = 0.0, mP2_0 = 0.0, mP2_1 = 0.0;
-      if (!smemA || va == 0) {
+      if (va == 0) {
         m1_0 = Fw0[0] - 2.0 * Fw0[1] + Fw0[2];
         m1_1 = Fw1[0] - 2.0 * Fw1[1] + Fw1[2];
       }
-      if (!smemA || vb == P - 1) {
+      if (vb == P - 1) {
         mP2_0 = Fw0[P - 3] - 2.0 * Fw0[P - 2] + Fw0[P - 1];
         mP2_1 = Fw1[P - 3] - 2.0 * Fw1[P - 2] + Fw1[P - 1];
       }
@@ -366,7 +445,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
         T0[WP + p] = r1;
       }
       __syncthreads();
-      PHASE_STAMP(5);
+      PHASE_STAMP(13);
       // constant-coefficient PCR, both fields, two levels per pass where possible:
       //   u = r - a1 (r[-s] + r[+s]),   v = u - a2 (u[-2s] + u[+2s])
       const double* A = T0;
@@ -407,9 +486,9 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
         A = B;
         B = const_cast<double*>(t);
       }
-      PHASE_STAMP(6);
+      PHASE_STAMP(14);
       const double ib = fz.inv_b;
-      double* ring1 = const_cast<double*>(s.ring) + (int64_t)slot[0] * s.slot_elems;
+      double* ringn = const_cast<double*>(s.ring) + (int64_t)slot_out * s.slot_elems;
 #pragma unroll
       for (int f = 0; f < 2; ++f) {
         const double* Fw = f ? Fw1 : Fw0;
@@ -423,7 +502,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
           if (k == P - 1) return 2.0 * mP2 - (P - 3 == 1 ? m1 : mt(P - 3));
           return mt(k);
         };
-        double* rf = ring1 + (int64_t)f * g.cfield;
+        double* rf = ringn + (int64_t)f * g.cfield;
         for (int k = k0 + tid; k < k1; k += NT) {
           double c;
           if (k >= 2 && k <= P - 3) c = Fw[k] - mt(k) * (1.0 / 6.0);
@@ -439,73 +518,16 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(StepArgs s, Grid g, Probl
           rf[k + 1] = c;
         }
       }
-    }
-    __syncthreads();
-    if (tid == 0) {                         // publish the CTA's ring stores (gpu-scope release)
-      __threadfence();
-      st_release(pp.ring_flag + bid, (unsigned)it + 1);
-    }
-    PHASE_STAMP(7);
-
-    // ---------------- level 1: the neighbours' coefficients of level n+1 from the ring
-    {
-      const int b = (K - 1) & 1;
-      if (warp == 0) issue_level(1, b);
-      level(1, b);
-      PHASE_STAMP(8);
-    }
-    __syncthreads();
-    PHASE_STAMP(3);
-
-    // ---------------- (4) reduction over node chunks (fixed order) and epilogue
-    double* red = buf0;
-    if (active) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        double* q = red + (chunk * TP + li0 + r) * 3;
-        q[0] = Az[r];
-        q[1] = Af[r];
-        q[2] = Ay[r];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      PHASE_STAMP(15);
+      // publish the CTA's ring stores: a gpu-scope release by one thread after the CTA
+      // barrier (cumulative over the CTA's stores)
+      if (tid == publisher) {
+        if (fz.flag_mode & 1) __threadfence();
+        st_release(pp.ring_flag + bid, (unsigned)it + 1);
       }
     }
-    __syncthreads();
-    for (int t = tid; t < hi - lo; t += NT) {
-      double az = 0.0, af = 0.0, ay = 0.0;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const double* q = red + (c * TP + t) * 3;
-        az += q[0];
-        af += q[1];
-        ay += q[2];
-      }
-      // z: Eq. 20 line 2 (explicit); y: Eq. 20 line 1 by Picard from E[y^{n+Ky}]
-      Driver<DRV, 1> dn(pb.dp);
-      dn.at(tn);
-      const double z = az * inv_gz0;
-      const double rhs = fma(s.ky_dt, af, ay);
-      double y = ay;
-      int itp;
-      for (itp = 1; itp <= s.picard_max; ++itp) {
-        const double yn = fma(s.ky_dt_gy0, dn(y, &z), rhs);
-        const double dy = fabs(yn - y);
-        const bool fixed = (yn == y);     // exact fixed point: the remaining iterations are identities
-        y = yn;
-        if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
-        if (fixed) { itp = s.picard_max; break; }
-      }
-      if (itp > s.picard_max) itp = s.picard_max;
-      const int p = lo + t;
-      vout[p] = y;
-      vout[P + p] = z;
-      s.picard[p] = itp;
-      if (!isfinite(y) || !isfinite(z)) atomicMin(s.bad, (unsigned long long)p);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release(pp.done_flag + bid, (unsigned)it + 1);
-    }
-    PHASE_STAMP(4);
   }
 }
 
@@ -520,8 +542,8 @@ static const FusedVariant kVariants[] = {
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 int fused1d_num_variants() { return kNumVariants; }
 
-bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int qspan1, int nsm, int variant, Fused1D& fz,
-                      int& threads, int& blocks, size_t& smem) {
+bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int nsm, int variant, Fused1D& fz, int& threads,
+                      int& blocks, size_t& smem) {
   if (variant < 0 || variant >= kNumVariants) return false;
   const FusedVariant v = kVariants[variant];
   const int64_t P = g.P[0];
@@ -529,16 +551,19 @@ bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int qspan1, in
   const int nwpg = v.NT / (32 * v.C);
   fz.variant = variant;
   fz.TP = 32 * nwpg * v.R;
-  if (P < 2 * fz.TP + 2 * kPcrHalo + 256) return false;     // small grids: generic kernel (smemA below)
+  // the pass-2 values window must contain every folded index of the odd extension
+  if (P < 2 * fz.TP + 2 * kPcrHalo + 256) return false;     // small grids: generic kernels
   threads = v.NT;
   blocks = (int)((P + fz.TP - 1) / fz.TP);
-  int wm = fz.TP + qspan_max + 4 + 2;
-  const int wr = (3 * v.C * fz.TP + 3) / 4;               // reduction reuses buf0/buf1
+  fz.WP = ((fz.TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;      // PCR extent of the own tile (+ window slack)
+  int wm = fz.TP + qspan_max + 4 + 2;                        // level window
+  const int wr = (3 * v.C * fz.TP + 3) / 4;                  // reduction (overlays buf0/buf1)
+  const int ws = (6 * fz.WP + 16 + 3) / 4;                   // pass-2 spline scratch (overlays them)
   if (wr > wm) wm = wr;
+  if (ws > wm) wm = ws;
   wm = (wm + 1) & ~1;
   fz.WMAX = wm;
-  fz.WP = ((fz.TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;      // PCR extent of the own tile (+ window slack)
-  smem = 128 + ((size_t)4 * wm + 2 * (size_t)(fz.WP + 8) + 4 * (size_t)fz.WP) * sizeof(double);
+  smem = 128 + (size_t)4 * wm * sizeof(double);
   (void)K; (void)L; (void)nsm;
   return smem <= (v.MB == 1 ? 220 * 1024 : 112 * 1024);
 }
@@ -546,10 +571,10 @@ bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int qspan1, in
 void pcr_constants(double* alpha, double* inv_b);
 
 template <int DRV, int R, int C, int NT, int MB>
-static cudaError_t launch_fused1d(const StepArgs& s, const Grid& g, const Problem& pb, const Fused1D& fz0,
-                                  const Persist1D& pp, int threads, int blocks, size_t smem, cudaStream_t st) {
-  Fused1D fz = fz0;
-  pcr_constants(fz.alpha, &fz.inv_b);
+static cudaError_t launch_fused1d(FusedBatch& bt, int threads, int blocks, size_t smem, cudaStream_t st) {
+  pcr_constants(bt.fz.alpha, &bt.fz.inv_b);
+  const char* fm = getenv("BSDE_FLAG_MODE");        // experiments: bit 0 __threadfence, bit 1 thread 0
+  bt.fz.flag_mode = fm ? atoi(fm) : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)blocks);
   cfg.blockDim = dim3((unsigned)threads);
@@ -560,15 +585,14 @@ static cudaError_t launch_fused1d(const StepArgs& s, const Grid& g, const Proble
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, quad1d_fused<DRV, R, C, NT, MB>, s, g, pb, fz, pp);
+  return cudaLaunchKernelEx(&cfg, quad1d_fused<DRV, R, C, NT, MB>, bt);
 }
 
 template <int DRV>
-static cudaError_t launch_fused1d_v(const StepArgs& s, const Grid& g, const Problem& pb, const Fused1D& fz,
-                                    const Persist1D& pp, int threads, int blocks, size_t smem, cudaStream_t st) {
-  switch (fz.variant) {
+static cudaError_t launch_fused1d_v(FusedBatch& bt, int threads, int blocks, size_t smem, cudaStream_t st) {
+  switch (bt.fz.variant) {
 #define BSDE_V_CASE(i, R, C, NT, MB) \
-    case i: return launch_fused1d<DRV, R, C, NT, MB>(s, g, pb, fz, pp, threads, blocks, smem, st);
+    case i: return launch_fused1d<DRV, R, C, NT, MB>(bt, threads, blocks, smem, st);
     BSDE_FUSED_VARIANTS(BSDE_V_CASE)
 #undef BSDE_V_CASE
   }
@@ -600,33 +624,53 @@ int fused1d_blocks_per_sm(int variant, size_t smem) {
   return e == cudaSuccess ? nb : 0;
 }
 
+// one cooperative launch over nprob problems (round-robin steps); the progress flags of
+// every problem (pp.ring_flag, 2 x blocks) are cleared first
+cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& g, const Fused1D& fz, int driver_id,
+                                 int threads, int blocks, size_t smem, cudaStream_t st) {
+  if (nprob < 1 || nprob > kMaxBatch) return cudaErrorInvalidValue;
+  thread_local static FusedBatch bt;     // ~6 KB: kept off the stack
+  bt = FusedBatch{};
+  bt.fz = fz;
+  bt.g = g;
+  bt.nprob = nprob;
+  bt.max_steps = 0;
+  for (int i = 0; i < nprob; ++i) {
+    bt.prob[i] = probs[i];
+    if (probs[i].pp.nsteps > bt.max_steps) bt.max_steps = probs[i].pp.nsteps;
+    cudaError_t e = cudaMemsetAsync(probs[i].pp.ring_flag, 0, sizeof(unsigned) * 2 * (size_t)blocks, st);
+    if (e != cudaSuccess) return e;
+  }
+  switch (driver_id) {
+    case DRV_ZERO: return launch_fused1d_v<DRV_ZERO>(bt, threads, blocks, smem, st);
+    case DRV_AFFINE: return launch_fused1d_v<DRV_AFFINE>(bt, threads, blocks, smem, st);
+    case DRV_EX1: return launch_fused1d_v<DRV_EX1>(bt, threads, blocks, smem, st);
+    case DRV_EX2: return launch_fused1d_v<DRV_EX2>(bt, threads, blocks, smem, st);
+    case DRV_DIFF: return launch_fused1d_v<DRV_DIFF>(bt, threads, blocks, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 // nsteps consecutive steps (ring_mode 1: levels n0, n0-1, ...) or one step with StepArgs'
 // fields (ring_mode 0); one cooperative launch either way
 cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem& pb, const Fused1D& fz, int n0,
                                  int nsteps, int ring_mode, int cur, double t0, double dt, double* v0, double* v1,
                                  unsigned* flags, const int* D, int DK, int threads, int blocks, size_t smem,
                                  cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(unsigned) * 2 * (size_t)blocks, st);
-  if (e != cudaSuccess) return e;
-  Persist1D pp{};
-  pp.n0 = n0;
-  pp.nsteps = nsteps;
-  pp.ring_mode = ring_mode;
-  pp.cur = cur;
-  pp.t0 = t0;
-  pp.dt = dt;
-  pp.vbuf[0] = v0;
-  pp.vbuf[1] = v1;
-  pp.ring_flag = flags;
-  pp.done_flag = flags + blocks;
-  for (int j = 0; j <= kMaxK; ++j) pp.D[j] = D[j];
-  pp.DK = DK;
-  switch (pb.driver_id) {
-    case DRV_ZERO: return launch_fused1d_v<DRV_ZERO>(s, g, pb, fz, pp, threads, blocks, smem, st);
-    case DRV_AFFINE: return launch_fused1d_v<DRV_AFFINE>(s, g, pb, fz, pp, threads, blocks, smem, st);
-    case DRV_EX1: return launch_fused1d_v<DRV_EX1>(s, g, pb, fz, pp, threads, blocks, smem, st);
-    case DRV_EX2: return launch_fused1d_v<DRV_EX2>(s, g, pb, fz, pp, threads, blocks, smem, st);
-    case DRV_DIFF: return launch_fused1d_v<DRV_DIFF>(s, g, pb, fz, pp, threads, blocks, smem, st);
-  }
-  return cudaErrorInvalidValue;
+  FusedProb fp{};
+  fp.s = s;
+  fp.pp.n0 = n0;
+  fp.pp.nsteps = nsteps;
+  fp.pp.ring_mode = ring_mode;
+  fp.pp.cur = cur;
+  fp.pp.t0 = t0;
+  fp.pp.dt = dt;
+  fp.pp.vbuf[0] = v0;
+  fp.pp.vbuf[1] = v1;
+  fp.pp.ring_flag = flags;
+  fp.pp.done_flag = flags + blocks;
+  for (int j = 0; j <= kMaxK; ++j) fp.pp.D[j] = D[j];
+  fp.pp.DK = DK;
+  for (int i = 0; i < 12; ++i) fp.dp[i] = pb.dp[i];
+  return launch_fused1d_batch(&fp, 1, g, fz, pb.driver_id, threads, blocks, smem, st);
 }

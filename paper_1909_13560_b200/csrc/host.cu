@@ -31,7 +31,7 @@ cudaError_t launch_layer(const Problem& pb, const Grid& g, double t, bool termin
 cudaError_t launch_spline(const Grid& g, const double* values, int F, double* slot, double* tmp0, double* tmp1,
                           cudaStream_t st, int64_t* launches);
 cudaError_t launch_generic_step(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st);
-bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int qspan1, int nsm, int variant, Fused1D& fz,
+bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int nsm, int variant, Fused1D& fz,
                       int& threads, int& blocks, size_t& smem);
 int fused1d_num_variants();
 cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem& pb, const Fused1D& fz, int n0,
@@ -39,6 +39,8 @@ cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem
                                  unsigned* flags, const int* D, int DK, int threads, int blocks, size_t smem,
                                  cudaStream_t st);
 int fused1d_blocks_per_sm(int variant, size_t smem);
+cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& g, const Fused1D& fz, int driver_id,
+                                 int threads, int blocks, size_t smem, cudaStream_t st);
 cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
 cudaError_t init_device_attributes();
 cudaError_t launch_quad2d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, cudaStream_t st);
@@ -65,7 +67,7 @@ struct bsde_ctx {
   bool own_ws = false;
   double* vbuf[2] = {nullptr, nullptr};   // ping-pong value buffers, F * npts each
   int cur = 0;                  // vbuf[cur] holds the newest level
-  int fused_variant = 0;        // fused 1-D kernel variant (kernel_variant >= 10 selects variant - 10)
+  int fused_variant = 0;        // fused 1-D kernel variant (kernel_variant = 10 + v)
   int wc2 = 0, boot_wc2 = 0;    // 2-D fused kernel column window (0: use the generic kernel)
   int nsm = 148;
   double* ring = nullptr;       // (RS + 1) * F * cfield ; slot RS = scratch
@@ -313,7 +315,7 @@ void set_distances(bsde_ctx* c, const std::vector<AxisTap>& t, int K, bsde_ctx::
     const int qa = -t[(size_t)(j - 1) * L].q, qb = t[(size_t)(j - 1) * L + L - 1].q;
     return std::max(qa, qb) + 4;
   };
-  geo.D[0] = (kPcrHalo + 6 + TP - 1) / TP;
+  geo.D[0] = (kPcrHalo + 6 + TP - 1) / TP;     // values halo of the pass-2 own-tile spline
   int dk = geo.D[0];
   for (int j = 1; j <= K; ++j) {
     geo.D[j] = (reach(j) + TP - 1) / TP;
@@ -490,9 +492,10 @@ bsde_status exchange_nccl(bsde_ctx* c);
 // levels n+2..n+K: slots[0] receives the spline of the newest values.  Output -> the other
 // value buffer, which becomes the newest.
 bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, const double* gzl, double dtl,
-                     double tn, const int* slots, int tap_off, int tap1_off, const bsde_ctx::Geo& geo, int variant,
-                     int wc2 = 0) {
+                     double tn, const int* slots, int slot_out, int tap_off, int tap1_off, const bsde_ctx::Geo& geo,
+                     int variant, int wc2 = 0) {
   StepArgs s{};
+  s.slot_out = slot_out;
   s.ring = c->ring;
   s.slot_elems = (int64_t)c->F * c->g.cfield;
   for (int j = 1; j <= Kl; ++j) {
@@ -806,7 +809,10 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   c->bad = (unsigned long long*)(c->ws + lay.bad);
   c->barrier = (unsigned*)(c->ws + lay.barrier);
   c->dres = (double*)(c->ws + lay.dres);
-  if (getenv("BSDE_PHASE_TIMING") && cudaMalloc((void**)&c->phase_ns, (size_t)8 * 16 * 600 * 1100) != cudaSuccess) c->phase_ns = nullptr;
+  if (getenv("BSDE_PHASE_TIMING")) {
+    if (cudaMalloc((void**)&c->phase_ns, (size_t)8 * 32 * 600 * 1100) != cudaSuccess) c->phase_ns = nullptr;
+    else cudaMemset(c->phase_ns, 0, (size_t)8 * 32 * 600 * 1100);
+  }
   // zero the whole ring once: the padding entry c_{P+1} of every line is read with weight 0
   ce = cudaMemsetAsync(c->ring, 0, sizeof(double) * (size_t)(c->RS + 1) * c->F * c->g.cfield, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->picard, 0, sizeof(int32_t) * c->g.npts, c->stream);
@@ -821,7 +827,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     if (fused2d_smem(c->wc2) > 112 * 1024) c->wc2 = 0;
   }
   if (c->d == 1) {
-    c->geo.ok = fused1d_geometry(c->g, c->K, c->L, c->qspan, c->qspan1, c->nsm, c->fused_variant, c->geo.fz,
+    c->geo.ok = fused1d_geometry(c->g, c->K, c->L, c->qspan, c->nsm, c->fused_variant, c->geo.fz,
                                  c->geo.threads, c->geo.blocks, c->geo.smem);
     set_distances(c, c->taps, c->K, c->geo);
   }
@@ -863,10 +869,11 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     const double db = c->dt / Sb;
     std::vector<AxisTap> bt;
     build_taps(c, 1, db, bt, &c->boot_qspan, &c->boot_qspan1);
-    if (c->d == 1)
-      c->boot_geo.ok = fused1d_geometry(c->g, 1, c->L, c->boot_qspan, c->boot_qspan1, c->nsm, c->fused_variant,
+    if (c->d == 1) {
+      c->boot_geo.ok = fused1d_geometry(c->g, 1, c->L, c->boot_qspan, c->nsm, c->fused_variant,
                                         c->boot_geo.fz, c->boot_geo.threads, c->boot_geo.blocks, c->boot_geo.smem);
       set_distances(c, bt, 1, c->boot_geo);
+    }
     if (c->d == 2) {
       c->boot_wc2 = fused2d_window(bt.data(), 1, c->L);
       if (fused2d_smem(c->boot_wc2) > 112 * 1024) c->boot_wc2 = 0;
@@ -892,7 +899,9 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
       for (int s = Sb - 1; s >= 0; --s) {
         const double tn = cfg->t0 + m * c->dt + s * db;
         const int slots[1] = {c->RS};                        // scratch slot
-        if ((st = run_step(c, 1, 1, 1, g1, g1, db, tn, slots, c->boot_tap_off, c->boot_tap1_off, c->boot_geo,
+        // the fused 1-D kernel reads the spline of its input level from the ring: build it
+        if (c->d == 1 && c->boot_geo.ok && (st = spline_into(c, c->RS))) return fail(st);
+        if ((st = run_step(c, 1, 1, 1, g1, g1, db, tn, slots, -1, c->boot_tap_off, c->boot_tap1_off, c->boot_geo,
                            cfg->kernel_variant, c->boot_wc2)))
           return fail(st);
       }
@@ -922,7 +931,7 @@ bsde_status bsde_step(bsde_ctx* c) {
   const int n = c->level - 1;
   int slots[kMaxK];
   for (int j = 1; j <= c->K; ++j) slots[j - 1] = (n + j) % c->RS;   // ring slot of level n+j
-  bsde_status st = run_step(c, c->K, c->Ky, c->Kz, c->gy, c->gz, c->dt, c->cfg.t0 + n * c->dt, slots, c->tap_off,
+  bsde_status st = run_step(c, c->K, c->Ky, c->Kz, c->gy, c->gz, c->dt, c->cfg.t0 + n * c->dt, slots, n % c->RS, c->tap_off,
                             c->tap1_off, c->geo, c->cfg.kernel_variant, c->wc2);
   if (st) return st;
   c->level = n;
@@ -937,6 +946,38 @@ static bsde_status check_bad(bsde_ctx* c) {
   if (bad != ~0ULL)
     return set_err(c, BSDE_ERR_NUMERICAL_DOMAIN, "non-finite y or z at point %llu (level <= %d)", bad, c->level + 1);
   return BSDE_OK;
+}
+
+// StepArgs of a persistent fused launch (ring_mode 1: the kernel derives the per-step slots,
+// times and value buffers from Persist1D)
+static StepArgs persistent_args(const bsde_ctx* c) {
+  StepArgs s{};
+  s.ring = c->ring;
+  s.slot_elems = (int64_t)c->F * c->g.cfield;
+  s.K = c->K; s.Ky = c->Ky; s.Kz = c->Kz; s.L = c->L;
+  s.ring_slots = c->RS;
+  s.tap_off = c->tap_off;
+  s.tap1_off = c->tap1_off;
+  s.gz0 = c->gz[0];
+  s.ky_dt = c->Ky * c->dt;
+  s.ky_dt_gy0 = c->Ky * c->dt * c->gy[0];
+  s.picard_max = c->cfg.picard_max;
+  s.picard_tol = c->cfg.picard_tol;
+  s.picard = c->picard;
+  s.bad = c->bad;
+  s.phase_ns = c->phase_ns;
+  return s;
+}
+
+static void fill_result(bsde_ctx* c, bsde_result* res, const double out[4], double t_sweep, double t_total,
+                        int64_t steps) {
+  memset(res, 0, sizeof *res);
+  res->y0 = out[0];
+  for (int a = 0; a < c->d; ++a) res->z0[a] = out[1 + a];
+  res->t_sweep_s = t_sweep;
+  res->t_total_s = t_total;
+  res->updates = c->g.nown0 * row_len(c) * steps;
+  res->picard_max_used = c->cfg.picard_max;
 }
 
 bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
@@ -954,21 +995,7 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
   const bool fused = c->d == 1 && (c->cfg.kernel_variant == 0 || c->cfg.kernel_variant >= 10) && c->geo.ok &&
                      c->tap1_off >= 0 && getenv("BSDE_NO_PERSISTENT") == nullptr;
   if (fused && c->level >= 2) {
-    StepArgs s{};
-    s.ring = c->ring;
-    s.slot_elems = (int64_t)c->F * c->g.cfield;
-    s.K = c->K; s.Ky = c->Ky; s.Kz = c->Kz; s.L = c->L;
-    s.ring_slots = c->RS;
-    s.tap_off = c->tap_off;
-    s.tap1_off = c->tap1_off;
-    s.gz0 = c->gz[0];
-    s.ky_dt = c->Ky * c->dt;
-    s.ky_dt_gy0 = c->Ky * c->dt * c->gy[0];
-    s.picard_max = c->cfg.picard_max;
-    s.picard_tol = c->cfg.picard_tol;
-    s.picard = c->picard;
-    s.bad = c->bad;
-    s.phase_ns = c->phase_ns;
+    const StepArgs s = persistent_args(c);
     const int ns = c->level;
     cudaError_t e = launch_fused1d_steps(s, c->g, c->pb, c->geo.fz, c->level - 1, ns, 1, c->cur, c->cfg.t0, c->dt, c->vbuf[0],
                                c->vbuf[1], c->barrier, c->geo.D, c->geo.DK, c->geo.threads, c->geo.blocks,
@@ -993,17 +1020,114 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (res) {
-    memset(res, 0, sizeof *res);
     double out[4] = {0, 0, 0, 0};
     if ((st = eval_point(c, out))) return st;
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
-    res->y0 = out[0];
-    for (int a = 0; a < c->d; ++a) res->z0[a] = out[1 + a];
-    res->t_sweep_s = ms * 1e-3;
-    res->t_total_s = now_s() - t0;
-    res->updates = c->g.nown0 * row_len(c) * steps;
-    res->picard_max_used = c->cfg.picard_max;
+    fill_result(c, res, out, ms * 1e-3, now_s() - t0, steps);
+  }
+  return BSDE_OK;
+}
+
+bsde_status bsde_solve_batch(bsde_ctx* const* cs, int32_t n, bsde_result* res) {
+  if (!cs || n < 1 || n > kMaxBatch) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: need 1..%d contexts", kMaxBatch);
+  for (int i = 0; i < n; ++i)
+    if (!cs[i]) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: ctx %d is NULL", i);
+  bsde_ctx* c0 = cs[0];
+  for (int i = 0; i < n; ++i) {
+    const bsde_ctx* c = cs[i];
+    for (int j = 0; j < i; ++j)
+      if (cs[j] == c) return set_err(c0, BSDE_ERR_INVALID_ARGUMENT, "batch: ctx %d repeated", i);
+    const bool fused = c->d == 1 && (c->cfg.kernel_variant == 0 || c->cfg.kernel_variant >= 10) && c->geo.ok &&
+                       c->tap1_off >= 0;
+    if (!fused || c->nranks > 1 || c->grouped)
+      return set_err(c0, BSDE_ERR_INVALID_ARGUMENT, "batch: ctx %d is not a one-rank d = 1 fused-kernel context", i);
+    if (c->cfg.device != c0->cfg.device || c->g.P[0] != c0->g.P[0] || c->g.xlo[0] != c0->g.xlo[0] ||
+        c->g.xhi[0] != c0->g.xhi[0] || c->pb.driver_id != c0->pb.driver_id)
+      return set_err(c0, BSDE_ERR_INVALID_ARGUMENT, "batch: ctx %d differs in device, grid or driver", i);
+    if (c->geo.fz.variant != c0->geo.fz.variant || c->geo.threads != c0->geo.threads || c->geo.blocks != c0->geo.blocks)
+      return set_err(c0, BSDE_ERR_INVALID_ARGUMENT, "batch: ctx %d has another fused-kernel geometry", i);
+  }
+  cudaSetDevice(c0->cfg.device);
+  // common geometry: the largest buffers of the batch
+  Fused1D fz = c0->geo.fz;
+  size_t smem = c0->geo.smem;
+  for (int i = 1; i < n; ++i) {
+    const Fused1D& f = cs[i]->geo.fz;
+    fz.WMAX = std::max(fz.WMAX, f.WMAX);
+    fz.WP = std::max(fz.WP, f.WP);
+    smem = std::max(smem, cs[i]->geo.smem);
+  }
+  const int per_sm = fused1d_blocks_per_sm(fz.variant, smem);
+  if (c0->geo.blocks > c0->nsm * per_sm)
+    return set_err(c0, BSDE_ERR_RESOURCE_LIMIT, "batch: %d CTAs with %zu B of shared memory are not co-resident", c0->geo.blocks, smem);
+  const double t0 = now_s();
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+    return set_err(c0, BSDE_ERR_CUDA, "event create");
+  // order the launch after every context's queued work
+  for (int i = 1; i < n; ++i)
+    if (cs[i]->stream != c0->stream) {
+      cudaEvent_t ev;
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      cudaEventRecord(ev, cs[i]->stream);
+      cudaStreamWaitEvent(c0->stream, ev, 0);
+      cudaEventDestroy(ev);
+    }
+  cudaEventRecord(e0, c0->stream);
+  FusedProb probs[kMaxBatch];
+  int64_t steps[kMaxBatch];
+  for (int i = 0; i < n; ++i) {
+    bsde_ctx* c = cs[i];
+    FusedProb& fp = probs[i];
+    fp = FusedProb{};
+    fp.s = persistent_args(c);
+    fp.pp.n0 = c->level - 1;
+    fp.pp.nsteps = c->level;
+    fp.pp.ring_mode = 1;
+    fp.pp.cur = c->cur;
+    fp.pp.t0 = c->cfg.t0;
+    fp.pp.dt = c->dt;
+    fp.pp.vbuf[0] = c->vbuf[0];
+    fp.pp.vbuf[1] = c->vbuf[1];
+    fp.pp.ring_flag = c->barrier;
+    fp.pp.done_flag = c->barrier + c->geo.blocks;
+    for (int j = 0; j <= kMaxK; ++j) fp.pp.D[j] = c->geo.D[j];
+    fp.pp.DK = c->geo.DK;
+    for (int k = 0; k < 12; ++k) fp.dp[k] = c->pb.dp[k];
+    steps[i] = c->level;
+  }
+  cudaError_t e = launch_fused1d_batch(probs, n, c0->g, fz, c0->pb.driver_id, c0->geo.threads, c0->geo.blocks, smem,
+                                       c0->stream);
+  cudaEventRecord(e1, c0->stream);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return set_err(c0, BSDE_ERR_CUDA, "batch kernel: %s", cudaGetErrorString(e));
+  }
+  for (int i = 0; i < n; ++i) {
+    bsde_ctx* c = cs[i];
+    ++c->launches;
+    c->cur ^= (int)(steps[i] & 1);
+    c->level = 0;
+    if (c->stream != c0->stream) cudaStreamWaitEvent(c->stream, e1, 0);
+  }
+  e = cudaEventSynchronize(e1);
+  float ms = 0;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (e != cudaSuccess) return set_err(c0, BSDE_ERR_CUDA, "batch kernel: %s", cudaGetErrorString(e));
+  for (int i = 0; i < n; ++i) {
+    bsde_status st = check_bad(cs[i]);
+    if (st) return st;
+    if (res) {
+      double out[4] = {0, 0, 0, 0};
+      if ((st = eval_point(cs[i], out))) return st;
+      e = cudaStreamSynchronize(cs[i]->stream);
+      if (e != cudaSuccess) return set_err(cs[i], BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
+      fill_result(cs[i], &res[i], out, ms * 1e-3, now_s() - t0, steps[i]);
+    }
   }
   return BSDE_OK;
 }

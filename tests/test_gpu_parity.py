@@ -206,6 +206,106 @@ def test_cfg2_full_size_parity_unstable_K(K):
     assert lvl == 256 - K + 1 - 48
 
 
+def _fused_persistent_parity(spec, variant):
+    """solve() (one persistent cooperative launch) vs the oracle's full solve; checks that
+    the fused 1-D kernel ran (one launch per step() / solve())."""
+    import oracle
+    from paper_1909_13560_b200 import Solver
+    with Solver(spec, kernel_variant=variant) as s:
+        n0 = s.kernel_launches
+        s.step()
+        assert s.kernel_launches - n0 == 1, "fused 1-D kernel not selected"
+        s.solve()
+        o = oracle.Oracle(spec, nthreads=NT)
+        o.solve()
+        g, r = s.layers(), o.layers()
+        for f in range(g.shape[0]):
+            assert relerr(g[f], r[f]) <= TOL, (variant, f, relerr(g[f], r[f]))
+        assert np.array_equal(s.picard_counts(), o.picard_counts())
+
+
+@gpu
+@pytest.mark.parametrize("K", [1, 3, 6])
+def test_fused_persistent_and_stepwise_parity(K):
+    """The fused 1-D kernel per step (bsde_step) and persistent (bsde_solve) vs the oracle."""
+    spec = W.diff_rates(K, N=24, P=4099)
+    assert_parity(spec, variant=10, every=True)
+    _fused_persistent_parity(spec, 10)
+
+
+@gpu
+def test_fused_persistent_full_size():
+    _fused_persistent_parity(W.cfg2(2), 0)
+
+
+@gpu
+def test_solve_batch_matches_single_solves_and_oracle():
+    """bsde_solve_batch over K = 1..6 (one persistent launch, round-robin steps) gives the
+    same bits as six single solves and matches the oracle (values and Picard counts)."""
+    import oracle
+    from paper_1909_13560_b200 import Solver, solve_batch
+    kv = 10
+    specs = [W.diff_rates(K, N=24, P=4099) for K in range(1, 7)]
+    singles = []
+    for spec in specs:
+        with Solver(spec, kernel_variant=kv) as s:
+            s.solve()
+            singles.append((s.layers(), s.picard_counts()))
+    batch = [Solver(spec, kernel_variant=kv) for spec in specs]
+    try:
+        res = solve_batch(batch)
+        assert len(res) == 6 and all(r.updates > 0 for r in res)
+        for spec, s, (lay, cnt) in zip(specs, batch, singles):
+            assert s.level == 0
+            assert np.array_equal(s.layers(), lay)
+            assert np.array_equal(s.picard_counts(), cnt)
+            o = oracle.Oracle(spec, nthreads=NT)
+            o.solve()
+            r = o.layers()
+            for f in range(2):
+                assert relerr(lay[f], r[f]) <= TOL
+            assert np.array_equal(cnt, o.picard_counts())
+    finally:
+        for s in batch:
+            s.close()
+
+
+@gpu
+def test_solve_batch_full_size_bitwise():
+    """cfg 2 at full size, K = 1..6 batched (the bench's step) == single persistent solves."""
+    from paper_1909_13560_b200 import Solver, solve_batch
+    specs = [W.cfg2(K) for K in range(1, 7)]
+    singles = []
+    for spec in specs:
+        with Solver(spec) as s:
+            s.solve()
+            singles.append(s.layers())
+    batch = [Solver(spec) for spec in specs]
+    try:
+        solve_batch(batch)
+        for s, lay in zip(batch, singles):
+            assert np.array_equal(s.layers(), lay)
+    finally:
+        for s in batch:
+            s.close()
+
+
+@gpu
+def test_solve_batch_rejects_incompatible():
+    from paper_1909_13560_b200 import Solver, solve_batch, BsdeError
+    a = Solver(W.diff_rates(2, N=16, P=4099))
+    b = Solver(W.diff_rates(2, N=16, P=4101))       # another grid
+    c = Solver(W.diff_rates(2, N=16, P=4099), kernel_variant=1)   # generic kernels: not batchable
+    try:
+        for bad in ([a, b], [a, a], [a, c]):
+            with pytest.raises(BsdeError):
+                solve_batch(bad)
+        assert a.level > 0                          # nothing ran
+    finally:
+        for s in (a, b, c):
+            s.close()
+
+
 @gpu
 def test_cfg2_generic_kernel_parity_K6():
     """The generic kernel (variant 1) on the cfg-2 shape at a stable size."""
