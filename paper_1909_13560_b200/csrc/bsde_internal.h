@@ -57,12 +57,17 @@ struct Grid {
   // local row 0 is global row off0, owned rows are local [own0, own0 + nown0); the global
   // axis-0 extent Pg0 is what clamping sees.  One rank: off0 = own0 = 0, nown0 = Pg0 = P[0].
   int64_t off0, Pg0, own0, nown0;
+  // d = 1: every coefficient line carries cpad virtual entries on each side (storage -cpad..-1
+  // and P+3..P+2+cpad) holding the clamped boundary values s(x_0), s(x_{P-1}) of that level
+  // (PAPER.md:385), so the fused kernel's windows need no boundary fill; 0 for d >= 2
+  int64_t cpad;
 };
 
 // Per-step parameters of the fused quadrature / z / Picard kernel (Eq. 20).
 struct StepArgs {
   const double* ring;      // coefficient ring base
   int64_t slot_elems;      // elements per ring slot (F * cfield)
+  int64_t cfield, cpad;    // the context's Grid::cfield / Grid::cpad (batched problems may differ)
   int32_t slot[kMaxK];     // ring slot of level n+j, j = 1..K (index j-1); the generic path
                            // rebuilds slot[0] from values_in at the start of the step
   int32_t slot_out;        // fused 1-D path: ring slot that receives the spline of the new

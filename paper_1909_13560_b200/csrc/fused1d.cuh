@@ -97,10 +97,12 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 // warp 0 waits until flag[b'] >= target for all CTAs b' within distance D of b (one lane per
-// flag, so a satisfied wait costs one acquire round trip)
-__device__ __forceinline__ void wait_neighbours_warp(const unsigned* flag, int b, int D, int nb, unsigned target) {
+// flag, so a satisfied wait costs one round trip); returns the smallest value it observed
+// (warp-uniform), a lower bound of every flag in the range from then on (flags only grow)
+__device__ __forceinline__ unsigned wait_neighbours_warp(const unsigned* flag, int b, int D, int nb, unsigned target) {
   const int lane = threadIdx.x & 31;
   const int a = max(0, b - D), e = min(nb - 1, b + D);
+  unsigned seen = 0xffffffffu;
   for (int q0 = a; q0 <= e; q0 += 32) {
     const int q = q0 + lane;
     bool ok = q > e;
@@ -108,10 +110,23 @@ __device__ __forceinline__ void wait_neighbours_warp(const unsigned* flag, int b
       if (!ok) ok = ld_relaxed(flag + q) >= target;      // relaxed polling (no L1 invalidation)
       if (!__all_sync(0xffffffffu, ok)) __nanosleep(32);
     }
-    if (q <= e) (void)ld_acquire(flag + q);              // synchronises with the release
+    const unsigned v = q <= e ? ld_acquire(flag + q) : 0xffffffffu;   // synchronises with the release
+    seen = min(seen, __reduce_min_sync(0xffffffffu, v));
   }
   __syncwarp();
   if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+  return seen;
+}
+
+// the same with a per-CTA low-water mark *low of the flags within DK (shared memory, touched
+// by warp 0 only): a wait whose target is already covered costs nothing; waits over the DK
+// range raise the mark
+__device__ __forceinline__ void wait_flags(const unsigned* flag, unsigned* low, int b, int D, int DK, int nb,
+                                           unsigned target) {
+  if (*low >= target) return;
+  const unsigned seen = wait_neighbours_warp(flag, b, D, nb, target);
+  if (D >= DK && (threadIdx.x & 31) == 0) *low = seen;
+  __syncwarp();
 }
 
 template <int DRV, int R, int C, int NT, int MB>
@@ -150,11 +165,14 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   const int va1 = (int)((((int64_t)P + va) & ~(int64_t)1) - P);  // field 1 start (P + va1 even)
   const int publisher = fz.flag_mode & 2 ? 0 : NT - 32;     // thread that releases the flags
 
+  // low-water marks of the neighbours' flags per problem: [ip] ring, [kMaxBatch + ip] done
+  unsigned* const lowc = reinterpret_cast<unsigned*>(smem_raw + 64);
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
     fence_mbar_init();
+    for (int i = 0; i < 2 * kMaxBatch; ++i) lowc[i] = 0;
   }
   grid_dep_wait();            // previous kernel in the stream has completed
   __syncthreads();
@@ -196,15 +214,16 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         const Tap1D* tj = tap0 + (j - 1) * L;
         int wv, we;
         level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
-        // real part [s0, s1) of the window (storage 0..P+2), even-aligned for the bulk copy
-        const int s0 = max(wv, 0);
-        const int s1 = (min(we, P + 2) + 2) & ~1;
+        // the whole window [wv, we] (the virtual boundary entries live in the line's pads,
+        // Grid::cpad), even-aligned for the bulk copy
+        const int s0 = wv;
+        const int s1 = (we + 2) & ~1;
         const uint32_t bytes = (uint32_t)((s1 - s0) * sizeof(double));
         const double* Cf = s.ring + (int64_t)slot[j - 1] * s.slot_elems;
-        double* dst = (b ? buf1 : buf0) + (s0 - wv);
+        double* dst = b ? buf1 : buf0;
         mbar_expect_tx(&bar[b], 2 * bytes);
         bulk_g2s(dst, Cf + s0, bytes, &bar[b]);
-        bulk_g2s(dst + WM, Cf + g.cfield + s0, bytes, &bar[b]);
+        bulk_g2s(dst + WM, Cf + s.cfield + s0, bytes, &bar[b]);
       };
       // Level n+j was written by pass 2 of round it-j by the CTAs within D[j]: levels >= 2 are
       // covered by the ring flags of round it-2 within DK, level 1 needs round it-1 within
@@ -212,8 +231,8 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       // barrier here: the previous pass ended with one; the other warps wait on the mbarriers.)
       auto ring_wait = [&](int j) {
         if (it == 0) return;
-        if (j == 1) wait_neighbours_warp(pp.ring_flag, bid, pp.D[1], nb, (unsigned)it);
-        else if (it >= 2) wait_neighbours_warp(pp.ring_flag, bid, pp.DK, nb, (unsigned)(it - 1));
+        if (j == 1) wait_flags(pp.ring_flag, lowc + ip, bid, pp.D[1], pp.DK, nb, (unsigned)it);
+        else if (it >= 2) wait_flags(pp.ring_flag, lowc + ip, bid, pp.DK, pp.DK, nb, (unsigned)(it - 1));
       };
       if (warp == 0) {
         ring_wait(K >= 2 ? 2 : 1);
@@ -242,26 +261,11 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         ph[b] ^= 1u;
         double* const wy = b ? buf1 : buf0;
         double* const wz = wy + WM;
-        // clamped boundary values: s(x_0) = (c_{-1} + 4 c_0 + c_1)/6, s(x_{P-1}) likewise
-        double fy0 = 0, fz0 = 0, fy1 = 0, fz1 = 0;
+        // clamped boundary values s(x_0) = (c_{-1} + 4 c_0 + c_1)/6 and s(x_{P-1}): the
+        // virtual entries of the window (from the line's pads)
         const bool left = wv < 0, right = we > P + 2;
-        if (left || right) {                      // edge CTAs only (CTA-uniform)
-          if (left) {
-            const double* cy = wy - wv;
-            const double* cz = wz - wv;
-            fy0 = (1.0 / 6.0) * cy[0] + (2.0 / 3.0) * cy[1] + (1.0 / 6.0) * cy[2];
-            fz0 = (1.0 / 6.0) * cz[0] + (2.0 / 3.0) * cz[1] + (1.0 / 6.0) * cz[2];
-            for (int k = tid; k < -wv; k += NT) { wy[k] = fy0; wz[k] = fz0; }
-          }
-          if (right) {
-            const double* cy = wy + (P - 1 - wv);
-            const double* cz = wz + (P - 1 - wv);
-            fy1 = (1.0 / 6.0) * cy[0] + (2.0 / 3.0) * cy[1] + (1.0 / 6.0) * cy[2];
-            fz1 = (1.0 / 6.0) * cz[0] + (2.0 / 3.0) * cz[1] + (1.0 / 6.0) * cz[2];
-            for (int k = P + 3 - wv + tid; k <= we - wv; k += NT) { wy[k] = fy1; wz[k] = fz1; }
-          }
-          __syncthreads();
-        }
+        const double fy0 = left ? wy[0] : 0.0, fz0 = left ? wz[0] : 0.0;
+        const double fy1 = right ? wy[we - wv] : 0.0, fz1 = right ? wz[we - wv] : 0.0;
         drv.at(tlev[j - 1]);
         const bool yj = (j == s.Ky);
         const int cl0 = lo + li0;                      // lane's first point
@@ -402,8 +406,9 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       // the CTAs within D[0] wrote their level-n values (done flag it+1); the CTAs within DK
       // finished pass 1 of round it-2, the last reader of ring slot n (level n + K + 2)
       if (warp == 0) {
-        wait_neighbours_warp(pp.done_flag, bid, pp.D[0], nb, (unsigned)it + 1);
-        if (it >= 2) wait_neighbours_warp(pp.done_flag, bid, pp.DK, nb, (unsigned)(it - 1));
+        unsigned* low = lowc + kMaxBatch + ip;
+        if (it >= 2) wait_flags(pp.done_flag, low, bid, pp.DK, pp.DK, nb, (unsigned)(it - 1));
+        wait_flags(pp.done_flag, low, bid, pp.D[0], pp.DK, nb, (unsigned)it + 1);
       }
       __syncthreads();
       PHASE_STAMP(11);
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
           if (k == P - 1) return 2.0 * mP2 - (P - 3 == 1 ? m1 : mt(P - 3));
           return mt(k);
         };
-        double* rf = ringn + (int64_t)f * g.cfield;
+        double* rf = ringn + (int64_t)f * s.cfield;
         for (int k = k0 + tid; k < k1; k += NT) {
           double c;
           if (k >= 2 && k <= P - 3) c = Fw[k] - mt(k) * (1.0 / 6.0);
@@ -516,6 +521,22 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
             c = 6.0 * Fw[P - 1] - 4.0 * cl - cm;
           }
           rf[k + 1] = c;
+        }
+      }
+      if (k0 == -1 || k1 == P + 1) {          // edge CTAs: the line's virtual boundary entries
+        __syncthreads();
+        const int64_t cpad = s.cpad;
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          double* rf = ringn + (int64_t)f * s.cfield;
+          if (k0 == -1) {
+            const double v = (1.0 / 6.0) * rf[0] + (2.0 / 3.0) * rf[1] + (1.0 / 6.0) * rf[2];
+            for (int64_t i = tid; i < cpad; i += NT) rf[-1 - i] = v;
+          }
+          if (k1 == P + 1) {
+            const double v = (1.0 / 6.0) * rf[P - 1] + (2.0 / 3.0) * rf[P] + (1.0 / 6.0) * rf[P + 1];
+            for (int64_t i = tid; i < cpad; i += NT) rf[P + 3 + i] = v;
+          }
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

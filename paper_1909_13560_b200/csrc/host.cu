@@ -431,6 +431,14 @@ void fill_grid(const bsde_config* cfg, Grid& g, double dt) {
   int64_t ext = lastQ;
   for (int a = d - 2; a >= 0; --a) { g.cstride[a] = ext; ext *= g.P[a] + 3; }
   g.cfield = ext;
+  g.cpad = 0;
+  if (d == 1) {
+    // the largest quadrature reach in cells (largest Hermite zero < sqrt(2L+1)) + slack
+    const int K = std::max(cfg->Ky, cfg->Kz);
+    const double reach = std::sqrt(2.0 * K * dt) * std::sqrt(2.0 * cfg->L + 1.0) / g.dx[0];
+    g.cpad = ((int64_t)std::ceil(reach) + 8 + 1) & ~(int64_t)1;
+    g.cfield += 2 * g.cpad;
+  }
   for (int a = d; a < 3; ++a) { g.vstride[a] = 0; g.cstride[a] = 0; }
   g.off0 = 0;
   g.Pg0 = g.P[0];
@@ -498,6 +506,8 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
   s.slot_out = slot_out;
   s.ring = c->ring;
   s.slot_elems = (int64_t)c->F * c->g.cfield;
+  s.cfield = c->g.cfield;
+  s.cpad = c->g.cpad;
   for (int j = 1; j <= Kl; ++j) {
     s.slot[j - 1] = slots[j - 1];
     s.t_level[j - 1] = tn + j * dtl;
@@ -802,7 +812,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   }
   c->vbuf[0] = (double*)(c->ws + lay.values);
   c->vbuf[1] = c->vbuf[0] + (lay.ring - lay.values) / (2 * sizeof(double));
-  c->ring = (double*)(c->ws + lay.ring);
+  c->ring = (double*)(c->ws + lay.ring) + c->g.cpad;      // storage 0 of slot 0, field 0
   c->tmp0 = (double*)(c->ws + lay.tmp0);
   c->tmp1 = (double*)(c->ws + lay.tmp1);
   c->picard = (int32_t*)(c->ws + lay.picard);
@@ -814,7 +824,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     else cudaMemset(c->phase_ns, 0, (size_t)8 * 32 * 600 * 1100);
   }
   // zero the whole ring once: the padding entry c_{P+1} of every line is read with weight 0
-  ce = cudaMemsetAsync(c->ring, 0, sizeof(double) * (size_t)(c->RS + 1) * c->F * c->g.cfield, c->stream);
+  ce = cudaMemsetAsync(c->ring - c->g.cpad, 0, sizeof(double) * (size_t)(c->RS + 1) * c->F * c->g.cfield, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->picard, 0, sizeof(int32_t) * c->g.npts, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->bad, 0xff, sizeof(unsigned long long), c->stream);
   if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "memset: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
@@ -954,6 +964,8 @@ static StepArgs persistent_args(const bsde_ctx* c) {
   StepArgs s{};
   s.ring = c->ring;
   s.slot_elems = (int64_t)c->F * c->g.cfield;
+  s.cfield = c->g.cfield;
+  s.cpad = c->g.cpad;
   s.K = c->K; s.Ky = c->Ky; s.Kz = c->Kz; s.L = c->L;
   s.ring_slots = c->RS;
   s.tap_off = c->tap_off;

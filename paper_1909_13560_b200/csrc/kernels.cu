@@ -271,6 +271,17 @@ static cudaError_t run_pass(PassArgs pa, bool strided, cudaStream_t st, int64_t*
 
 // Tensor-product spline of F fields of `values` (value layout) into a ring slot
 // (coefficient layout): pass along axis 0, then 1, ....
+// d = 1: the virtual boundary entries of every field of a freshly built slot (Grid::cpad)
+__global__ void pad_fill_1d(double* slot, int64_t cfield, int64_t P, int64_t cpad) {
+  double* c = slot + (int64_t)blockIdx.x * cfield;          // storage 0 of field blockIdx.x
+  const double f0 = (1.0 / 6.0) * c[0] + (2.0 / 3.0) * c[1] + (1.0 / 6.0) * c[2];
+  const double f1 = (1.0 / 6.0) * c[P - 1] + (2.0 / 3.0) * c[P] + (1.0 / 6.0) * c[P + 1];
+  for (int64_t i = threadIdx.x; i < cpad; i += blockDim.x) {
+    c[-1 - i] = f0;
+    c[P + 3 + i] = f1;
+  }
+}
+
 cudaError_t launch_spline(const Grid& g, const double* values, int F, double* slot, double* tmp0, double* tmp1,
                           cudaStream_t st, int64_t* launches) {
   const int d = g.d;
@@ -314,6 +325,11 @@ cudaError_t launch_spline(const Grid& g, const double* values, int F, double* sl
       src = dst;
       src_is_values = false;
     }
+  }
+  if (d == 1 && g.cpad > 0) {
+    pad_fill_1d<<<F, 256, 0, st>>>(slot, g.cfield, g.P[0], g.cpad);
+    if (launches) ++*launches;
+    return cudaGetLastError();
   }
   return cudaSuccess;
 }

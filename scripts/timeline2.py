@@ -40,3 +40,9 @@ for K in Ks:
             parts.append(f"{nm}={np.median(d):.2f}/{np.percentile(d, 90):.2f}")
         gap = (a[1:, :, 0] - a[:-1, :, 15])[st]
         print("   ", " ".join(parts), f"| loop={np.median(gap):.2f}")
+        # per-CTA busy time (everything but the two neighbour waits), to find the pacing CTAs
+        busy = (a[:, :, 15] - a[:, :, 0]) - (a[:, :, 1] - a[:, :, 0]) - (a[:, :, 11] - a[:, :, 10])
+        bm = np.median(busy[st], axis=0)
+        idx = np.argsort(bm)[::-1][:12]
+        print("    busy median over CTAs %.2f us; slowest:" % np.median(bm),
+              " ".join(f"{i}:{bm[i]:.2f}" for i in idx))
