@@ -129,6 +129,50 @@ __device__ __forceinline__ void wait_flags(const unsigned* flag, unsigned* low, 
   __syncwarp();
 }
 
+// ring slot of level n+j (j = 1..K) of a problem at round it
+__device__ __forceinline__ int level_slot(const FusedProb& fp, int it, int j) {
+  return fp.pp.ring_mode ? (fp.pp.n0 - it + j) % fp.s.ring_slots : fp.s.slot[j - 1];
+}
+
+// bulk-load the window of level j of problem fp into dst (lane 0 of the calling warp): the
+// whole window [wv, we] (the virtual boundary entries live in the line's pads, Grid::cpad),
+// even-aligned for the bulk copy
+__device__ __forceinline__ void issue_window(const FusedProb& fp, int it, int j, double* dst, int WM, uint64_t* bar,
+                                             int lo, int hi) {
+  if ((threadIdx.x & 31) != 0) return;
+  const int L = fp.s.L;
+  const Tap1D* tj = taps1d(fp.s.tap1_off) + (j - 1) * L;
+  int wv, we;
+  level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
+  const int s1 = (we + 2) & ~1;
+  const uint32_t bytes = (uint32_t)((s1 - wv) * sizeof(double));
+  const double* Cf = fp.s.ring + (int64_t)level_slot(fp, it, j) * fp.s.slot_elems;
+  mbar_expect_tx(bar, 2 * bytes);
+  bulk_g2s(dst, Cf + wv, bytes, bar);
+  bulk_g2s(dst + WM, Cf + fp.s.cfield + wv, bytes, bar);
+}
+
+// Level n+j was written by pass 2 of round it-j by the CTAs within D[j]: levels >= 2 are
+// covered by the ring flags of round it-2 within DK, level 1 needs round it-1 within D[1].
+__device__ __forceinline__ void ring_wait(const FusedProb& fp, unsigned* low, int it, int j, int bid, int nb) {
+  if (it == 0) return;
+  const Persist1D& pp = fp.pp;
+  if (j == 1) wait_flags(pp.ring_flag, low, bid, pp.D[1], pp.DK, nb, (unsigned)it);
+  else if (it >= 2) wait_flags(pp.ring_flag, low, bid, pp.DK, pp.DK, nb, (unsigned)(it - 1));
+}
+
+// the first one or two windows of a problem's step (levels K and K-1; warp 0)
+__device__ __forceinline__ void start_windows(const FusedProb& fp, unsigned* low, int it, double* buf0, double* buf1,
+                                              int WM, uint64_t* bar, int lo, int hi, int bid, int nb) {
+  const int K = fp.s.K;
+  ring_wait(fp, low, it, K >= 2 ? 2 : 1, bid, nb);
+  issue_window(fp, it, K, buf0, WM, &bar[0], lo, hi);
+  if (K >= 2) {
+    if (K == 2) ring_wait(fp, low, it, 1, bid, nb);
+    issue_window(fp, it, K - 1, buf1, WM, &bar[1], lo, hi);
+  }
+}
+
 template <int DRV, int R, int C, int NT, int MB>
 __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ FusedBatch bt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -180,6 +224,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
 
   for (int it = 0; it < bt.max_steps; ++it) {
     // ================= pass 1: levels K..1, z and Picard of step it of every problem
+    bool prefetched = false;                 // the current problem's first windows are in flight
     for (int ip = 0; ip < bt.nprob; ++ip) {
       const FusedProb& fp = bt.prob[ip];
       const Persist1D& pp = fp.pp;
@@ -189,59 +234,26 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       PHASE_STAMP(0);
       const int L = s.L, K = s.K;
       const Tap1D* const tap0 = taps1d(s.tap1_off);
-      int slot[kMaxK];
       double tlev[kMaxK];
       double tn;
       double* vout;
       if (pp.ring_mode) {
         const int n = pp.n0 - it;
 #pragma unroll
-        for (int j = 1; j <= kMaxK; ++j) {
-          slot[j - 1] = (n + j) % s.ring_slots;
-          tlev[j - 1] = pp.t0 + (n + j) * pp.dt;
-        }
+        for (int j = 1; j <= kMaxK; ++j) tlev[j - 1] = pp.t0 + (n + j) * pp.dt;
         tn = pp.t0 + n * pp.dt;
         vout = pp.vbuf[(pp.cur + it + 1) & 1];
       } else {
 #pragma unroll
-        for (int j = 0; j < kMaxK; ++j) { slot[j] = s.slot[j]; tlev[j] = s.t_level[j]; }
+        for (int j = 0; j < kMaxK; ++j) tlev[j] = s.t_level[j];
         tn = s.tn;
         vout = s.values;
       }
-      // bulk-load level j's window into buffer b (lane 0 of warp 0)
-      auto issue_level = [&](int j, int b) {
-        if (lane != 0) return;
-        const Tap1D* tj = tap0 + (j - 1) * L;
-        int wv, we;
-        level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
-        // the whole window [wv, we] (the virtual boundary entries live in the line's pads,
-        // Grid::cpad), even-aligned for the bulk copy
-        const int s0 = wv;
-        const int s1 = (we + 2) & ~1;
-        const uint32_t bytes = (uint32_t)((s1 - s0) * sizeof(double));
-        const double* Cf = s.ring + (int64_t)slot[j - 1] * s.slot_elems;
-        double* dst = b ? buf1 : buf0;
-        mbar_expect_tx(&bar[b], 2 * bytes);
-        bulk_g2s(dst, Cf + s0, bytes, &bar[b]);
-        bulk_g2s(dst + WM, Cf + s.cfield + s0, bytes, &bar[b]);
-      };
-      // Level n+j was written by pass 2 of round it-j by the CTAs within D[j]: levels >= 2 are
-      // covered by the ring flags of round it-2 within DK, level 1 needs round it-1 within
-      // D[1] (waited for just before its window is issued, behind levels K..3).  (No CTA
-      // barrier here: the previous pass ended with one; the other warps wait on the mbarriers.)
-      auto ring_wait = [&](int j) {
-        if (it == 0) return;
-        if (j == 1) wait_flags(pp.ring_flag, lowc + ip, bid, pp.D[1], pp.DK, nb, (unsigned)it);
-        else if (it >= 2) wait_flags(pp.ring_flag, lowc + ip, bid, pp.DK, pp.DK, nb, (unsigned)(it - 1));
-      };
-      if (warp == 0) {
-        ring_wait(K >= 2 ? 2 : 1);
-        issue_level(K, 0);
-        if (K >= 2) {
-          if (K == 2) ring_wait(1);
-          issue_level(K - 1, 1);
-        }
-      }
+      // windows of levels K and K-1 (unless prefetched during the previous problem's
+      // epilogue); later levels are issued behind the computation.  (No CTA barrier here:
+      // the previous pass ended with one; the other warps wait on the mbarriers.)
+      if (!prefetched && warp == 0) start_windows(fp, lowc + ip, it, buf0, buf1, WM, bar, lo, hi, bid, nb);
+      prefetched = false;
       PHASE_STAMP(1);
 
       Driver<DRV, 1> drv(fp.dp);
@@ -323,8 +335,8 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
           if (warp == 0) {
-            if (j - 2 == 1) ring_wait(1);
-            issue_level(j - 2, b);
+            if (j - 2 == 1) ring_wait(fp, lowc + ip, it, 1, bid, nb);
+            issue_window(fp, it, j - 2, b ? buf1 : buf0, WM, &bar[b], lo, hi);
           }
         }
       }
@@ -343,22 +355,42 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       }
       __syncthreads();
       PHASE_STAMP(8);
-      const double inv_gz0 = 1.0 / s.gz0;
-      for (int t = tid; t < hi - lo; t += NT) {
-        double az = 0.0, af = 0.0, ay = 0.0;
+      // the sums of this thread's points (TP <= 2 NT for every variant) into registers, so
+      // the level buffers are free during the epilogue
+      double az[2] = {0.0, 0.0}, af[2] = {0.0, 0.0}, ay[2] = {0.0, 0.0};
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const double* q = red + (c * TP + t) * 3;
-          az += q[0];
-          af += q[1];
-          ay += q[2];
+      for (int u = 0; u < 2; ++u) {
+        const int t = tid + u * NT;
+        if (t < hi - lo) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const double* q = red + (c * TP + t) * 3;
+            az[u] += q[0];
+            af[u] += q[1];
+            ay[u] += q[2];
+          }
         }
+      }
+      // the next problem's first windows stream in during this epilogue
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      for (int iq = ip + 1; iq < bt.nprob; ++iq) {
+        if (it >= bt.prob[iq].pp.nsteps) continue;
+        if (warp == 0) start_windows(bt.prob[iq], lowc + iq, it, buf0, buf1, WM, bar, lo, hi, bid, nb);
+        prefetched = true;
+        break;
+      }
+      const double inv_gz0 = 1.0 / s.gz0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int t = tid + u * NT;
+        if (t >= hi - lo) continue;
         // z: Eq. 20 line 2 (explicit); y: Eq. 20 line 1 by Picard from E[y^{n+Ky}]
         Driver<DRV, 1> dn(fp.dp);
         dn.at(tn);
-        const double z = az * inv_gz0;
-        const double rhs = fma(s.ky_dt, af, ay);
-        double y = ay;
+        const double z = az[u] * inv_gz0;
+        const double rhs = fma(s.ky_dt, af[u], ay[u]);
+        double y = ay[u];
         int itp;
         for (itp = 1; itp <= s.picard_max; ++itp) {
           const double yn = fma(s.ky_dt_gy0, dn(y, &z), rhs);
