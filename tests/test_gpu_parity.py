@@ -518,3 +518,65 @@ def test_2d_fused_matches_generic(spec):
         b.solve()
         for f in range(3):
             assert relerr(a.layer(f), b.layer(f)) <= 1e-13, f
+
+
+def _sample_indices(shape, n_random, band=3):
+    """Flat indices: every point within `band` of a face (the clamped boundary bands) plus
+    n_random interior points drawn with numpy PCG64(1909135600)."""
+    shape = tuple(shape)
+    masks = np.zeros(shape, dtype=bool)
+    for a, P in enumerate(shape):
+        sl = [slice(None)] * len(shape)
+        sl[a] = slice(0, band)
+        masks[tuple(sl)] = True
+        sl[a] = slice(P - band, P)
+        masks[tuple(sl)] = True
+    idx = np.flatnonzero(masks)
+    if idx.size > 40000:
+        idx = idx[np.random.Generator(np.random.PCG64(1909135601)).choice(idx.size, 40000, replace=False)]
+    rng = np.random.Generator(np.random.PCG64(1909135600))
+    rnd = rng.integers(0, int(np.prod(shape)), size=n_random)
+    return np.unique(np.concatenate([idx, rnd]))
+
+
+def _first_step_sampled_parity(spec, n_random, variant=0):
+    """One GPU step of `spec` at its full size vs the oracle's own setup + one step evaluated
+    point by point (orc_step_points) on a sample; values to 1e-11 of the sampled magnitude,
+    identical Picard counts."""
+    import oracle
+    from paper_1909_13560_b200 import Solver
+    with Solver(spec, kernel_variant=variant) as s:
+        s.step()
+        g = s.layers().reshape(1 + spec["d"], -1)
+        pc = s.picard_counts().reshape(-1)
+        shape = s.shape
+    o = oracle.Oracle(spec, nthreads=NT)
+    try:
+        assert o.shape == shape
+        idx = _sample_indices(shape, n_random)
+        ref, pic = o.step_points(idx)
+    finally:
+        o.close()
+    for f in range(g.shape[0]):
+        a, b = g[f][idx], ref[f]
+        err = float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+        assert err <= TOL, (spec.get("name"), f, err)
+    assert np.array_equal(pc[idx], pic)
+    return idx.size
+
+
+@gpu
+def test_cfg4_full_size_first_step_sampled():
+    """cfg 4 (4096^2, K=4, N=128, L=8, exchange option with smoothing) at its full size in the
+    launch configuration of the fused 2-D kernel: the first backward step on every boundary-band
+    point and 2e4 random interior points."""
+    n = _first_step_sampled_parity(W.cfg4(), 20000)
+    assert n > 20000
+
+
+@gpu
+def test_cfg5_shape_first_step_sampled():
+    """cfg 5 shape (3-D geometric basket, differential rates, K=3, N=64, L=8) at 128^3: the
+    first backward step on the boundary bands and 5e3 random points (the full 512^3 oracle
+    needs ~100 GB of host memory for its tensor splines)."""
+    _first_step_sampled_parity(W.basket_3d(3, 64, 8, P=128), 5000)
