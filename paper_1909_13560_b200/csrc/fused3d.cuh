@@ -1,0 +1,304 @@
+// fused3d.cuh -- the d = 3 quadrature path (included by kernels.cu, which owns the constant
+// tap arena).  The hot kernels of BASELINE cfg 5.
+//
+// The tensor-product B-spline value at a tap (l0, l1, l2) is separable:
+//   u(x + s) = sum_c B_c(l2) sum_b B_b(l1) A_l0[i0][c1 + b][c2 + c],
+//   A_l0[i0][y][x] = sum_a B_a(l0) C[c0(i0) + a][y][x]
+// so per level j
+//   (1) `axis0_pass` builds the L planes-stacks A_l0 (one streaming pass over the level's
+//       coefficients per node, axis-0 clamping folded into the per-plane basis);
+//   (2) `quad3d` treats every plane i0 as a 2-D problem with quad2d's structure: for each
+//       (l0, l1) a "row pass" contracts TY + 3 axis-1 lines of A_l0 into TY shared-memory rows
+//       (7 loads per 4 outputs), then the L axis-2 nodes are evaluated on those rows (4 FMA per
+//       field per point), the driver is applied and the folded weights accumulated;
+//       partial sums of the levels are kept in `acc` (5 per point) between launches;
+//   (3) `epilogue_zy` forms z (Eq. 20 line 2) and solves y by Picard (Eq. 20 line 1).
+// Exact algebra: per tap 4 FMA per field instead of the direct 64-term tricubic stencil
+// (DESIGN.md §4).  Axis-1 clamping is per row in the row pass, axis-2 clamping uses the
+// virtual-window extension of the 1-D and 2-D kernels.
+#pragma once
+
+constexpr int k3TY = 4;            // tile rows (axis 1)
+constexpr int k3R = 3;             // points per thread along axis 2 (odd: conflict-free LDS.64)
+constexpr int k3NT = 256;          // threads per CTA
+constexpr int k3TX = k3NT / k3TY * k3R;   // 192 tile columns (axis 2)
+constexpr int k3F = 4;             // fields y, z_0, z_1, z_2
+constexpr int k3Acc = 5;           // accumulators per point: Az_0..2, Af, Ay
+
+// (1) A[l][f][i0][e] = sum_a Bt_a(l, i0) C[f][crow(l, i0) + a][e] over the plane elements e
+__global__ void axis0_pass(const double* __restrict__ C, double* __restrict__ A, Grid g, int tap_off, int j, int L) {
+  const int64_t plane = g.cstride[0];
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= plane) return;
+  const int64_t i0 = blockIdx.y;                   // local storage plane = local value row
+  const int l = blockIdx.z;
+  const AxisTap& ta = axis_taps(tap_off)[(size_t)(j - 1) * 3 * L + l];
+  double Bt[4];
+  const int64_t crow = clamp_cell(i0 + g.off0 + ta.q, g.Pg0, ta.B, Bt) - g.off0;
+  const int64_t P0 = g.P[0];
+#pragma unroll
+  for (int f = 0; f < k3F; ++f) {
+    const double* c = C + (int64_t)f * g.cfield + crow * plane + e;
+    const double v = fma(Bt[0], __ldcg(c), fma(Bt[1], __ldcg(c + plane), fma(Bt[2], __ldcg(c + 2 * plane),
+                                                                              Bt[3] * __ldcg(c + 3 * plane))));
+    A[(((int64_t)l * k3F + f) * P0 + i0) * plane + e] = v;
+  }
+}
+
+// (2) one level of taps for a 4 x 256 tile of plane i0 (own rows only)
+template <int DRV>
+__global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb, int WC, const double* __restrict__ A,
+                                                  double* __restrict__ acc, int j, int first) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* const Rw = reinterpret_cast<double*>(smem_raw);     // [4 fields][TY rows][WC]
+  const int tid = threadIdx.x;
+  const int r = tid / (k3NT / k3TY), lb = tid % (k3NT / k3TY);
+  const int64_t P1 = g.P[1], P2 = g.P[2];
+  const int64_t plane = g.cstride[0], cs1 = g.cstride[1];
+  const int x0 = blockIdx.x * k3TX;
+  const int64_t y0 = (int64_t)blockIdx.y * k3TY;
+  const int64_t i0 = g.own0 + blockIdx.z;                       // local plane
+  const int L = s.L;
+  const int cx0 = x0 + lb * k3R;
+  const int64_t yrow = y0 + r;
+  const bool rowok = yrow < P1;
+  const AxisTap* t0 = axis_taps(s.tap_off) + (size_t)(j - 1) * 3 * L;
+  const AxisTap* t1 = t0 + L;
+  const AxisTap* t2 = t1 + L;
+  const int64_t Afield = g.P[0] * plane;
+
+  Driver<DRV, 3> drv(pb.dp);
+  drv.at(s.t_level[j - 1]);
+  const double czj = s.czj[j - 1], gzj = s.gzj[j - 1], gyj = s.gyj[j - 1];
+  const bool yj = (j == s.Ky);
+  double Az[3][k3R], Af[k3R], Ay[k3R];
+#pragma unroll
+  for (int q = 0; q < k3R; ++q) { Az[0][q] = 0.0; Az[1][q] = 0.0; Az[2][q] = 0.0; Af[q] = 0.0; Ay[q] = 0.0; }
+
+  // column (axis-2) window of this level: storage columns [wv, we] (wv even)
+  const int qmin2 = t2[0].q, qmax2 = t2[L - 1].q;
+  const int wa = x0 + qmin2;
+  const int wv = wa - (wa & 1);
+  const int we = x0 + k3TX - 1 + qmax2 + 3;
+  const int nwin = we - wv + 1;
+  const int s0 = max(wv, 0), s1 = min(we, (int)P2 + 2);        // real columns
+  const bool left = wv < 0, right = we > P2 + 2;
+
+  for (int l0 = 0; l0 < L; ++l0) {
+    const AxisTap& ta = t0[l0];
+    const double* Al = A + (int64_t)l0 * k3F * Afield + i0 * plane;
+    for (int l1 = 0; l1 < L; ++l1) {
+      const AxisTap& tb = t1[l1];
+      // ---- row pass: Rw[f][r'][k] = sum_b B_b A_l0[f][i0][row(r') + b][wv + k], r' < TY
+      {
+        // rows y0 + rr + q (+ 0..3) of the plane; clamped rows (cells < 0 or >= P1 - 1) take
+        // the boundary basis (1/6, 2/3, 1/6, 0) at cell 0 / P1 - 1, computed per row below
+        const int64_t crow0 = y0 + tb.q;
+        const bool consecutive = crow0 >= 0 && crow0 + k3TY - 1 <= P1 - 2;
+        for (int k = s0 - wv + tid; k <= s1 - wv; k += k3NT) {
+#pragma unroll
+          for (int f = 0; f < k3F; ++f) {
+            const double* Cf = Al + (int64_t)f * Afield + wv + k;
+            if (consecutive) {
+              double cin[k3TY + 3];
+#pragma unroll
+              for (int a = 0; a < k3TY + 3; ++a) cin[a] = __ldcg(Cf + (crow0 + a) * cs1);
+#pragma unroll
+              for (int rr = 0; rr < k3TY; ++rr)
+                Rw[(f * k3TY + rr) * WC + k] =
+                    fma(tb.B[0], cin[rr], fma(tb.B[1], cin[rr + 1], fma(tb.B[2], cin[rr + 2], tb.B[3] * cin[rr + 3])));
+            } else {
+#pragma unroll
+              for (int rr = 0; rr < k3TY; ++rr) {
+                double Bt[4];
+                const int64_t cr = clamp_cell(crow0 + rr, P1, tb.B, Bt);
+                const double* Cr = Cf + cr * cs1;
+                Rw[(f * k3TY + rr) * WC + k] =
+                    fma(Bt[0], __ldcg(Cr), fma(Bt[1], __ldcg(Cr + cs1),
+                        fma(Bt[2], __ldcg(Cr + 2 * cs1), Bt[3] * __ldcg(Cr + 3 * cs1))));
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+      // ---- axis-2 boundary: clamped values of every row, virtual window entries
+      double bl[k3F] = {0, 0, 0, 0}, br[k3F] = {0, 0, 0, 0};
+      if (left || right) {
+#pragma unroll
+        for (int f = 0; f < k3F; ++f) {
+          const double* row = Rw + (f * k3TY + r) * WC;
+          if (left) bl[f] = (1.0 / 6.0) * row[-wv] + (2.0 / 3.0) * row[1 - wv] + (1.0 / 6.0) * row[2 - wv];
+          if (right)
+            br[f] = (1.0 / 6.0) * row[P2 - 1 - wv] + (2.0 / 3.0) * row[P2 - wv] + (1.0 / 6.0) * row[P2 + 1 - wv];
+        }
+        __syncthreads();                   // all boundary values read before the fill below
+        for (int idx = tid; idx < k3F * k3TY * nwin; idx += k3NT) {
+          const int k = idx % nwin, fr = idx / nwin;
+          const int sc = wv + k;
+          if (sc >= 0 && sc <= P2 + 2) continue;
+          double* row = Rw + fr * WC;
+          row[k] = sc < 0 ? (1.0 / 6.0) * row[-wv] + (2.0 / 3.0) * row[1 - wv] + (1.0 / 6.0) * row[2 - wv]
+                          : (1.0 / 6.0) * row[P2 - 1 - wv] + (2.0 / 3.0) * row[P2 - wv] + (1.0 / 6.0) * row[P2 + 1 - wv];
+        }
+        __syncthreads();
+      }
+      // ---- column pass over the axis-2 nodes
+      const double W01 = ta.w * tb.w;
+      const double Wcz = W01 * czj, Wgz = W01 * gzj, Wgy = W01 * gyj;
+      const double sa = ta.s, sb = tb.s;
+      const int rel0 = cx0 - wv;
+      for (int m = 0; m < L; ++m) {
+        const AxisTap& tc = t2[m];
+        const int q = tc.q;
+        double v[k3F][k3R];
+#pragma unroll
+        for (int f = 0; f < k3F; ++f) {
+          const double* rp = Rw + (f * k3TY + r) * WC + rel0 + q;
+          double c[k3R + 3];
+#pragma unroll
+          for (int k = 0; k < k3R + 3; ++k) c[k] = rp[k];
+#pragma unroll
+          for (int p = 0; p < k3R; ++p)
+            v[f][p] = fma(tc.B[0], c[p], fma(tc.B[1], c[p + 1], fma(tc.B[2], c[p + 2], tc.B[3] * c[p + 3])));
+        }
+        const int cb = cx0 + q, ce = cb + k3R - 1;
+        if ((left && cb <= -1 && ce >= -3) || (right && cb <= P2 + 2 && ce >= P2 - 1)) {
+#pragma unroll
+          for (int p = 0; p < k3R; ++p) {
+            const int cell = cb + p;
+            if (cell >= -3 && cell <= -1) {
+#pragma unroll
+              for (int f = 0; f < k3F; ++f) v[f][p] = bl[f];
+            }
+            if (cell >= P2 - 1 && cell <= P2 + 2) {
+#pragma unroll
+              for (int f = 0; f < k3F; ++f) v[f][p] = br[f];
+            }
+          }
+        }
+        const double wm = tc.w;
+        const double wcz = Wcz * wm, wgy = Wgy * wm, wg = Wgz * wm;
+        const double wgz0 = wg * sa, wgz1 = wg * sb, wgz2 = wg * tc.s;
+#pragma unroll
+        for (int p = 0; p < k3R; ++p) {
+          const double zz[3] = {v[1][p], v[2][p], v[3][p]};
+          const double f = drv(v[0][p], zz);
+          Az[0][p] = fma(wcz, v[1][p], fma(wgz0, f, Az[0][p]));
+          Az[1][p] = fma(wcz, v[2][p], fma(wgz1, f, Az[1][p]));
+          Az[2][p] = fma(wcz, v[3][p], fma(wgz2, f, Az[2][p]));
+          Af[p] = fma(wgy, f, Af[p]);
+        }
+        if (yj) {
+          const double wy = W01 * wm;
+#pragma unroll
+          for (int p = 0; p < k3R; ++p) Ay[p] = fma(wy, v[0][p], Ay[p]);
+        }
+      }
+      __syncthreads();                     // Rw is rewritten by the next row pass
+    }
+  }
+  // ---- partial sums of this level
+  if (!rowok) return;
+  const int64_t nown = g.nown0 * P1 * P2;
+#pragma unroll
+  for (int p = 0; p < k3R; ++p) {
+    const int64_t col = cx0 + p;
+    if (col >= P2) break;
+    const int64_t o = ((int64_t)blockIdx.z * P1 + yrow) * P2 + col;     // index among the owned points
+    const double vals[k3Acc] = {Az[0][p], Az[1][p], Az[2][p], Af[p], Ay[p]};
+#pragma unroll
+    for (int a = 0; a < k3Acc; ++a) {
+      double* dst = acc + (int64_t)a * nown + o;
+      *dst = first ? vals[a] : *dst + vals[a];
+    }
+  }
+}
+
+// (3) z explicit (Eq. 20 line 2), y by Picard (Eq. 20 line 1) from the accumulated sums
+template <int DRV>
+__global__ void epilogue_zy3(StepArgs s, Grid g, Problem pb, const double* __restrict__ acc) {
+  const int64_t nown = g.nown0 * g.P[1] * g.P[2];
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= nown) return;
+  const double inv_gz0 = 1.0 / s.gz0;
+  Driver<DRV, 3> dn(pb.dp);
+  dn.at(s.tn);
+  const double z[3] = {acc[o] * inv_gz0, acc[nown + o] * inv_gz0, acc[2 * nown + o] * inv_gz0};
+  const double af = acc[3 * nown + o], ay = acc[4 * nown + o];
+  const double rhs = fma(s.ky_dt, af, ay);
+  double y = ay;
+  int it;
+  for (it = 1; it <= s.picard_max; ++it) {
+    const double yn = fma(s.ky_dt_gy0, dn(y, z), rhs);
+    const double dy = fabs(yn - y);
+    const bool fixed = (yn == y);
+    y = yn;
+    if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
+    if (fixed) { it = s.picard_max; break; }
+  }
+  if (it > s.picard_max) it = s.picard_max;
+  const int64_t pidx = g.own0 * g.P[1] * g.P[2] + o;       // local value index
+  s.values[pidx] = y;
+  s.values[g.npts + pidx] = z[0];
+  s.values[2 * g.npts + pidx] = z[1];
+  s.values[3 * g.npts + pidx] = z[2];
+  s.picard[pidx] = it;
+  if (!isfinite(y) || !isfinite(z[0]) || !isfinite(z[1]) || !isfinite(z[2])) atomicMin(s.bad, (unsigned long long)pidx);
+}
+
+// shared memory of quad3d for a column-window width WC (doubles)
+size_t fused3d_smem(int WC) { return (size_t)k3F * k3TY * WC * sizeof(double); }
+
+// the widest axis-2 window over the levels: TX + (q_max - q_min) on axis 2 + 4 + 2
+int fused3d_window(const AxisTap* host_taps, int K, int L) {
+  int span = 0;
+  for (int j = 1; j <= K; ++j) {
+    const AxisTap* t2 = host_taps + ((size_t)(j - 1) * 3 + 2) * L;
+    span = span > t2[L - 1].q - t2[0].q ? span : t2[L - 1].q - t2[0].q;
+  }
+  return k3TX + span + 6;
+}
+
+template <int DRV>
+static cudaError_t launch_step3d_t(const StepArgs& s, const Grid& g, const Problem& pb, int WC, double* A,
+                                   double* acc, cudaStream_t st, int64_t* launches) {
+  const size_t smem = fused3d_smem(WC);
+  const int64_t plane = g.cstride[0];
+  for (int j = 1; j <= s.K; ++j) {
+    const double* C = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
+    dim3 ga((unsigned)((plane + 255) / 256), (unsigned)g.P[0], (unsigned)s.L);
+    axis0_pass<<<ga, 256, 0, st>>>(C, A, g, s.tap_off, j, s.L);
+    dim3 gq((unsigned)((g.P[2] + k3TX - 1) / k3TX), (unsigned)((g.P[1] + k3TY - 1) / k3TY), (unsigned)g.nown0);
+    quad3d<DRV><<<gq, k3NT, smem, st>>>(s, g, pb, WC, A, acc, j, j == 1 ? 1 : 0);
+    if (launches) *launches += 2;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t nown = g.nown0 * g.P[1] * g.P[2];
+  epilogue_zy3<DRV><<<(unsigned)((nown + 255) / 256), 256, 0, st>>>(s, g, pb, acc);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+// one d = 3 step: K x (axis-0 pass + quad3d) + epilogue; A holds L x 4 plane stacks of the
+// local slab, acc 5 x (owned points) doubles
+cudaError_t launch_step3d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, double* A, double* acc,
+                          cudaStream_t st, int64_t* launches) {
+  if (fused3d_smem(WC) > 112 * 1024) return cudaErrorInvalidConfiguration;
+  switch (pb.driver_id) {
+    case DRV_ZERO: return launch_step3d_t<DRV_ZERO>(s, g, pb, WC, A, acc, st, launches);
+    case DRV_AFFINE: return launch_step3d_t<DRV_AFFINE>(s, g, pb, WC, A, acc, st, launches);
+    case DRV_EX1: return launch_step3d_t<DRV_EX1>(s, g, pb, WC, A, acc, st, launches);
+    case DRV_DIFF: return launch_step3d_t<DRV_DIFF>(s, g, pb, WC, A, acc, st, launches);
+  }
+  return cudaErrorInvalidValue;
+}
+
+static cudaError_t set_attr_3d() {
+  cudaError_t e = cudaFuncSetAttribute(quad3d<DRV_ZERO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad3d<DRV_AFFINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad3d<DRV_EX1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad3d<DRV_DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  return e;
+}

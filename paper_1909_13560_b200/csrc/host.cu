@@ -46,6 +46,10 @@ cudaError_t init_device_attributes();
 cudaError_t launch_quad2d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, cudaStream_t st);
 int fused2d_window(const AxisTap* host_taps, int K, int L);
 size_t fused2d_smem(int WC);
+int fused3d_window(const AxisTap* host_taps, int K, int L);
+size_t fused3d_smem(int WC);
+cudaError_t launch_step3d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, double* A, double* acc,
+                          cudaStream_t st, int64_t* launches);
 }  // namespace bsde
 
 using namespace bsde;
@@ -68,13 +72,15 @@ struct bsde_ctx {
   double* vbuf[2] = {nullptr, nullptr};   // ping-pong value buffers, F * npts each
   int cur = 0;                  // vbuf[cur] holds the newest level
   int fused_variant = 0;        // fused 1-D kernel variant (kernel_variant = 10 + v)
-  int wc2 = 0, boot_wc2 = 0;    // 2-D fused kernel column window (0: use the generic kernel)
+  int wc2 = 0, boot_wc2 = 0;    // 2-D / 3-D fused kernel column window (0: use the generic kernel)
   int nsm = 148;
   double* ring = nullptr;       // (RS + 1) * F * cfield ; slot RS = scratch
   int RS = 3;                   // ring slots: K + 2 (level m in slot m % RS; the 2 spare slots let the
                                 // fused kernel's CTAs run up to 2 steps apart without write-after-read hazards)
   double* tmp0 = nullptr;       // cfield
   double* tmp1 = nullptr;       // cfield
+  double* a3 = nullptr;         // d = 3 fused path: L x F plane stacks of one level (axis0_pass)
+  double* acc3 = nullptr;       // d = 3 fused path: 5 partial sums per owned point
   int32_t* picard = nullptr;    // npts
   unsigned long long* bad = nullptr;
   unsigned* barrier = nullptr;  // grid-barrier counter of the persistent fused kernel
@@ -469,12 +475,14 @@ void localize_grid(Grid& g, int64_t lo_e, int64_t hi_e, int64_t r0, int64_t r1) 
 
 
 struct Layout {
-  size_t values, ring, tmp0, tmp1, picard, bad, barrier, dres, total;
+  size_t values, ring, tmp0, tmp1, a3, acc3, picard, bad, barrier, dres, total;
 };
 // values: 2 ping-pong buffers of F * npts (the fused 1-D step reads level n+1 while
 // other CTAs write level n)
 
-Layout layout(const Grid& g, int F, int K) {
+// fused3d: the d = 3 fused path's per-level plane stacks (L x F x local planes) and the
+// 5 partial sums per owned point
+Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   Layout L{};
   size_t off = 0;
@@ -482,6 +490,9 @@ Layout layout(const Grid& g, int F, int K) {
   L.ring = off; off += al(sizeof(double) * (size_t)(K + 3) * F * g.cfield);
   L.tmp0 = off; off += g.d >= 2 ? al(sizeof(double) * g.cfield) : 0;
   L.tmp1 = off; off += g.d >= 3 ? al(sizeof(double) * g.cfield) : 0;
+  const bool f3 = g.d == 3 && fused3d;
+  L.a3 = off; off += f3 ? al(sizeof(double) * (size_t)nodes * F * g.P[0] * g.cstride[0]) : 0;
+  L.acc3 = off; off += f3 ? al(sizeof(double) * 5 * (size_t)g.nown0 * g.P[1] * g.P[2]) : 0;
   L.picard = off; off += al(sizeof(int32_t) * g.npts);
   L.bad = off; off += 256;
   L.barrier = off; off += al(sizeof(unsigned) * 2 * 8192);      // fused-kernel progress flags
@@ -542,6 +553,8 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
     if (e == cudaSuccess) {
       if (c->d == 2 && variant == 0 && wc2 > 0 && c->pb.driver_id != 3)
         e = launch_quad2d(s, c->g, c->pb, wc2, c->stream);
+      else if (c->d == 3 && variant == 0 && wc2 > 0 && c->pb.driver_id != 3 && c->a3 && c->acc3)
+        e = launch_step3d(s, c->g, c->pb, wc2, c->a3, c->acc3, c->stream, &c->launches);
       else
         e = launch_generic_step(s, c->g, c->pb, c->stream);
       ++c->launches;
@@ -720,7 +733,7 @@ bsde_status bsde_query_workspace(const bsde_config* cfg, size_t* bytes) {
   const int K = std::max(cfg->Ky, cfg->Kz);
   Grid g{};
   fill_grid(cfg, g, (cfg->T - cfg->t0) / cfg->N);
-  *bytes = layout(g, 1 + cfg->d, K).total;
+  *bytes = layout(g, 1 + cfg->d, K, cfg->L, cfg->kernel_variant == 0).total;
   return BSDE_OK;
 }
 
@@ -791,7 +804,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     }
   }
   // memory
-  Layout lay = layout(c->g, c->F, c->K);
+  Layout lay = layout(c->g, c->F, c->K, c->L, cfg->kernel_variant == 0);
   if (d_workspace) {
     if (bytes < lay.total) {
       set_err(c, BSDE_ERR_RESOURCE_LIMIT, "workspace of %zu bytes < required %zu", bytes, lay.total);
@@ -815,6 +828,8 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   c->ring = (double*)(c->ws + lay.ring) + c->g.cpad;      // storage 0 of slot 0, field 0
   c->tmp0 = (double*)(c->ws + lay.tmp0);
   c->tmp1 = (double*)(c->ws + lay.tmp1);
+  c->a3 = lay.a3 != lay.acc3 ? (double*)(c->ws + lay.a3) : nullptr;
+  c->acc3 = lay.acc3 != lay.picard ? (double*)(c->ws + lay.acc3) : nullptr;
   c->picard = (int32_t*)(c->ws + lay.picard);
   c->bad = (unsigned long long*)(c->ws + lay.bad);
   c->barrier = (unsigned*)(c->ws + lay.barrier);
@@ -835,6 +850,10 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   if (c->d == 2) {
     c->wc2 = fused2d_window(c->taps.data(), c->K, c->L);
     if (fused2d_smem(c->wc2) > 112 * 1024) c->wc2 = 0;
+  }
+  if (c->d == 3) {
+    c->wc2 = fused3d_window(c->taps.data(), c->K, c->L);
+    if (fused3d_smem(c->wc2) > 112 * 1024) c->wc2 = 0;
   }
   if (c->d == 1) {
     c->geo.ok = fused1d_geometry(c->g, c->K, c->L, c->qspan, c->nsm, c->fused_variant, c->geo.fz,
@@ -887,6 +906,10 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     if (c->d == 2) {
       c->boot_wc2 = fused2d_window(bt.data(), 1, c->L);
       if (fused2d_smem(c->boot_wc2) > 112 * 1024) c->boot_wc2 = 0;
+    }
+    if (c->d == 3) {
+      c->boot_wc2 = fused3d_window(bt.data(), 1, c->L);
+      if (fused3d_smem(c->boot_wc2) > 112 * 1024) c->boot_wc2 = 0;
     }
     const double g1[2] = {0.5, 0.5};
     {

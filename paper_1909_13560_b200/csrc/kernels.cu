@@ -484,6 +484,7 @@ __global__ void __launch_bounds__(256) quad_generic(StepArgs s, Grid g, Problem 
 
 // ------------------------------------------------------------------ 2-D fused quadrature kernel
 #include "fused2d.cuh"
+#include "fused3d.cuh"
 
 template <int D, int DRV>
 static cudaError_t launch_generic(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st) {
@@ -528,6 +529,7 @@ cudaError_t init_device_attributes() {
   if (e == cudaSuccess) e = set_attr_drv<DRV_EX2>();
   if (e == cudaSuccess) e = set_attr_drv<DRV_DIFF>();
   if (e == cudaSuccess) e = set_attr_2d();
+  if (e == cudaSuccess) e = set_attr_3d();
   return e;
 }
 

@@ -419,6 +419,28 @@ def test_3d_parity(spec):
 
 
 @gpu
+def test_3d_fused_parity_oracle():
+    """The fused 3-D path (axis-0 plane stacks + quad3d + epilogue) against the oracle on a
+    cfg-5-shaped problem spanning several tiles along every axis."""
+    spec = W.basket_3d(K=3, N=8, L=8, P=33)
+    spec["npts"] = [29, 33, 203]
+    assert_parity(spec, every=True)
+
+
+@gpu
+@pytest.mark.parametrize("spec", [W.basket_3d(K=3, N=6, L=8, P=40), dict(W.ex1_3d(K=2, N=6, L=6, P=21), npts=[17, 23, 401])],
+                         ids=lambda s: s["name"] + "_" + "x".join(map(str, s["npts"])))
+def test_3d_fused_matches_generic(spec):
+    """quad3d (separable plane/row/column passes) vs the generic direct tricubic stencil."""
+    from paper_1909_13560_b200 import Solver
+    with Solver(spec, kernel_variant=0) as a, Solver(spec, kernel_variant=1) as b:
+        a.solve()
+        b.solve()
+        for f in range(4):
+            assert relerr(a.layer(f), b.layer(f)) <= 1e-13, f
+
+
+@gpu
 def test_determinism_bitwise():
     from paper_1909_13560_b200 import Solver
     spec = W.diff_rates(6, N=32, P=8193)
