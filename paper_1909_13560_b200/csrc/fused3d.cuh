@@ -9,8 +9,9 @@
 //       coefficients per node, axis-0 clamping folded into the per-plane basis);
 //   (2) `quad3d` treats every plane i0 as a 2-D problem with quad2d's structure: for each
 //       (l0, l1) a "row pass" contracts TY + 3 axis-1 lines of A_l0 into TY shared-memory rows
-//       (7 loads per 4 outputs), then the L axis-2 nodes are evaluated on those rows (4 FMA per
-//       field per point), the driver is applied and the folded weights accumulated;
+//       (7 loads per 4 outputs; the raw lines stream in by bulk copies one pair ahead, behind
+//       the previous pair's column pass), then the L axis-2 nodes are evaluated on those rows
+//       (4 FMA per field per point), the driver is applied and the folded weights accumulated;
 //       partial sums of the levels are kept in `acc` (5 per point) between launches;
 //   (3) `epilogue_zy` forms z (Eq. 20 line 2) and solves y by Picard (Eq. 20 line 1).
 // Exact algebra: per tap 4 FMA per field instead of the direct 64-term tricubic stencil
@@ -84,43 +85,77 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
   const int s0 = max(wv, 0), s1 = min(we, (int)P2 + 2);        // real columns
   const bool left = wv < 0, right = we > P2 + 2;
 
+  // raw axis-1 rows of the current (l0, l1) pair: storage rows c0 .. c0 + TY + 2 of plane i0
+  // of A_l0, columns [s0, s0 + nraw), all fields; streamed by bulk copies one pair ahead
+  double* const raw = Rw + (size_t)k3F * k3TY * WC;              // [4 fields][TY + 3][WC]
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(raw + (size_t)k3F * (k3TY + 3) * WC);
+  const int nraw = ((s1 - s0 + 1) + 1) & ~1;
+  auto first_row = [&](int l1) -> int64_t {
+    const int64_t c = y0 + t1[l1].q;
+    return c < 0 ? 0 : (c > P1 - 1 ? P1 - 1 : c);
+  };
+  auto issue_rows = [&](int l0, int l1) {        // thread 0
+    const double* Al = A + (int64_t)l0 * k3F * Afield + i0 * plane + s0;
+    const int64_t c0 = first_row(l1);
+    const int nrows = (int)(P1 + 3 - c0 < k3TY + 3 ? P1 + 3 - c0 : k3TY + 3);
+    const uint32_t bytes = (uint32_t)(nraw * sizeof(double));
+    mbar_expect_tx(bar, bytes * nrows * k3F);
+    for (int f = 0; f < k3F; ++f)
+      for (int a = 0; a < nrows; ++a)
+        bulk_g2s(raw + ((size_t)f * (k3TY + 3) + a) * WC, Al + (int64_t)f * Afield + (c0 + a) * cs1, bytes, bar);
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) issue_rows(0, 0);
+  uint32_t phase = 0;
+
   for (int l0 = 0; l0 < L; ++l0) {
     const AxisTap& ta = t0[l0];
-    const double* Al = A + (int64_t)l0 * k3F * Afield + i0 * plane;
     for (int l1 = 0; l1 < L; ++l1) {
       const AxisTap& tb = t1[l1];
-      // ---- row pass: Rw[f][r'][k] = sum_b B_b A_l0[f][i0][row(r') + b][wv + k], r' < TY
+      // ---- row pass: Rw[f][r'][k] = sum_b B_b A_l0[f][i0][row(r') + b][wv + k], r' < TY, from
+      // the raw rows; clamped rows (cells < 0 or >= P1 - 1) take the boundary basis
+      // (1/6, 2/3, 1/6, 0) at cell 0 / P1 - 1
       {
-        // rows y0 + rr + q (+ 0..3) of the plane; clamped rows (cells < 0 or >= P1 - 1) take
-        // the boundary basis (1/6, 2/3, 1/6, 0) at cell 0 / P1 - 1, computed per row below
-        const int64_t crow0 = y0 + tb.q;
-        const bool consecutive = crow0 >= 0 && crow0 + k3TY - 1 <= P1 - 2;
-        for (int k = s0 - wv + tid; k <= s1 - wv; k += k3NT) {
+        const int64_t cy = y0 + tb.q;                 // cell of tile row 0
+        const int64_t c0 = first_row(l1);
+        const bool consecutive = cy >= 0 && cy + k3TY - 1 <= P1 - 2;
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        for (int k = tid; k < s1 - s0 + 1; k += k3NT) {
 #pragma unroll
           for (int f = 0; f < k3F; ++f) {
-            const double* Cf = Al + (int64_t)f * Afield + wv + k;
+            const double* rc = raw + (size_t)f * (k3TY + 3) * WC + k;
+            double* out = Rw + (size_t)f * k3TY * WC + (s0 - wv) + k;
             if (consecutive) {
               double cin[k3TY + 3];
 #pragma unroll
-              for (int a = 0; a < k3TY + 3; ++a) cin[a] = __ldcg(Cf + (crow0 + a) * cs1);
+              for (int a = 0; a < k3TY + 3; ++a) cin[a] = rc[a * WC];
 #pragma unroll
               for (int rr = 0; rr < k3TY; ++rr)
-                Rw[(f * k3TY + rr) * WC + k] =
+                out[rr * WC] =
                     fma(tb.B[0], cin[rr], fma(tb.B[1], cin[rr + 1], fma(tb.B[2], cin[rr + 2], tb.B[3] * cin[rr + 3])));
             } else {
 #pragma unroll
               for (int rr = 0; rr < k3TY; ++rr) {
                 double Bt[4];
-                const int64_t cr = clamp_cell(crow0 + rr, P1, tb.B, Bt);
-                const double* Cr = Cf + cr * cs1;
-                Rw[(f * k3TY + rr) * WC + k] =
-                    fma(Bt[0], __ldcg(Cr), fma(Bt[1], __ldcg(Cr + cs1),
-                        fma(Bt[2], __ldcg(Cr + 2 * cs1), Bt[3] * __ldcg(Cr + 3 * cs1))));
+                const int64_t cr = clamp_cell(cy + rr, P1, tb.B, Bt) - c0;
+                const double* q = rc + cr * WC;
+                out[rr * WC] = fma(Bt[0], q[0], fma(Bt[1], q[WC], fma(Bt[2], q[2 * WC], Bt[3] * q[3 * WC])));
               }
             }
           }
         }
+        // the raw rows are free: stream the next pair's while this pair's columns are evaluated
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
+        if (tid == 0) {
+          const int n1 = l1 + 1 < L ? l1 + 1 : 0, n0 = l1 + 1 < L ? l0 : l0 + 1;
+          if (n0 < L) issue_rows(n0, n1);
+        }
       }
       // ---- axis-2 boundary: clamped values of every row, virtual window entries
       double bl[k3F] = {0, 0, 0, 0}, br[k3F] = {0, 0, 0, 0};
@@ -248,7 +283,7 @@ __global__ void epilogue_zy3(StepArgs s, Grid g, Problem pb, const double* __res
 }
 
 // shared memory of quad3d for a column-window width WC (doubles)
-size_t fused3d_smem(int WC) { return (size_t)k3F * k3TY * WC * sizeof(double); }
+size_t fused3d_smem(int WC) { return (size_t)k3F * (2 * k3TY + 3) * WC * sizeof(double) + 16; }
 
 // the widest axis-2 window over the levels: TX + (q_max - q_min) on axis 2 + 4 + 2
 int fused3d_window(const AxisTap* host_taps, int K, int L) {
@@ -257,7 +292,7 @@ int fused3d_window(const AxisTap* host_taps, int K, int L) {
     const AxisTap* t2 = host_taps + ((size_t)(j - 1) * 3 + 2) * L;
     span = span > t2[L - 1].q - t2[0].q ? span : t2[L - 1].q - t2[0].q;
   }
-  return k3TX + span + 6;
+  return (k3TX + span + 6 + 1) & ~1;            // even: 16-byte aligned raw rows
 }
 
 template <int DRV>
