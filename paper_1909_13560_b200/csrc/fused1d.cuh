@@ -626,8 +626,7 @@ void pcr_constants(double* alpha, double* inv_b);
 template <int DRV, int R, int C, int NT, int MB>
 static cudaError_t launch_fused1d(FusedBatch& bt, int threads, int blocks, size_t smem, cudaStream_t st) {
   pcr_constants(bt.fz.alpha, &bt.fz.inv_b);
-  const char* fm = getenv("BSDE_FLAG_MODE");        // experiments: bit 0 __threadfence, bit 1 thread 0
-  bt.fz.flag_mode = fm ? atoi(fm) : 0;
+  bt.fz.flag_mode = 0;                             // release by the last warp, no extra fence
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)blocks);
   cfg.blockDim = dim3((unsigned)threads);
