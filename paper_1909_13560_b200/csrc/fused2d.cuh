@@ -18,12 +18,12 @@
 #pragma once
 
 constexpr int k2TY = 4;            // tile rows
-constexpr int k2R = 5;             // points per thread along axis 1
-constexpr int k2NT = 256;          // threads per CTA
-constexpr int k2TX = k2NT / k2TY * k2R;   // 320 tile columns
+constexpr int k2R = 3;             // points per thread along axis 1 (odd: conflict-free LDS.64)
+constexpr int k2NT = 512;          // threads per CTA (one CTA per SM: 16 warps)
+constexpr int k2TX = k2NT / k2TY * k2R;   // 384 tile columns
 
 template <int DRV>
-__global__ void __launch_bounds__(k2NT, 2) quad2d(StepArgs s, Grid g, Problem pb, int WC) {
+__global__ void __launch_bounds__(k2NT, 1) quad2d(StepArgs s, Grid g, Problem pb, int WC) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* const Rw = reinterpret_cast<double*>(smem_raw);     // [3 fields][TY rows][WC]
   const int tid = threadIdx.x;
@@ -43,60 +43,98 @@ __global__ void __launch_bounds__(k2NT, 2) quad2d(StepArgs s, Grid g, Problem pb
 #pragma unroll
   for (int q = 0; q < k2R; ++q) { Az1[q] = 0.0; Az2[q] = 0.0; Af[q] = 0.0; Ay[q] = 0.0; }
 
+  // raw axis-0 rows of the current (level, node) pair: local storage rows first .. first + TY + 2,
+  // columns [s0, s0 + nraw) of the level's window, all fields; streamed by bulk copies one pair
+  // ahead, behind the previous pair's column pass
+  double* const raw = Rw + (size_t)3 * k2TY * WC;                // [3 fields][TY + 3][WC]
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(raw + (size_t)3 * (k2TY + 3) * WC);
+  const int64_t P0loc = g.P[0];
+  auto window = [&](int j, int& wv, int& we) {
+    const AxisTap* t1 = axis_taps(s.tap_off) + ((size_t)(j - 1) * 2 + 1) * L;
+    const int wa = x0 + t1[0].q;
+    wv = wa - (wa & 1);
+    we = x0 + k2TX - 1 + t1[L - 1].q + 3;
+  };
+  auto first_row = [&](int j, int l) -> int64_t {      // local storage row of raw row 0
+    const int64_t c = yl0 + g.off0 + axis_taps(s.tap_off)[(size_t)(j - 1) * 2 * L + l].q;
+    return (c < 0 ? 0 : (c > P0g - 1 ? P0g - 1 : c)) - g.off0;
+  };
+  auto issue_rows = [&](int j, int l) {                 // thread 0
+    int wv, we;
+    window(j, wv, we);
+    const int s0 = max(wv, 0), s1 = min(we, (int)P1 + 2);
+    const int nraw = ((s1 - s0 + 1) + 1) & ~1;
+    const double* Cb = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems + s0;
+    const int64_t c0 = first_row(j, l);
+    const int nrows = (int)(P0loc + 3 - c0 < k2TY + 3 ? P0loc + 3 - c0 : k2TY + 3);
+    const uint32_t bytes = (uint32_t)(nraw * sizeof(double));
+    mbar_expect_tx(bar, bytes * nrows * 3);
+    for (int f = 0; f < 3; ++f)
+      for (int a = 0; a < nrows; ++a)
+        bulk_g2s(raw + ((size_t)f * (k2TY + 3) + a) * WC, Cb + (int64_t)f * g.cfield + (c0 + a) * g.cstride[0], bytes,
+                 bar);
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) issue_rows(1, 0);
+  uint32_t phase = 0;
+
   for (int j = 1; j <= K; ++j) {
     const AxisTap* t0 = axis_taps(s.tap_off) + (j - 1) * 2 * L;     // axis 0 nodes
     const AxisTap* t1 = t0 + L;                                      // axis 1 nodes
-    const double* Cb = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
     drv.at(s.t_level[j - 1]);
     const double czj = s.czj[j - 1], gzj = s.gzj[j - 1], gyj = s.gyj[j - 1];
     const bool yj = (j == s.Ky);
     // column window of this level: storage columns [wv, we] (wv even)
-    const int qmin2 = t1[0].q, qmax2 = t1[L - 1].q;
-    const int wa = x0 + qmin2;
-    const int wv = wa - (wa & 1);
-    const int we = x0 + k2TX - 1 + qmax2 + 3;
+    int wv, we;
+    window(j, wv, we);
     const int nwin = we - wv + 1;
     const int s0 = max(wv, 0), s1 = min(we, (int)P1 + 2);          // real columns
     const bool left = wv < 0, right = we > P1 + 2;
     for (int l = 0; l < L; ++l) {
       const AxisTap& ta = t0[l];
-      // ---- row pass: Rw[f][r'][k] = sum_a B_a C[f][row(r') + a][wv + k], r' < TY
+      // ---- row pass: Rw[f][r'][k] = sum_a B_a C[f][row(r') + a][wv + k], r' < TY, from the raw
+      // rows; clamped rows (global cells < 0 or >= P0 - 1) take the boundary basis
       {
-        // per tile row: clamped axis-0 cell (global), local storage row, basis
-        int64_t crow[k2TY];
-        double Bt[k2TY][4];
-        bool consecutive = true;
-#pragma unroll
-        for (int rr = 0; rr < k2TY; ++rr) {
-          const int64_t gcell = yl0 + rr + g.off0 + ta.q;
-          crow[rr] = clamp_cell(gcell, P0g, ta.B, Bt[rr]) - g.off0;    // local storage row of a = 0
-          if (gcell < 0 || gcell > P0g - 2) consecutive = false;        // clamped row (cell P0-1 too)
-        }
-        const int64_t cs0 = g.cstride[0];
-        for (int k = s0 - wv + tid; k <= s1 - wv; k += k2NT) {
+        const int64_t cy = yl0 + g.off0 + ta.q;                       // global cell of tile row 0
+        const int64_t c0 = first_row(j, l);
+        const bool consecutive = cy >= 0 && cy + k2TY - 1 <= P0g - 2;
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        for (int k = tid; k < s1 - s0 + 1; k += k2NT) {
 #pragma unroll
           for (int f = 0; f < 3; ++f) {
-            const double* Cf = Cb + (int64_t)f * g.cfield + wv + k;
+            const double* rc = raw + (size_t)f * (k2TY + 3) * WC + k;
+            double* out = Rw + (size_t)f * k2TY * WC + (s0 - wv) + k;
             if (consecutive) {
               double cin[k2TY + 3];
 #pragma unroll
-              for (int a = 0; a < k2TY + 3; ++a) cin[a] = __ldcg(Cf + (crow[0] + a) * cs0);
+              for (int a = 0; a < k2TY + 3; ++a) cin[a] = rc[a * WC];
 #pragma unroll
               for (int rr = 0; rr < k2TY; ++rr)
-                Rw[(f * k2TY + rr) * WC + k] =
+                out[rr * WC] =
                     fma(ta.B[0], cin[rr], fma(ta.B[1], cin[rr + 1], fma(ta.B[2], cin[rr + 2], ta.B[3] * cin[rr + 3])));
             } else {
 #pragma unroll
               for (int rr = 0; rr < k2TY; ++rr) {
-                const double* Cr = Cf + crow[rr] * cs0;
-                Rw[(f * k2TY + rr) * WC + k] =
-                    fma(Bt[rr][0], __ldcg(Cr), fma(Bt[rr][1], __ldcg(Cr + cs0),
-                        fma(Bt[rr][2], __ldcg(Cr + 2 * cs0), Bt[rr][3] * __ldcg(Cr + 3 * cs0))));
+                double Bt[4];
+                const int64_t cr = clamp_cell(cy + rr, P0g, ta.B, Bt) - g.off0 - c0;
+                const double* q = rc + cr * WC;
+                out[rr * WC] = fma(Bt[0], q[0], fma(Bt[1], q[WC], fma(Bt[2], q[2 * WC], Bt[3] * q[3 * WC])));
               }
             }
           }
         }
+        // the raw rows are free: stream the next pair's behind this pair's column pass
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
+        if (tid == 0) {
+          if (l + 1 < L) issue_rows(j, l + 1);
+          else if (j + 1 <= K) issue_rows(j + 1, 0);
+        }
       }
       // ---- axis-1 boundary: clamped values of every row, virtual window entries
       double bl[3] = {0, 0, 0}, br[3] = {0, 0, 0};     // this thread's row
@@ -209,7 +247,7 @@ __global__ void __launch_bounds__(k2NT, 2) quad2d(StepArgs s, Grid g, Problem pb
 }
 
 // shared memory of quad2d for a column-window width WC (doubles)
-size_t fused2d_smem(int WC) { return (size_t)3 * k2TY * WC * sizeof(double); }
+size_t fused2d_smem(int WC) { return (size_t)3 * (2 * k2TY + 3) * WC * sizeof(double) + 16; }
 
 // the widest column window over the levels: TX + (q_max - q_min) on axis 1 + 4 + 2
 int fused2d_window(const AxisTap* host_taps, int K, int L) {
@@ -218,7 +256,7 @@ int fused2d_window(const AxisTap* host_taps, int K, int L) {
     const AxisTap* t1 = host_taps + ((size_t)(j - 1) * 2 + 1) * L;
     span = span > t1[L - 1].q - t1[0].q ? span : t1[L - 1].q - t1[0].q;
   }
-  return k2TX + span + 6;
+  return (k2TX + span + 6 + 1) & ~1;            // even: 16-byte aligned raw rows
 }
 
 template <int DRV>
@@ -230,7 +268,7 @@ static cudaError_t launch_quad2d_t(const StepArgs& s, const Grid& g, const Probl
 }
 
 cudaError_t launch_quad2d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, cudaStream_t st) {
-  if (fused2d_smem(WC) > 112 * 1024) return cudaErrorInvalidConfiguration;
+  if (fused2d_smem(WC) > 220 * 1024) return cudaErrorInvalidConfiguration;
   switch (pb.driver_id) {
     case DRV_ZERO: return launch_quad2d_t<DRV_ZERO>(s, g, pb, WC, st);
     case DRV_AFFINE: return launch_quad2d_t<DRV_AFFINE>(s, g, pb, WC, st);
@@ -241,9 +279,9 @@ cudaError_t launch_quad2d(const StepArgs& s, const Grid& g, const Problem& pb, i
 }
 
 static cudaError_t set_attr_2d() {
-  cudaError_t e = cudaFuncSetAttribute(quad2d<DRV_ZERO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad2d<DRV_AFFINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad2d<DRV_EX1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad2d<DRV_DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(quad2d<DRV_ZERO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad2d<DRV_AFFINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad2d<DRV_EX1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad2d<DRV_DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   return e;
 }

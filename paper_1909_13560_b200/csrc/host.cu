@@ -849,7 +849,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
   if (c->d == 2) {
     c->wc2 = fused2d_window(c->taps.data(), c->K, c->L);
-    if (fused2d_smem(c->wc2) > 112 * 1024) c->wc2 = 0;
+    if (fused2d_smem(c->wc2) > 220 * 1024) c->wc2 = 0;
   }
   if (c->d == 3) {
     c->wc2 = fused3d_window(c->taps.data(), c->K, c->L);
@@ -905,7 +905,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     }
     if (c->d == 2) {
       c->boot_wc2 = fused2d_window(bt.data(), 1, c->L);
-      if (fused2d_smem(c->boot_wc2) > 112 * 1024) c->boot_wc2 = 0;
+      if (fused2d_smem(c->boot_wc2) > 220 * 1024) c->boot_wc2 = 0;
     }
     if (c->d == 3) {
       c->boot_wc2 = fused3d_window(bt.data(), 1, c->L);
