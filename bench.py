@@ -220,11 +220,83 @@ def run_ours(args):
            "reference_solution": list(W.reference_solution(specs[1])[:1]) + [W.reference_solution(specs[1])[1][0]]}
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0 and not args.no_tts:
+        out["tts"] = tts_sweep(dev)
     if rank == 0:
         print(json.dumps(out))
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+TTS_NS = [16, 32, 64, 128, 256, 512, 1024]
+TTS_EPS = {"ex1": [1e-6, 1e-8, 1e-10, 1e-12], "ex2": [1e-6, 1e-8]}
+
+
+def tts_sweep(dev, oracle_budget_s=90.0):
+    """Time-to-solution at fixed error (BASELINE metric): for Ex. 1 and Ex. 2
+    (closed forms y0 = 1/2, ln 3) on the (K, N) grid K = 1..6 x N = 16..1024 (L = 32, balanced
+    grid), the smallest wall time from bsde_setup to bsde_solve's return among runs with
+    |y0 - y_exact| <= eps.  The oracle is timed on the same runs (identical y0 by parity), the
+    two cheapest qualifying (K, N) per eps, within a bounded budget."""
+    from paper_1909_13560_b200 import Solver, workloads as W
+    out = {}
+    for prob in ("ex1", "ex2"):
+        mk = W.ex1 if prob == "ex1" else W.ex2
+        exact = W.reference_solution(mk(1, 16))[0]
+        with Solver(mk(3, 64), device=dev) as s:          # warm-up (context, caches)
+            s.solve()
+        runs = []
+        for K in range(1, 7):
+            for N in TTS_NS:
+                if N < K + 1:
+                    continue
+                spec = mk(K, N)
+                t0 = time.perf_counter()
+                try:
+                    with Solver(spec, device=dev) as s:
+                        r = s.solve()
+                        P = s.shape[0]
+                except Exception:                          # e.g. a non-finite solution (unstable K, N)
+                    continue
+                t = time.perf_counter() - t0
+                runs.append({"K": K, "N": N, "P": P, "s": t, "err": abs(r.y0 - exact),
+                             "work": P * (N - K + 1) * K})
+        res = {}
+        for eps in TTS_EPS[prob]:
+            ok = [r for r in runs if r["err"] <= eps]
+            if not ok:
+                res[f"{eps:g}"] = {"gpu": None, "note": "no (K, N) of the grid reaches this error"}
+                continue
+            best = min(ok, key=lambda r: r["s"])
+            res[f"{eps:g}"] = {"gpu": {"s": best["s"], "K": best["K"], "N": best["N"], "P": best["P"],
+                                       "err": best["err"]},
+                               "candidates": sorted(ok, key=lambda r: r["work"])[:2]}
+        out[prob] = res
+    # the oracle on the cheapest qualifying runs
+    import oracle
+    nthreads = os.cpu_count() or 1
+    spent = 0.0
+    for prob, res in out.items():
+        mk = W.ex1 if prob == "ex1" else W.ex2
+        for eps, e in res.items():
+            cands = e.pop("candidates", [])
+            best = None
+            for c in cands:
+                est = c["work"] * 32 * 40e-9 / nthreads              # ~40 ns per tap per core
+                if spent + est > oracle_budget_s:
+                    continue
+                t0 = time.perf_counter()
+                o = oracle.Oracle(mk(c["K"], c["N"]), nthreads=nthreads)
+                y0, _ = o.solve()
+                o.close()
+                t = time.perf_counter() - t0
+                spent += t
+                if best is None or t < best["s"]:
+                    best = {"s": t, "K": c["K"], "N": c["N"], "err": abs(y0 - W.reference_solution(mk(1, 16))[0])}
+            e["oracle"] = best if best is not None else "not measured (budget)"
+    return {"grid": "K=1..6 x N=16..1024, L=32, balanced P (SURVEY A.1), wall time setup+solve",
+            "oracle_cores": nthreads, "results": out}
 
 
 def _oracle_sample(max_seconds=15.0, steps_per_K=120):
@@ -291,6 +363,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution sweep")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
