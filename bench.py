@@ -222,6 +222,8 @@ def run_ours(args):
         out["cpu_baseline"] = cpu_baseline(args)
     if rank == 0 and not args.no_tts:
         out["tts"] = tts_sweep(dev)
+    if rank == 0 and world == 1 and not args.no_d23:
+        out["d23_configs"] = d23_configs(dev, stream)
     if rank == 0:
         print(json.dumps(out))
     if dist:
@@ -299,6 +301,39 @@ def tts_sweep(dev, oracle_budget_s=90.0):
             "oracle_cores": nthreads, "results": out}
 
 
+# algorithmic FP64 flops per point-step of the d >= 2 configs (separable evaluation, FMA = 2;
+# DESIGN.md §5): per tap F x 4 FMA (last axis) + the staged row/plane passes' share + driver +
+# accumulation, K L^d taps, + Picard + spline passes
+FLOPS_CFG4 = 4 * 64 * (24 + 3 + 6 + 10) + 2 * 64 + 30 * 8 + 3 * 2 * 21
+FLOPS_CFG5 = 3 * 512 * (32 + 4 + 18 + 14) + 2 * 512 + 30 * 22 + 4 * 3 * 21
+
+
+def d23_configs(dev, stream):
+    """cfg 4 and cfg 5 at their full sizes: device time of backward steps (after one warm-up
+    step) through bsde_step, with the FP64 fraction of the derived peak.  Setup untimed."""
+    import torch
+    from paper_1909_13560_b200 import Solver, workloads as W
+    out = {}
+    for name, spec, steps, fl in (("cfg4", W.cfg4(), 3, FLOPS_CFG4), ("cfg5", W.basket_3d(3, 64, 8, P=512), 2, FLOPS_CFG5)):
+        with Solver(spec, device=dev, stream=stream) as s:
+            npts = 1
+            for n in s.shape:
+                npts *= n
+            s.step()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):
+                s.step()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+        ups = npts / (ms * 1e-3)
+        out[name] = {"workload": spec["name"], "points": npts, "ms_per_step": ms, "updates_per_s": ups,
+                     "flops_per_point_step": fl, "tflops": fl * ups / 1e12,
+                     "frac_fp64_peak": fl * ups / 1e12 / peak_fp64_tflops(1965.0)}
+    return out
+
+
 def _oracle_sample(max_seconds=15.0, steps_per_K=120):
     """Time the oracle (as it stands) on a bounded sample of cfg 2: steps_per_K backward
     steps of each K after its (untimed) setup."""
@@ -364,6 +399,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution sweep")
+    ap.add_argument("--no-d23", action="store_true", help="skip the cfg 4 / cfg 5 step timings")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
