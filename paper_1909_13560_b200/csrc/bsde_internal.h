@@ -96,7 +96,6 @@ struct Fused1D {
   int TP;                    // points per CTA
   int WMAX;                  // doubles per field buffer in shared memory
   int WP;                    // doubles per PCR scratch array (own-tile spline)
-  int flag_mode;             // progress-flag release: bit 0 full fence first, bit 1 by thread 0
   double alpha[kPcrLevels];  // PCR elimination ratios
   double inv_b;              // 1 / b after the last PCR level
 };

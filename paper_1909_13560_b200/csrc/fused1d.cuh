@@ -39,11 +39,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
                  : "=r"(done) : "r"(smem_addr(bar)), "r"(phase) : "memory");
   } while (!done);
 }
-// order generic-proxy accesses (smem and global) before subsequent async-proxy (bulk copy) ones
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -56,7 +51,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
       s.phase_ns[((size_t)it_stamp * gridDim.x + blockIdx.x) * 32 + (i)] = gtimer();              \
   } while (0)
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -66,15 +60,6 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
-}
-
-// window of level j: storage indices [clo, clo + nwin) of the coefficient array
-__device__ __forceinline__ void level_window(int qmin, int qmax, int64_t lo, int64_t hi, int64_t P,
-                                             int64_t& clo, int& nwin) {
-  const int64_t a = lo + qmin, b = hi - 1 + qmax;                 // nodes ascending
-  clo = max((int64_t)0, min(a, P - 1));
-  const int64_t chi = max((int64_t)0, min(b, P - 1));
-  nwin = (int)(chi - clo + 4);
 }
 
 // span [wv, we] (storage indices, wv even) of the window of a level whose node offsets
@@ -207,7 +192,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   const int va = max(base - 3, 0), vb = min(base + Wa + 2, P - 1);
   const int va0 = va & ~1;                                   // field 0 start, even
   const int va1 = (int)((((int64_t)P + va) & ~(int64_t)1) - P);  // field 1 start (P + va1 even)
-  const int publisher = fz.flag_mode & 2 ? 0 : NT - 32;     // thread that releases the flags
+  const int publisher = NT - 32;  // thread that releases the flags (the last warp pays the fence)
 
   // low-water marks of the neighbours' flags per problem: [ip] ring, [kMaxBatch + ip] done
   unsigned* const lowc = reinterpret_cast<unsigned*>(smem_raw + 64);
@@ -411,10 +396,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       PHASE_STAMP(9);
-      if (tid == publisher) {
-        if (fz.flag_mode & 1) __threadfence();
-        st_release(pp.done_flag + bid, (unsigned)it + 1);
-      }
+      if (tid == publisher) st_release(pp.done_flag + bid, (unsigned)it + 1);
     }
 
     // ================= pass 2: spline of every problem's new level n on this CTA's tile
@@ -576,10 +558,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       PHASE_STAMP(15);
       // publish the CTA's ring stores: a gpu-scope release by one thread after the CTA
       // barrier (cumulative over the CTA's stores)
-      if (tid == publisher) {
-        if (fz.flag_mode & 1) __threadfence();
-        st_release(pp.ring_flag + bid, (unsigned)it + 1);
-      }
+      if (tid == publisher) st_release(pp.ring_flag + bid, (unsigned)it + 1);
     }
   }
 }
@@ -626,7 +605,6 @@ void pcr_constants(double* alpha, double* inv_b);
 template <int DRV, int R, int C, int NT, int MB>
 static cudaError_t launch_fused1d(FusedBatch& bt, int threads, int blocks, size_t smem, cudaStream_t st) {
   pcr_constants(bt.fz.alpha, &bt.fz.inv_b);
-  bt.fz.flag_mode = 0;                             // release by the last warp, no extra fence
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)blocks);
   cfg.blockDim = dim3((unsigned)threads);
