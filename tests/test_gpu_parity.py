@@ -602,3 +602,33 @@ def test_cfg5_shape_first_step_sampled():
     first backward step on the boundary bands and 5e3 random points (the full 512^3 oracle
     needs ~100 GB of host memory for its tensor splines)."""
     _first_step_sampled_parity(W.basket_3d(3, 64, 8, P=128), 5000)
+
+
+def _printed_rows():
+    rows = []
+    with open(os.path.join(os.path.dirname(__file__), "golden", "printed_errors.txt")) as fh:
+        for line in fh:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line.split())
+    return rows
+
+
+@gpu
+@pytest.mark.parametrize("row", _printed_rows(), ids=lambda r: f"{r[0]}_K{r[1]}_N{r[2]}")
+def test_gpu_reproduces_printed_errors(row):
+    """Every error row the paper prints for Ex. 1/2 (Tables 4-5, up to N = 1024) and Ex. 4
+    (Table 9) reproduced by the GPU path at the paper's sizes (balanced grids, L = 32 / 8),
+    to the 3 % the oracle pins use (tests/golden/printed_errors.txt, cited per row)."""
+    from paper_1909_13560_b200 import Solver
+    ex, K, N, M, ye, ze, _ = row
+    K, N = int(K), int(N)
+    spec = {"ex1": W.ex1, "ex2": W.ex2}[ex](K, N) if ex != "ex4" else W.ex4_2d(K, N)
+    with Solver(spec) as s:
+        assert s.shape[0] == int(M) + 1
+        r = s.solve()
+    ref = W.reference_solution(spec)
+    ey = abs(r.y0 - ref[0])
+    ez = float(np.sqrt(sum((r.z0[k] - ref[1][k]) ** 2 for k in range(spec["d"]))))
+    assert abs(ey / float(ye) - 1) <= 0.03, (ey, ye)
+    assert abs(ez / float(ze) - 1) <= 0.03, (ez, ze)
