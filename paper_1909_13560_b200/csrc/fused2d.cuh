@@ -146,16 +146,20 @@ __global__ void __launch_bounds__(k2NT, 1) quad2d(StepArgs s, Grid g, Problem pb
           if (right)
             br[f] = (1.0 / 6.0) * row[P1 - 1 - wv] + (2.0 / 3.0) * row[P1 - wv] + (1.0 / 6.0) * row[P1 + 1 - wv];
         }
-        __syncthreads();                   // all boundary values read before the fill below
-        for (int idx = tid; idx < 3 * k2TY * nwin; idx += k2NT) {
-          const int k = idx % nwin, fr = idx / nwin;
-          const int sc = wv + k;
-          if (sc >= 0 && sc <= P1 + 2) continue;
+        // virtual window entries of every row (one warp per row, no index division); they
+        // are disjoint from the real entries the boundary values are read from
+        const int nleft = left ? -wv : 0, kright = right ? (int)P1 + 3 - wv : nwin;
+        for (int fr = tid >> 5; fr < 3 * k2TY; fr += k2NT / 32) {
           double* row = Rw + fr * WC;
-          const double v = sc < 0 ? (1.0 / 6.0) * row[-wv] + (2.0 / 3.0) * row[1 - wv] + (1.0 / 6.0) * row[2 - wv]
-                                  : (1.0 / 6.0) * row[P1 - 1 - wv] + (2.0 / 3.0) * row[P1 - wv] +
-                                        (1.0 / 6.0) * row[P1 + 1 - wv];
-          row[k] = v;
+          const int ln = tid & 31;
+          if (left) {
+            const double v = (1.0 / 6.0) * row[-wv] + (2.0 / 3.0) * row[1 - wv] + (1.0 / 6.0) * row[2 - wv];
+            for (int k = ln; k < nleft; k += 32) row[k] = v;
+          }
+          if (right) {
+            const double v = (1.0 / 6.0) * row[P1 - 1 - wv] + (2.0 / 3.0) * row[P1 - wv] + (1.0 / 6.0) * row[P1 + 1 - wv];
+            for (int k = kright + ln; k < nwin; k += 32) row[k] = v;
+          }
         }
         __syncthreads();
       }
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(k2NT, 1) quad2d(StepArgs s, Grid g, Problem pb
             z2v[p] = fma(tb.B[0], c[p], fma(tb.B[1], c[p + 1], fma(tb.B[2], c[p + 2], tb.B[3] * c[p + 3])));
         }
         const int cb = cx0 + q, ce = cb + k2R - 1;
-        if ((left && cb <= -1 && ce >= -3) || (right && cb <= P1 + 2 && ce >= P1 - 1)) {
+        if ((left || right) && ((left && cb <= -1 && ce >= -3) || (right && cb <= P1 + 2 && ce >= P1 - 1))) {
 #pragma unroll
           for (int p = 0; p < k2R; ++p) {
             const int cell = cb + p;
