@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(k2NT, 1) quad2d(StepArgs s, Grid g, Problem pb
       // rows; clamped rows (global cells < 0 or >= P0 - 1) take the boundary basis
       {
         const int64_t cy = yl0 + g.off0 + ta.q;                       // global cell of tile row 0
-        const int64_t c0 = first_row(j, l);
+        const int64_t c0 = (cy < 0 ? 0 : (cy > P0g - 1 ? P0g - 1 : cy)) - g.off0;   // = first_row(j, l)
         const bool consecutive = cy >= 0 && cy + k2TY - 1 <= P0g - 2;
         mbar_wait(bar, phase);
         phase ^= 1u;

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
       // (1/6, 2/3, 1/6, 0) at cell 0 / P1 - 1
       {
         const int64_t cy = y0 + tb.q;                 // cell of tile row 0
-        const int64_t c0 = first_row(l1);
+        const int64_t c0 = cy < 0 ? 0 : (cy > P1 - 1 ? P1 - 1 : cy);   // = first_row(l1)
         const bool consecutive = cy >= 0 && cy + k3TY - 1 <= P1 - 2;
         mbar_wait(bar, phase);
         phase ^= 1u;
