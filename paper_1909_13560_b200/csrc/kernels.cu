@@ -171,22 +171,21 @@ __device__ inline double rhs_tilde(const double* F, int64_t sl, int64_t P, int64
   return sgn * r;
 }
 
-template <bool STRIDED>
+// One spline pass: LANES lines per CTA (1: lines along the contiguous axis; > 1: adjacent
+// lines of a strided axis, coalesced across the lanes), a tile of TS outputs per line.  The
+// line's values window is staged in shared memory first (every global element read once,
+// coalesced), then the odd-extension RHS, 5 PCR levels in 3 passes on zero-padded arrays (no
+// bounds checks) and the coefficients c = F - m/6 with the not-a-knot end entries, all from
+// shared memory; the output is written once.
+constexpr int kSplZP = 16;        // zero pad of the PCR arrays: the widest pass reads p +- 16
+template <int LANES>
 __global__ void spline_pass(PassArgs a) {
   extern __shared__ double sm[];
   const int H = kPcrHalo;
-  int lane, worker, nworkers, nlanes;
-  int64_t b1;
-  bool valid;
-  if (STRIDED) {
-    lane = threadIdx.x; worker = threadIdx.y; nworkers = blockDim.y; nlanes = 32;
-    b1 = (int64_t)blockIdx.y * 32 + lane;
-    valid = b1 < a.nb1;
-  } else {
-    lane = 0; worker = threadIdx.x; nworkers = blockDim.x; nlanes = 1;
-    b1 = blockIdx.y;
-    valid = true;
-  }
+  const int lane = LANES > 1 ? threadIdx.x % LANES : 0;
+  const int worker = threadIdx.x / LANES, nworkers = blockDim.x / LANES;
+  const int64_t b1 = LANES > 1 ? (int64_t)blockIdx.y * LANES + lane : blockIdx.y;
+  const bool valid = b1 < a.nb1;
   const int64_t b0 = blockIdx.z;
   const int64_t P = a.P;
   const double* F = a.src + b0 * a.s_b0 + (valid ? b1 : 0) * a.s_b1;
@@ -196,32 +195,79 @@ __global__ void spline_pass(PassArgs a) {
   const int64_t k1 = min(k0 + (int64_t)a.TS, P + 1);
   const int64_t base = k0 - 3 - H;
   const int W = a.TS + 6 + 2 * H;
-  double* A = sm;
-  double* B = sm + (size_t)W * nlanes;
-  double m1 = 0.0, mP2 = 0.0;
-  if (valid) {
-    m1 = F[0] - 2.0 * F[sl] + F[2 * sl];
-    mP2 = F[(P - 3) * sl] - 2.0 * F[(P - 2) * sl] + F[(P - 1) * sl];
+  const int WZ = W + 2 * kSplZP;
+  // staged values F[lo_v .. hi_v] (every index the tile and the folded end rows touch)
+  const int64_t lo_v = max(base - 3, (int64_t)0), hi_v = min(base + W + 2, P - 1);
+  const int NV = W + 8;
+  double* Fs = sm;                                          // [NV][LANES]
+  double* A = sm + (size_t)NV * LANES + kSplZP * LANES;     // [WZ][LANES], data at [0, W)
+  double* B = A + (size_t)WZ * LANES;
+  for (int64_t k = lo_v + worker; k <= hi_v; k += nworkers)
+    Fs[(k - lo_v) * LANES + lane] = valid ? F[k * sl] : 0.0;
+  for (int i = worker; i < kSplZP; i += nworkers) {        // zero pads of both PCR arrays
+    A[(-1 - i) * LANES + lane] = 0.0;
+    A[(W + i) * LANES + lane] = 0.0;
+    B[(-1 - i) * LANES + lane] = 0.0;
+    B[(W + i) * LANES + lane] = 0.0;
   }
-  for (int p = worker; p < W; p += nworkers)
-    A[p * nlanes + lane] = valid ? rhs_tilde(F, sl, P, base + p, m1, mP2) : 0.0;
   __syncthreads();
-  // constant-coefficient PCR on the (1,4,1) system: r_i <- r_i - (a/b)(r_{i-s} + r_{i+s})
+  auto Fv = [&](int64_t k) { return Fs[(k - lo_v) * LANES + lane]; };
+  const double m1 = lo_v == 0 ? Fv(0) - 2.0 * Fv(1) + Fv(2) : 0.0;   // not-a-knot end rows, where used
+  const double mP2 = hi_v == P - 1 ? Fv(P - 3) - 2.0 * Fv(P - 2) + Fv(P - 1) : 0.0;
+  for (int p = worker; p < W; p += nworkers) {
+    const int64_t k = base + p;
+    double r;
+    if (k >= 2 && k <= P - 3) {
+      r = 6.0 * (Fv(k - 1) - 2.0 * Fv(k) + Fv(k + 1));
+      if (k == 2) r -= m1;
+      if (k == P - 3) r -= mP2;
+    } else {                                                // odd periodic extension (images)
+      const int64_t period = 2 * (P - 3);
+      int64_t u = (k - 1) % period;
+      if (u < 0) u += period;
+      if (u == 0 || u == P - 3) {
+        r = 0.0;
+      } else {
+        int64_t i;
+        double sgn;
+        if (u < P - 3) { i = 1 + u; sgn = 1.0; }
+        else { i = 1 + period - u; sgn = -1.0; }
+        r = 6.0 * (Fv(i - 1) - 2.0 * Fv(i) + Fv(i + 1));
+        if (i == 2) r -= m1;
+        if (i == P - 3) r -= mP2;
+        r *= sgn;
+      }
+    }
+    A[p * LANES + lane] = r;
+  }
+  __syncthreads();
+  // constant-coefficient PCR, two levels per pass where possible:
+  //   u = r - a1 (r[-s] + r[+s]),   v = u - a2 (u[-2s] + u[+2s])
 #pragma unroll
-  for (int l = 0; l < kPcrLevels; ++l) {
-    const int s = 1 << l;
-    const double al = a.alpha[l];
-    for (int p = worker; p < W; p += nworkers) {
-      const double lft = p - s >= 0 ? A[(p - s) * nlanes + lane] : 0.0;
-      const double rgt = p + s < W ? A[(p + s) * nlanes + lane] : 0.0;
-      B[p * nlanes + lane] = A[p * nlanes + lane] - al * (lft + rgt);
+  for (int l = 0; l < kPcrLevels; l += 2) {
+    const int sh = 1 << l;
+    const double a1 = a.alpha[l];
+    if (l + 1 < kPcrLevels) {
+      const double a2 = a.alpha[l + 1];
+      for (int p = worker; p < W; p += nworkers) {
+        auto at = [&](int q) { return A[q * LANES + lane]; };
+        const double cm1 = at(p - sh), cp1 = at(p + sh), cm2 = at(p - 2 * sh), cp2 = at(p + 2 * sh);
+        const double cm3 = at(p - 3 * sh), cp3 = at(p + 3 * sh);
+        const double u0 = at(p) - a1 * (cm1 + cp1);
+        const double um = cm2 - a1 * (cm3 + cm1);
+        const double up = cp2 - a1 * (cp1 + cp3);
+        B[p * LANES + lane] = u0 - a2 * (um + up);
+      }
+    } else {
+      for (int p = worker; p < W; p += nworkers)
+        B[p * LANES + lane] = A[p * LANES + lane] - a1 * (A[(p - sh) * LANES + lane] + A[(p + sh) * LANES + lane]);
     }
     __syncthreads();
     double* t = A; A = B; B = t;
   }
   if (!valid) return;
   const double ib = a.inv_b;
-  auto mt = [&](int64_t k) { return A[(k - base) * nlanes + lane] * ib; };
+  auto mt = [&](int64_t k) { return A[(k - base) * LANES + lane] * ib; };
   auto mk = [&](int64_t k) -> double {
     if (k == 1) return m1;
     if (k == P - 2) return mP2;
@@ -231,16 +277,23 @@ __global__ void spline_pass(PassArgs a) {
   };
   for (int64_t k = k0 + worker; k < k1; k += nworkers) {
     double c;
-    if (k >= 0 && k < P) c = F[k * sl] - mk(k) * (1.0 / 6.0);
+    if (k >= 2 && k <= P - 3) c = Fv(k) - mt(k) * (1.0 / 6.0);
+    else if (k >= 0 && k < P) c = Fv(k) - mk(k) * (1.0 / 6.0);
     else if (k < 0) {
-      const double c0 = F[0] - mk(0) * (1.0 / 6.0), c1 = F[sl] - m1 * (1.0 / 6.0);
-      c = 6.0 * F[0] - 4.0 * c0 - c1;
+      const double c0 = Fv(0) - mk(0) * (1.0 / 6.0), c1 = Fv(1) - m1 * (1.0 / 6.0);
+      c = 6.0 * Fv(0) - 4.0 * c0 - c1;
     } else {
-      const double cl = F[(P - 1) * sl] - mk(P - 1) * (1.0 / 6.0), cm = F[(P - 2) * sl] - mP2 * (1.0 / 6.0);
-      c = 6.0 * F[(P - 1) * sl] - 4.0 * cl - cm;
+      const double cl = Fv(P - 1) - mk(P - 1) * (1.0 / 6.0), cm = Fv(P - 2) - mP2 * (1.0 / 6.0);
+      c = 6.0 * Fv(P - 1) - 4.0 * cl - cm;
     }
     out[(k + 1) * a.d_line] = c;
   }
+}
+
+// shared memory of one spline_pass CTA
+static size_t spline_smem(int TS, int lanes) {
+  const int W = TS + 6 + 2 * kPcrHalo;
+  return ((size_t)(W + 8) + 2 * (size_t)(W + 2 * kSplZP)) * lanes * sizeof(double);
 }
 
 // PCR constants of the infinite (1,4,1) Toeplitz system, long double on the host
@@ -255,21 +308,23 @@ void pcr_constants(double* alpha, double* inv_b) {
 }
 
 static cudaError_t run_pass(PassArgs pa, bool strided, cudaStream_t st, int64_t* launches) {
-  const int H = kPcrHalo;
   pcr_constants(pa.alpha, &pa.inv_b);
+  const int64_t n = pa.P + 2;                              // outputs per line (c_{-1} .. c_P)
   if (strided) {
-    pa.TS = 128;                                   // halo overhead (6 + 2 H) / TS = 53 %
-    const int W = pa.TS + 6 + 2 * H;
-    const size_t smem = (size_t)W * 32 * 2 * sizeof(double);
-    dim3 grid((unsigned)((pa.P + 2 + pa.TS - 1) / pa.TS), (unsigned)((pa.nb1 + 31) / 32), (unsigned)pa.nb0);
-    spline_pass<true><<<grid, dim3(32, 8), smem, st>>>(pa);
+    // 8 adjacent lines per CTA (64-byte coalesced rows), tiles of ~256 outputs (halo 27 %)
+    constexpr int LN = 8;
+    const int64_t nt = (n + 255) / 256;
+    pa.TS = (int)((n + nt - 1) / nt);
+    dim3 grid((unsigned)nt, (unsigned)((pa.nb1 + LN - 1) / LN), (unsigned)pa.nb0);
+    spline_pass<LN><<<grid, 256, spline_smem(pa.TS, LN), st>>>(pa);
   } else {
-    pa.TS = pa.P + 2 <= 4096 ? (int)(pa.P + 2) : 1024;
-    if (pa.P + 2 > 4096 && pa.nb0 * pa.nb1 == 1) pa.TS = 512;   // one long line: spread over SMs
-    const int W = pa.TS + 6 + 2 * H;
-    const size_t smem = (size_t)W * 2 * sizeof(double);
-    dim3 grid((unsigned)((pa.P + 2 + pa.TS - 1) / pa.TS), (unsigned)pa.nb1, (unsigned)pa.nb0);
-    spline_pass<false><<<grid, 256, smem, st>>>(pa);
+    // one line per CTA, tiles of ~2048 outputs (balanced; halo 3 %), or spread over the SMs
+    // when there is a single long line
+    int64_t nt = (n + 2047) / 2048;
+    if (pa.nb0 * pa.nb1 == 1 && n > 4096) nt = (n + 511) / 512;
+    pa.TS = (int)((n + nt - 1) / nt);
+    dim3 grid((unsigned)nt, (unsigned)pa.nb1, (unsigned)pa.nb0);
+    spline_pass<1><<<grid, 256, spline_smem(pa.TS, 1), st>>>(pa);
   }
   ++*launches;
   return cudaGetLastError();
@@ -527,8 +582,8 @@ cudaError_t launch_generic_step(const StepArgs& s, const Grid& g, const Problem&
 // opt in to > 48 KB dynamic shared memory on the current device (called per context)
 cudaError_t init_device_attributes() {
   const int lim = 200 * 1024;
-  cudaError_t e = cudaFuncSetAttribute(spline_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaError_t e = cudaFuncSetAttribute(spline_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = set_attr_drv<DRV_ZERO>();
   if (e == cudaSuccess) e = set_attr_drv<DRV_AFFINE>();
   if (e == cudaSuccess) e = set_attr_drv<DRV_EX1>();
