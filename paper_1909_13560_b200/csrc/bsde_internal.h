@@ -96,6 +96,10 @@ struct Fused1D {
   int TP;                    // points per CTA
   int WMAX;                  // doubles per field buffer in shared memory
   int WP;                    // doubles per PCR scratch array (own-tile spline)
+  int WS;                    // doubles of the pass-2 spline scratch (values window + 2 PCR arrays)
+  int TK;                    // doubles of the shared-memory tap table (K x L Tap1D)
+  int sep;                   // 1: the spline scratch has its own shared memory (the next round's
+                             // first windows stream in during pass 2); 0: it overlays the buffers
   double alpha[kPcrLevels];  // PCR elimination ratios
   double inv_b;              // 1 / b after the last PCR level
 };
@@ -113,6 +117,8 @@ struct Persist1D {
   unsigned* done_flag;
   int D[kMaxK + 1];  // D[j]: CTA distance of level j's window (j >= 1); D[0]: values halo of phase A
   int DK;            // max of D
+  int nowait;        // debug (BSDE_DEBUG_NOWAIT): skip every flag wait -- wrong results, busy time only
+  int nopad;         // debug (BSDE_DEBUG_NOPAD): skip the edge CTAs' pad fill -- wrong results
 };
 
 // One problem of a fused launch and the launch itself.  All problems of a launch share the

@@ -32,6 +32,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
 }
+// bulk shared -> global copy (bulk-group completion)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t done = 0;
   do {
@@ -70,10 +80,33 @@ __device__ __forceinline__ void level_span(int qmin, int qmax, int lo, int hi, i
   we = hi - 1 + qmax + 3;
 }
 
+// shared-memory header: 4 mbarriers @0, the flag marks @64, the window spans @256, the
+// problems' parameters @1024
+constexpr int kFusedHdr = (int)((1024 + kMaxBatch * sizeof(FusedProb) + 127) & ~(size_t)127);
+// rhs_tilde (kernels.cu) for the rows near the line ends that the fused kernel's PCR extent
+// reaches (|k| and |k - P| below the 2 (P - 3) period): the same odd extension, folded
+// without a 64-bit modulo
+__device__ __forceinline__ double rhs_fold(const double* F, int P, int k, double m1, double mP2) {
+  const int period = 2 * (P - 3);
+  int u = k - 1;
+  if (u < 0) u += period;
+  if (u >= period) u -= period;
+  if (u == 0 || u == P - 3) return 0.0;
+  int i;
+  double sgn;
+  if (u < P - 3) { i = 1 + u; sgn = 1.0; }
+  else { i = 1 + period - u; sgn = -1.0; }
+  double r = 6.0 * (F[i - 1] - 2.0 * F[i] + F[i + 1]);
+  if (i == 2) r -= m1;
+  if (i == P - 3) r -= mP2;
+  return sgn * r;
+}
+
 // Persist1D, FusedProb: bsde_internal.h
 struct FusedBatch {
   Fused1D fz;
   Grid g;
+  const unsigned char* arena;   // global address of the constant tap arena (bulk-copy source)
   int nprob, max_steps;
   FusedProb prob[kMaxBatch];
 };
@@ -90,12 +123,17 @@ __device__ __forceinline__ unsigned wait_neighbours_warp(const unsigned* flag, i
   unsigned seen = 0xffffffffu;
   for (int q0 = a; q0 <= e; q0 += 32) {
     const int q = q0 + lane;
-    bool ok = q > e;
-    while (!__all_sync(0xffffffffu, ok)) {
-      if (!ok) ok = ld_relaxed(flag + q) >= target;      // relaxed polling (no L1 invalidation)
-      if (!__all_sync(0xffffffffu, ok)) __nanosleep(32);
+    // first an acquire read (one round trip when the flags are already set), then relaxed
+    // polling (no L1 invalidation) and a final acquire
+    unsigned v = q <= e ? ld_acquire(flag + q) : 0xffffffffu;
+    if (!__all_sync(0xffffffffu, v >= target)) {
+      bool ok = v >= target;
+      while (!__all_sync(0xffffffffu, ok)) {
+        __nanosleep(32);
+        if (!ok) ok = ld_relaxed(flag + q) >= target;
+      }
+      v = q <= e ? ld_acquire(flag + q) : 0xffffffffu;   // synchronises with the release
     }
-    const unsigned v = q <= e ? ld_acquire(flag + q) : 0xffffffffu;   // synchronises with the release
     seen = min(seen, __reduce_min_sync(0xffffffffu, v));
   }
   __syncwarp();
@@ -103,15 +141,57 @@ __device__ __forceinline__ unsigned wait_neighbours_warp(const unsigned* flag, i
   return seen;
 }
 
-// the same with a per-CTA low-water mark *low of the flags within DK (shared memory, touched
-// by warp 0 only): a wait whose target is already covered costs nothing; waits over the DK
-// range raise the mark
-__device__ __forceinline__ void wait_flags(const unsigned* flag, unsigned* low, int b, int D, int DK, int nb,
+// Progress marks of a problem's neighbour flags (shared memory, touched by one warp at a time):
+// mk[0] = a lower bound of the flags within the short distance Dn of that flag kind (ring
+// flags: D[1], the newest level's window; done flags: D[0], the values halo), mk[1] = a lower
+// bound within DK.  Flags only grow, so a wait whose target is covered costs nothing.
+__device__ __forceinline__ void wait_flags(const unsigned* flag, unsigned* mk, int b, int D, int DK, int nb,
                                            unsigned target) {
-  if (*low >= target) return;
+  if (mk[1] >= target || (D < DK && mk[0] >= target)) return;
   const unsigned seen = wait_neighbours_warp(flag, b, D, nb, target);
-  if (D >= DK && (threadIdx.x & 31) == 0) *low = seen;
+  if ((threadIdx.x & 31) == 0) {
+    if (D >= DK) mk[1] = seen;
+    mk[0] = max(mk[0], seen);          // every short-range wait of a kind uses that kind's Dn <= D
+  }
   __syncwarp();
+}
+
+// warp 0: one read of every problem's flags of one kind within DK, raising the marks; a
+// problem whose DK range is wider than a warp keeps its marks (its waits poll).  The loads
+// are relaxed so that all problems' reads are in flight together (a chain of acquire loads
+// would cost one round trip each); one acquire fence afterwards orders every later access
+// of the CTA (after the barrier that follows) behind them.
+template <int KIND>   // 0: ring flags (short range D[1]), 1: done flags (short range D[0])
+__device__ __forceinline__ void refresh_marks(const FusedProb* prob, int nprob, int it, unsigned* marks, int b, int nb) {
+  const int lane = threadIdx.x & 31;
+  unsigned v[kMaxBatch];
+#pragma unroll
+  for (int ip = 0; ip < kMaxBatch; ++ip) {
+    v[ip] = 0xffffffffu;
+    if (ip < nprob && it < prob[ip].pp.nsteps) {
+      const Persist1D& pp = prob[ip].pp;
+      const int q = b - pp.DK + lane;
+      if (2 * pp.DK + 1 <= 32 && lane <= 2 * pp.DK && q >= 0 && q < nb)
+        v[ip] = ld_relaxed((KIND ? pp.done_flag : pp.ring_flag) + q);
+    }
+  }
+#pragma unroll
+  for (int ip = 0; ip < kMaxBatch; ++ip) {
+    if (ip >= nprob || it >= prob[ip].pp.nsteps || 2 * prob[ip].pp.DK + 1 > 32) continue;
+    const Persist1D& pp = prob[ip].pp;
+    const int Dn = KIND ? pp.D[0] : pp.D[1];
+    const int d = lane - pp.DK;
+    const unsigned mK = __reduce_min_sync(0xffffffffu, v[ip]);
+    const unsigned mN = __reduce_min_sync(0xffffffffu, (d >= -Dn && d <= Dn) ? v[ip] : 0xffffffffu);
+    if (lane == 0) {
+      unsigned* mk = marks + 4 * ip + 2 * KIND;
+      mk[0] = max(mk[0], mN);
+      mk[1] = max(mk[1], mK);
+    }
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // ring slot of level n+j (j = 1..K) of a problem at round it
@@ -122,16 +202,17 @@ __device__ __forceinline__ int level_slot(const FusedProb& fp, int it, int j) {
 // bulk-load the window of level j of problem fp into dst (lane 0 of the calling warp): the
 // whole window [wv, we] (the virtual boundary entries live in the line's pads, Grid::cpad),
 // even-aligned for the bulk copy
-__device__ __forceinline__ void issue_window(const FusedProb& fp, int it, int j, double* dst, int WM, uint64_t* bar,
-                                             int lo, int hi) {
+__device__ __forceinline__ void issue_window(const FusedProb& fp, const int* sp, int it, int j, double* dst, int WM,
+                                             uint64_t* bar, int lo, int hi) {
   if ((threadIdx.x & 31) != 0) return;
-  const int L = fp.s.L;
-  const Tap1D* tj = taps1d(fp.s.tap1_off) + (j - 1) * L;
   int wv, we;
-  level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
+  level_span(sp[2 * (j - 1)], sp[2 * (j - 1) + 1], lo, hi, wv, we);
   const int s1 = (we + 2) & ~1;
   const uint32_t bytes = (uint32_t)((s1 - wv) * sizeof(double));
   const double* Cf = fp.s.ring + (int64_t)level_slot(fp, it, j) * fp.s.slot_elems;
+  // the flags may have been acquired by another warp (before a CTA barrier): order this
+  // thread's async-proxy reads behind them
+  asm volatile("fence.proxy.async.global;" ::: "memory");
   mbar_expect_tx(bar, 2 * bytes);
   bulk_g2s(dst, Cf + wv, bytes, bar);
   bulk_g2s(dst + WM, Cf + fp.s.cfield + wv, bytes, bar);
@@ -139,37 +220,65 @@ __device__ __forceinline__ void issue_window(const FusedProb& fp, int it, int j,
 
 // Level n+j was written by pass 2 of round it-j by the CTAs within D[j]: levels >= 2 are
 // covered by the ring flags of round it-2 within DK, level 1 needs round it-1 within D[1].
-__device__ __forceinline__ void ring_wait(const FusedProb& fp, unsigned* low, int it, int j, int bid, int nb) {
-  if (it == 0) return;
+__device__ __forceinline__ void ring_wait(const FusedProb& fp, unsigned* mk, int it, int j, int bid, int nb) {
+  if (it == 0 || fp.pp.nowait) return;
   const Persist1D& pp = fp.pp;
-  if (j == 1) wait_flags(pp.ring_flag, low, bid, pp.D[1], pp.DK, nb, (unsigned)it);
-  else if (it >= 2) wait_flags(pp.ring_flag, low, bid, pp.DK, pp.DK, nb, (unsigned)(it - 1));
+  if (j == 1) wait_flags(pp.ring_flag, mk, bid, pp.D[1], pp.DK, nb, (unsigned)it);
+  else if (it >= 2) wait_flags(pp.ring_flag, mk, bid, pp.DK, pp.DK, nb, (unsigned)(it - 1));
 }
 
-// the first one or two windows of a problem's step (levels K and K-1; warp 0)
-__device__ __forceinline__ void start_windows(const FusedProb& fp, unsigned* low, int it, double* buf0, double* buf1,
-                                              int WM, uint64_t* bar, int lo, int hi, int bid, int nb) {
+// the first one or two windows of a problem's step it (levels K and K-1 into buffers 0 and 1;
+// warp 0), skipping the `have` already in flight
+__device__ __forceinline__ void start_windows(const FusedProb& fp, const int* sp, unsigned* mk, int it, int have,
+                                              double* buf0, double* buf1, int WM, uint64_t* bar, int lo, int hi,
+                                              int bid, int nb) {
   const int K = fp.s.K;
-  ring_wait(fp, low, it, K >= 2 ? 2 : 1, bid, nb);
-  issue_window(fp, it, K, buf0, WM, &bar[0], lo, hi);
-  if (K >= 2) {
-    if (K == 2) ring_wait(fp, low, it, 1, bid, nb);
-    issue_window(fp, it, K - 1, buf1, WM, &bar[1], lo, hi);
+  for (int w = have; w < min(2, K); ++w) {
+    ring_wait(fp, mk, it, K - w, bid, nb);
+    issue_window(fp, sp, it, K - w, w ? buf1 : buf0, WM, &bar[w], lo, hi);
   }
+}
+
+// the problem's Tap1D table (K x L) from the arena into shared memory (lane 0 of warp 0)
+__device__ __forceinline__ void issue_taps(const FusedProb& fp, const unsigned char* arena, Tap1D* dst, uint64_t* bar) {
+  if ((threadIdx.x & 31) != 0) return;
+  const uint32_t bytes = (uint32_t)(((size_t)fp.s.K * fp.s.L * sizeof(Tap1D) + 15) & ~(size_t)15);
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(dst, arena + fp.s.tap1_off, bytes, bar);
+}
+
+// the same for step it of a problem issued one round early (at the end of pass 1 of round
+// it-1, streaming in during pass 2): only levels >= 2, whose ring data is from round it-2 or
+// older (level 1 is written by that pass 2); returns the number of windows issued
+__device__ __forceinline__ int start_windows_ahead(const FusedProb& fp, const int* sp, unsigned* mk, int it,
+                                                   double* buf0, double* buf1, int WM, uint64_t* bar, int lo, int hi,
+                                                   int bid, int nb) {
+  const int K = fp.s.K;
+  int w = 0;
+  for (; w < 2 && K - w >= 2; ++w) {
+    ring_wait(fp, mk, it, K - w, bid, nb);
+    issue_window(fp, sp, it, K - w, w ? buf1 : buf0, WM, &bar[w], lo, hi);
+  }
+  return w;
 }
 
 template <int DRV, int R, int C, int NT, int MB>
 __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ FusedBatch bt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);        // 0/1: level buffers, 2: values tile
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);   // 0/1: level buffers, 2: values tile, 3: taps
   const Fused1D& fz = bt.fz;
   const Grid& g = bt.g;
   const int WM = fz.WMAX, WP = fz.WP;
-  double* const buf0 = reinterpret_cast<double*>(smem_raw + 128);
+  double* const buf0 = reinterpret_cast<double*>(smem_raw + kFusedHdr);
   double* const buf1 = buf0 + 2 * WM;
-  // spline scratch of pass 2, overlaying the level buffers (free after the epilogue):
-  // values window Fs (2 x (WP + 8)) and the PCR arrays T0, T1 (2 x WP each)
-  double* const Fs = buf0;
+  // spline scratch of pass 2: values window Fs (2 x (WP + 8)) and the PCR arrays T0, T1
+  // (2 x WP each), behind the level buffers (fz.sep) or overlaying them (free after the
+  // epilogue)
+  double* const Fs = buf0 + (fz.sep ? 4 * WM : 0);
+  // the current problem's tap table (bulk-copied one problem ahead) and window spans
+  Tap1D* const tsm = reinterpret_cast<Tap1D*>(buf0 + 4 * WM + (fz.sep ? fz.WS : 0));
+  int* const spans = reinterpret_cast<int*>(smem_raw + 256);     // [problem][level][qmin, qmax]
+  FusedProb* const PB = reinterpret_cast<FusedProb*>(smem_raw + 1024);
   double* const T0 = Fs + 2 * (WP + 8);
   double* const T1 = T0 + 2 * WP;
   constexpr int NWPG = NT / (32 * C);
@@ -194,31 +303,56 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   const int va1 = (int)((((int64_t)P + va) & ~(int64_t)1) - P);  // field 1 start (P + va1 even)
   const int publisher = NT - 32;  // thread that releases the flags (the last warp pays the fence)
 
-  // low-water marks of the neighbours' flags per problem: [ip] ring, [kMaxBatch + ip] done
-  unsigned* const lowc = reinterpret_cast<unsigned*>(smem_raw + 64);
+  // progress marks of the neighbours' flags, 4 per problem: ring (short range, DK), done
+  // (short range, DK); see wait_flags
+  unsigned* const marks = reinterpret_cast<unsigned*>(smem_raw + 64);
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
+    mbar_init(&bar[3], 1);
     fence_mbar_init();
-    for (int i = 0; i < 2 * kMaxBatch; ++i) lowc[i] = 0;
+    for (int i = 0; i < 4 * kMaxBatch; ++i) marks[i] = 0;
+  }
+  // the problems' parameters in shared memory (indexed accesses to the kernel parameter
+  // would go through the small constant cache)
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(bt.prob);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(PB);
+    for (int i = tid; i < bt.nprob * (int)(sizeof(FusedProb) / 4); i += NT) dst[i] = src[i];
+  }
+  for (int i = tid; i < bt.nprob * kMaxK; i += NT) {
+    const FusedProb& fp = bt.prob[i / kMaxK];
+    const int j = i % kMaxK;
+    if (j < fp.s.K) {
+      const Tap1D* tj = taps1d(fp.s.tap1_off) + j * fp.s.L;
+      spans[2 * i] = tj[0].q;
+      spans[2 * i + 1] = tj[fp.s.L - 1].q;
+    }
   }
   grid_dep_wait();            // previous kernel in the stream has completed
   __syncthreads();
-  uint32_t ph[3] = {0, 0, 0};
+  uint32_t ph[4] = {0, 0, 0, 0};
+  int prefetched = 0;         // windows of the current problem already in flight
+  // the warp that issues the next problem's copies during the epilogue: one without points
+  // (its lanes would otherwise idle through the Picard iterations), else warp 0.  It touches
+  // the flag marks only between CTA barriers that separate it from warp 0's waits.
+  const int iw = (hi - lo <= NT - 32) ? NT / 32 - 1 : 0;
+  bool taps_in = false;       // its tap table is in flight
 
   for (int it = 0; it < bt.max_steps; ++it) {
     // ================= pass 1: levels K..1, z and Picard of step it of every problem
-    bool prefetched = false;                 // the current problem's first windows are in flight
+    if (warp == 0 && it > 0) refresh_marks<0>(PB, bt.nprob, it, marks, bid, nb);
     for (int ip = 0; ip < bt.nprob; ++ip) {
-      const FusedProb& fp = bt.prob[ip];
+      const FusedProb& fp = PB[ip];
       const Persist1D& pp = fp.pp;
       if (it >= pp.nsteps) continue;
       const StepArgs& s = fp.s;
       const int it_stamp = it;
       PHASE_STAMP(0);
       const int L = s.L, K = s.K;
-      const Tap1D* const tap0 = taps1d(s.tap1_off);
+      const Tap1D* const tap0 = tsm;
+      const int* const sp = spans + 2 * kMaxK * ip;
       double tlev[kMaxK];
       double tn;
       double* vout;
@@ -237,8 +371,15 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       // windows of levels K and K-1 (unless prefetched during the previous problem's
       // epilogue); later levels are issued behind the computation.  (No CTA barrier here:
       // the previous pass ended with one; the other warps wait on the mbarriers.)
-      if (!prefetched && warp == 0) start_windows(fp, lowc + ip, it, buf0, buf1, WM, bar, lo, hi, bid, nb);
-      prefetched = false;
+      if (warp == 0) {
+        if (!taps_in) issue_taps(fp, bt.arena, tsm, &bar[3]);
+        start_windows(fp, spans + 2 * kMaxK * ip, marks + 4 * ip, it, prefetched, buf0, buf1, WM, bar, lo, hi, bid,
+                      nb);
+      }
+      prefetched = 0;
+      taps_in = false;
+      mbar_wait(&bar[3], ph[3]);
+      ph[3] ^= 1u;
       PHASE_STAMP(1);
 
       Driver<DRV, 1> drv(fp.dp);
@@ -253,7 +394,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       auto level = [&](int j, int b) {
         const Tap1D* tj = tap0 + (j - 1) * L;
         int wv, we;
-        level_span(tj[0].q, tj[L - 1].q, lo, hi, wv, we);
+        level_span(sp[2 * (j - 1)], sp[2 * (j - 1) + 1], lo, hi, wv, we);
         mbar_wait(&bar[b], ph[b]);
         ph[b] ^= 1u;
         double* const wy = b ? buf1 : buf0;
@@ -320,8 +461,8 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
           if (warp == 0) {
-            if (j - 2 == 1) ring_wait(fp, lowc + ip, it, 1, bid, nb);
-            issue_window(fp, it, j - 2, b ? buf1 : buf0, WM, &bar[b], lo, hi);
+            if (j - 2 == 1) ring_wait(fp, marks + 4 * ip, it, 1, bid, nb);
+            issue_window(fp, sp, it, j - 2, b ? buf1 : buf0, WM, &bar[b], lo, hi);
           }
         }
       }
@@ -359,12 +500,36 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       // the next problem's first windows stream in during this epilogue
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
-      for (int iq = ip + 1; iq < bt.nprob; ++iq) {
-        if (it >= bt.prob[iq].pp.nsteps) continue;
-        if (warp == 0) start_windows(bt.prob[iq], lowc + iq, it, buf0, buf1, WM, bar, lo, hi, bid, nb);
-        prefetched = true;
-        break;
+      PHASE_STAMP(16);
+      {
+        int iq = ip + 1;
+        while (iq < bt.nprob && it >= PB[iq].pp.nsteps) ++iq;
+        if (iq < bt.nprob) {
+          if (warp == iw) {
+            issue_taps(PB[iq], bt.arena, tsm, &bar[3]);
+            start_windows(PB[iq], spans + 2 * kMaxK * iq, marks + 4 * iq, it, 0, buf0, buf1, WM, bar, lo, hi,
+                          bid, nb);
+          }
+          prefetched = 2;
+          taps_in = true;
+        } else {
+          // last problem of the round: the first problem of the next round (its taps; with a
+          // separate spline scratch also its windows of levels >= 2)
+          iq = 0;
+          while (iq < bt.nprob && it + 1 >= PB[iq].pp.nsteps) ++iq;
+          if (iq < bt.nprob) {
+            if (warp == iw) {
+              issue_taps(PB[iq], bt.arena, tsm, &bar[3]);
+              if (fz.sep)
+                start_windows_ahead(PB[iq], spans + 2 * kMaxK * iq, marks + 4 * iq, it + 1, buf0, buf1, WM, bar, lo,
+                                    hi, bid, nb);
+            }
+            prefetched = fz.sep ? min(2, max(0, PB[iq].s.K - 1)) : 0;   // what start_windows_ahead issued
+            taps_in = true;
+          }
+        }
       }
+      PHASE_STAMP(17);
       const double inv_gz0 = 1.0 / s.gz0;
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -392,6 +557,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         s.picard[p] = itp;
         if (!isfinite(y) || !isfinite(z)) atomicMin(s.bad, (unsigned long long)p);
       }
+      PHASE_STAMP(18);
       // generic-proxy accesses of the level buffers before later bulk copies into them
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
@@ -400,8 +566,9 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
     }
 
     // ================= pass 2: spline of every problem's new level n on this CTA's tile
+    if (warp == 0) refresh_marks<1>(PB, bt.nprob, it, marks, bid, nb);
     for (int ip = 0; ip < bt.nprob; ++ip) {
-      const FusedProb& fp = bt.prob[ip];
+      const FusedProb& fp = PB[ip];
       const Persist1D& pp = fp.pp;
       if (it >= pp.nsteps) continue;
       const StepArgs& s = fp.s;
@@ -419,10 +586,10 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       PHASE_STAMP(10);
       // the CTAs within D[0] wrote their level-n values (done flag it+1); the CTAs within DK
       // finished pass 1 of round it-2, the last reader of ring slot n (level n + K + 2)
-      if (warp == 0) {
-        unsigned* low = lowc + kMaxBatch + ip;
-        if (it >= 2) wait_flags(pp.done_flag, low, bid, pp.DK, pp.DK, nb, (unsigned)(it - 1));
-        wait_flags(pp.done_flag, low, bid, pp.D[0], pp.DK, nb, (unsigned)it + 1);
+      if (warp == 0 && !pp.nowait) {
+        unsigned* mk = marks + 4 * ip + 2;
+        if (it >= 2) wait_flags(pp.done_flag, mk, bid, pp.DK, pp.DK, nb, (unsigned)(it - 1));
+        wait_flags(pp.done_flag, mk, bid, pp.D[0], pp.DK, nb, (unsigned)it + 1);
       }
       __syncthreads();
       PHASE_STAMP(11);
@@ -457,8 +624,8 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
           if (k == 2) { r0 -= m1_0; r1 -= m1_1; }
           if (k == P - 3) { r0 -= mP2_0; r1 -= mP2_1; }
         } else {
-          r0 = rhs_tilde(Fw0, 1, P, (int64_t)k, m1_0, mP2_0);
-          r1 = rhs_tilde(Fw1, 1, P, (int64_t)k, m1_1, mP2_1);
+          r0 = rhs_fold(Fw0, P, k, m1_0, mP2_0);
+          r1 = rhs_fold(Fw1, P, k, m1_1, mP2_1);
         }
         T0[p] = r0;
         T0[WP + p] = r1;
@@ -521,36 +688,30 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
           if (k == P - 1) return 2.0 * mP2 - (P - 3 == 1 ? m1 : mt(P - 3));
           return mt(k);
         };
-        double* rf = ringn + (int64_t)f * s.cfield;
-        for (int k = k0 + tid; k < k1; k += NT) {
-          double c;
-          if (k >= 2 && k <= P - 3) c = Fw[k] - mt(k) * (1.0 / 6.0);
-          else if (k >= 0 && k < P) c = Fw[k] - mk(k) * (1.0 / 6.0);
-          else if (k < 0) {
+        auto coef = [&](int k) -> double {
+          if (k >= 2 && k <= P - 3) return Fw[k] - mt(k) * (1.0 / 6.0);
+          if (k >= 0 && k < P) return Fw[k] - mk(k) * (1.0 / 6.0);
+          if (k < 0) {
             const double c0 = Fw[0] - mk(0) * (1.0 / 6.0), c1 = Fw[1] - m1 * (1.0 / 6.0);
-            c = 6.0 * Fw[0] - 4.0 * c0 - c1;
-          } else {
-            const double cl = Fw[P - 1] - mk(P - 1) * (1.0 / 6.0);
-            const double cm = Fw[P - 2] - mP2 * (1.0 / 6.0);
-            c = 6.0 * Fw[P - 1] - 4.0 * cl - cm;
+            return 6.0 * Fw[0] - 4.0 * c0 - c1;
           }
-          rf[k + 1] = c;
+          const double cl = Fw[P - 1] - mk(P - 1) * (1.0 / 6.0);
+          const double cm = Fw[P - 2] - mP2 * (1.0 / 6.0);
+          return 6.0 * Fw[P - 1] - 4.0 * cl - cm;
+        };
+        double* rf = ringn + (int64_t)f * s.cfield;
+        for (int k = k0 + tid; k < k1; k += NT) rf[k + 1] = coef(k);
+        // edge CTAs: the line's virtual boundary entries, the clamped boundary values
+        // s(x_0) = (c_{-1} + 4 c_0 + c_1)/6 and s(x_{P-1}), from shared memory
+        // edge CTAs: the line's virtual boundary entries, the clamped boundary values
+        // s(x_0) = (c_{-1} + 4 c_0 + c_1)/6 and s(x_{P-1}), from shared memory
+        if (k0 == -1 && !pp.nopad) {
+          const double v = (1.0 / 6.0) * coef(-1) + (2.0 / 3.0) * coef(0) + (1.0 / 6.0) * coef(1);
+          for (int64_t i = tid; i < s.cpad; i += NT) rf[-1 - i] = v;
         }
-      }
-      if (k0 == -1 || k1 == P + 1) {          // edge CTAs: the line's virtual boundary entries
-        __syncthreads();
-        const int64_t cpad = s.cpad;
-#pragma unroll
-        for (int f = 0; f < 2; ++f) {
-          double* rf = ringn + (int64_t)f * s.cfield;
-          if (k0 == -1) {
-            const double v = (1.0 / 6.0) * rf[0] + (2.0 / 3.0) * rf[1] + (1.0 / 6.0) * rf[2];
-            for (int64_t i = tid; i < cpad; i += NT) rf[-1 - i] = v;
-          }
-          if (k1 == P + 1) {
-            const double v = (1.0 / 6.0) * rf[P - 1] + (2.0 / 3.0) * rf[P] + (1.0 / 6.0) * rf[P + 1];
-            for (int64_t i = tid; i < cpad; i += NT) rf[P + 3 + i] = v;
-          }
+        if (k1 == P + 1 && !pp.nopad) {
+          const double v = (1.0 / 6.0) * coef(P - 2) + (2.0 / 3.0) * coef(P - 1) + (1.0 / 6.0) * coef(P);
+          for (int64_t i = tid; i < s.cpad; i += NT) rf[P + 3 + i] = v;
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -574,6 +735,20 @@ static const FusedVariant kVariants[] = {
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 int fused1d_num_variants() { return kNumVariants; }
 
+// shared memory of the fused kernel for fz's buffer sizes: the spline scratch gets its own
+// region when it fits (fz.sep = 1), else it overlays the level buffers; 0 if neither fits
+size_t fused1d_smem(Fused1D& fz) {
+  const size_t limit = kVariants[fz.variant].MB == 1 ? 220 * 1024 : 112 * 1024;
+  const size_t sep = kFusedHdr + ((size_t)4 * fz.WMAX + fz.WS + fz.TK) * sizeof(double);
+  const int wo = std::max(fz.WMAX, (fz.WS + 3) / 4);
+  const size_t ovl = kFusedHdr + ((size_t)4 * wo + fz.TK) * sizeof(double);
+  fz.sep = sep <= limit;
+  if (fz.sep) return sep;
+  if (ovl > limit) return 0;
+  fz.WMAX = (wo + 1) & ~1;
+  return kFusedHdr + ((size_t)4 * fz.WMAX + fz.TK) * sizeof(double);
+}
+
 bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int nsm, int variant, Fused1D& fz, int& threads,
                       int& blocks, size_t& smem) {
   if (variant < 0 || variant >= kNumVariants) return false;
@@ -590,14 +765,13 @@ bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int nsm, int v
   fz.WP = ((fz.TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;      // PCR extent of the own tile (+ window slack)
   int wm = fz.TP + qspan_max + 4 + 2;                        // level window
   const int wr = (3 * v.C * fz.TP + 3) / 4;                  // reduction (overlays buf0/buf1)
-  const int ws = (6 * fz.WP + 16 + 3) / 4;                   // pass-2 spline scratch (overlays them)
   if (wr > wm) wm = wr;
-  if (ws > wm) wm = ws;
-  wm = (wm + 1) & ~1;
-  fz.WMAX = wm;
-  smem = 128 + (size_t)4 * wm * sizeof(double);
+  fz.WMAX = (wm + 1) & ~1;
+  fz.WS = 6 * fz.WP + 16;                                    // pass-2 spline scratch
+  fz.TK = ((int)((size_t)K * L * sizeof(Tap1D) / sizeof(double)) + 1) & ~1;   // tap table
+  smem = fused1d_smem(fz);
   (void)K; (void)L; (void)nsm;
-  return smem <= (v.MB == 1 ? 220 * 1024 : 112 * 1024);
+  return smem > 0;
 }
 
 void pcr_constants(double* alpha, double* inv_b);
@@ -663,11 +837,25 @@ cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& 
   bt = FusedBatch{};
   bt.fz = fz;
   bt.g = g;
+  {
+    void* a = nullptr;
+    cudaError_t e = cudaGetSymbolAddress(&a, c_arena);
+    if (e != cudaSuccess) return e;
+    bt.arena = static_cast<const unsigned char*>(a);
+  }
   bt.nprob = nprob;
   bt.max_steps = 0;
+  // problems with more levels first: the first problem of a round then has windows of levels
+  // >= 2 that stream in during the previous round's pass 2 (a stable order; each problem's
+  // arithmetic does not depend on it)
+  int order[kMaxBatch];
+  for (int i = 0; i < nprob; ++i) order[i] = i;
+  std::stable_sort(order, order + nprob, [&](int a, int b) { return probs[a].s.K > probs[b].s.K; });
   for (int i = 0; i < nprob; ++i) {
-    bt.prob[i] = probs[i];
-    if (probs[i].pp.nsteps > bt.max_steps) bt.max_steps = probs[i].pp.nsteps;
+    bt.prob[i] = probs[order[i]];
+    if (bt.prob[i].pp.nsteps > bt.max_steps) bt.max_steps = bt.prob[i].pp.nsteps;
+    if (getenv("BSDE_DEBUG_NOWAIT")) bt.prob[i].pp.nowait = 1;
+    if (getenv("BSDE_DEBUG_NOPAD")) bt.prob[i].pp.nopad = 1;
     cudaError_t e = cudaMemsetAsync(probs[i].pp.ring_flag, 0, sizeof(unsigned) * 2 * (size_t)blocks, st);
     if (e != cudaSuccess) return e;
   }

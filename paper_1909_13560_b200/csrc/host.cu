@@ -39,6 +39,7 @@ cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem
                                  unsigned* flags, const int* D, int DK, int threads, int blocks, size_t smem,
                                  cudaStream_t st);
 int fused1d_blocks_per_sm(int variant, size_t smem);
+size_t fused1d_smem(Fused1D& fz);
 cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& g, const Fused1D& fz, int driver_id,
                                  int threads, int blocks, size_t smem, cudaStream_t st);
 cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
@@ -1086,13 +1087,15 @@ bsde_status bsde_solve_batch(bsde_ctx* const* cs, int32_t n, bsde_result* res) {
   cudaSetDevice(c0->cfg.device);
   // common geometry: the largest buffers of the batch
   Fused1D fz = c0->geo.fz;
-  size_t smem = c0->geo.smem;
   for (int i = 1; i < n; ++i) {
     const Fused1D& f = cs[i]->geo.fz;
     fz.WMAX = std::max(fz.WMAX, f.WMAX);
     fz.WP = std::max(fz.WP, f.WP);
-    smem = std::max(smem, cs[i]->geo.smem);
+    fz.WS = std::max(fz.WS, f.WS);
+    fz.TK = std::max(fz.TK, f.TK);
   }
+  const size_t smem = fused1d_smem(fz);
+  if (smem == 0) return set_err(c0, BSDE_ERR_RESOURCE_LIMIT, "batch: the level windows do not fit in shared memory");
   const int per_sm = fused1d_blocks_per_sm(fz.variant, smem);
   if (c0->geo.blocks > c0->nsm * per_sm)
     return set_err(c0, BSDE_ERR_RESOURCE_LIMIT, "batch: %d CTAs with %zu B of shared memory are not co-resident", c0->geo.blocks, smem);

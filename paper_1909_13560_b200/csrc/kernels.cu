@@ -10,6 +10,8 @@
 //   quad1d_fused      d = 1: level-1 spline (PCR) + quadrature on shared-memory windows
 //                     streamed by cp.async.bulk + z + Picard, one kernel per step (cfg 2)
 //   eval_kernel       spline of the newest level at one point (the evaluation point)
+#include <cstdlib>
+#include <algorithm>
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "bsde_internal.h"

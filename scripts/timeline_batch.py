@@ -38,7 +38,9 @@ for K, a in zip(Ks, A):
 ends = [a[:, :, 9] for a in A]
 starts = [a[:, :, 0] for a in A]
 for i in range(len(A) - 1):
-    print(f"p1 gap {Ks[i]}->{Ks[i+1]}: {np.median((starts[i+1] - ends[i])[st]):.2f} us")
-print(f"p1 end -> p2 start: {np.median((A[0][:, :, 10] - ends[-1])[st]):.2f} us")
+    m = min(len(starts[i + 1]), len(ends[i]))
+    print(f"p1 gap {Ks[i]}->{Ks[i+1]}: {np.median((starts[i+1][:m] - ends[i][:m])[st]):.2f} us")
+m = min(len(A[0]), len(ends[-1]))
+print(f"p1 end -> p2 start: {np.median((A[0][:m, :, 10] - ends[-1][:m])[st]):.2f} us")
 for s in ss:
     s.close()
