@@ -205,6 +205,13 @@ bsde_status bsde_group_solve(bsde_ctx** ctxs, int32_t n, bsde_result* res);
 /* Number of kernels launched by this context so far.                                  */
 bsde_status bsde_kernel_launches(const bsde_ctx* ctx, int64_t* count);
 
+/* Measured FP64 peak of `device` (the denominator of the roofline in DESIGN.md §5):
+ * a kernel of independent DFMA chains (16 per thread, 8 warps per CTA, 8 CTAs per SM) is
+ * timed with CUDA events over `iters` chain steps after one warm-up launch.  Outputs the
+ * sustained rate in TFLOP/s (DFMA = 2 flops) and the kernel time in ms.  Not thread-safe
+ * with respect to other work on the device (it owns the device while it runs).          */
+bsde_status bsde_measure_fp64_peak(int32_t device, int32_t iters, double* tflops, double* ms);
+
 /* Message of the last failing call on ctx (owned by ctx; valid until the next call), or
  * of the last failing bsde_setup/bsde_query_workspace when ctx == NULL (thread-local). */
 const char* bsde_last_error(const bsde_ctx* ctx);

@@ -7,5 +7,5 @@ problem parameters of the paper's examples and BASELINE.json's configs.
 from . import workloads  # noqa: F401
 from .bsde import (  # noqa: F401
     BsdeError, Solver, GroupSolver, bsde_config, bsde_result, load_library, make_config, query_workspace,
-    query_partition, nccl_unique_id, solve_batch, EXPORTS,
+    query_partition, nccl_unique_id, solve_batch, measure_fp64_peak, EXPORTS,
 )

@@ -27,7 +27,8 @@ TERMINALS = {"const": 0, "poly": 1, "logistic": 2, "ex2": 3, "call_w": 4, "sin_s
 EXPORTS = ["bsde_query_workspace", "bsde_setup", "bsde_step", "bsde_solve", "bsde_level", "bsde_get_layer",
            "bsde_get_picard_counts", "bsde_query_grid", "bsde_query_taps", "bsde_eval", "bsde_layer_device_ptr",
            "bsde_query_partition", "bsde_query_partition_cfg", "bsde_nccl_unique_id", "bsde_group_step",
-           "bsde_group_solve", "bsde_solve_batch", "bsde_kernel_launches", "bsde_last_error", "bsde_destroy"]
+           "bsde_group_solve", "bsde_solve_batch", "bsde_kernel_launches", "bsde_measure_fp64_peak",
+           "bsde_last_error", "bsde_destroy"]
 
 
 class BsdeError(RuntimeError):
@@ -86,6 +87,7 @@ def load_library(path: str = LIB_PATH):
             lib.bsde_group_step.argtypes = [C.POINTER(C.c_void_p), I32]
             lib.bsde_group_solve.argtypes = [C.POINTER(C.c_void_p), I32, C.POINTER(bsde_result)]
             lib.bsde_solve_batch.argtypes = [C.POINTER(C.c_void_p), I32, C.POINTER(bsde_result)]
+            lib.bsde_measure_fp64_peak.argtypes = [I32, I32, D, D]
             lib.bsde_last_error.argtypes = [P]
             lib.bsde_last_error.restype = C.c_char_p
             lib.bsde_destroy.argtypes = [P]
@@ -134,6 +136,16 @@ def make_config(spec: dict, device: int = 0, stream: int | None = None, kernel_v
     c.device = int(device)
     c.kernel_variant = int(kernel_variant)
     return c
+
+
+def measure_fp64_peak(device: int = 0, iters: int = 200000) -> dict:
+    """Measured FP64 DFMA throughput of `device` (bsde_measure_fp64_peak)."""
+    lib = load_library()
+    tf, ms = C.c_double(), C.c_double()
+    st = lib.bsde_measure_fp64_peak(int(device), int(iters), C.byref(tf), C.byref(ms))
+    if st:
+        raise BsdeError(st, lib.bsde_last_error(None).decode())
+    return {"tflops": tf.value, "ms": ms.value}
 
 
 def query_workspace(spec: dict) -> int:

@@ -104,9 +104,14 @@ __global__ void __launch_bounds__(k2NT, 1) quad2d(StepArgs s, Grid g, Problem pb
         const bool consecutive = cy >= 0 && cy + k2TY - 1 <= P0g - 2;
         mbar_wait(bar, phase);
         phase ^= 1u;
-        for (int k = tid; k < s1 - s0 + 1; k += k2NT) {
-#pragma unroll
-          for (int f = 0; f < 3; ++f) {
+        // (field, column) items spread evenly over the threads (3 x ncol items)
+        const int ncol = s1 - s0 + 1;
+        int f = 0, k = tid;
+        while (k >= ncol) { k -= ncol; ++f; }
+        for (; f < 3; k += k2NT) {
+          while (k >= ncol) { k -= ncol; ++f; }
+          if (f >= 3) break;
+          {
             const double* rc = raw + (size_t)f * (k2TY + 3) * WC + k;
             double* out = Rw + (size_t)f * k2TY * WC + (s0 - wv) + k;
             if (consecutive) {

@@ -125,9 +125,14 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
         const bool consecutive = cy >= 0 && cy + k3TY - 1 <= P1 - 2;
         mbar_wait(bar, phase);
         phase ^= 1u;
-        for (int k = tid; k < s1 - s0 + 1; k += k3NT) {
-#pragma unroll
-          for (int f = 0; f < k3F; ++f) {
+        // (field, column) items spread evenly over the threads (k3F x ncol items)
+        const int ncol = s1 - s0 + 1;
+        int f = 0, k = tid;
+        while (k >= ncol) { k -= ncol; ++f; }
+        for (; f < k3F; k += k3NT) {
+          while (k >= ncol) { k -= ncol; ++f; }
+          if (f >= k3F) break;
+          {
             const double* rc = raw + (size_t)f * (k3TY + 3) * WC + k;
             double* out = Rw + (size_t)f * k3TY * WC + (s0 - wv) + k;
             if (consecutive) {

@@ -40,6 +40,7 @@ cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem
                                  cudaStream_t st);
 int fused1d_blocks_per_sm(int variant, size_t smem);
 size_t fused1d_smem(Fused1D& fz);
+cudaError_t measure_fp64_peak(int device, int iters, double* tflops, double* ms_out);
 cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& g, const Fused1D& fz, int driver_id,
                                  int threads, int blocks, size_t smem, cudaStream_t st);
 cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
@@ -1324,6 +1325,13 @@ bsde_status bsde_eval(bsde_ctx* c, const double* x, double* out) {
 bsde_status bsde_layer_device_ptr(const bsde_ctx* c, int32_t field, const double** dptr) {
   if (!c || !dptr || field < 0 || field >= c->F) return BSDE_ERR_INVALID_ARGUMENT;
   *dptr = c->vbuf[c->cur] + (int64_t)field * c->g.npts;
+  return BSDE_OK;
+}
+
+bsde_status bsde_measure_fp64_peak(int32_t device, int32_t iters, double* tflops, double* ms) {
+  if (!tflops || !ms || iters < 1) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "fp64 peak: bad arguments");
+  const cudaError_t e = measure_fp64_peak(device, iters, tflops, ms);
+  if (e != cudaSuccess) return set_err(nullptr, BSDE_ERR_CUDA, "fp64 peak: %s", cudaGetErrorString(e));
   return BSDE_OK;
 }
 

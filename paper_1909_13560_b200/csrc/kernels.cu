@@ -633,3 +633,49 @@ cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* 
 }
 
 }  // namespace bsde
+
+namespace bsde {
+// FP64 peak probe: 16 independent DFMA chains per thread (enough ILP to cover the DFMA
+// latency at 8 warps per SM partition), results folded into one store so nothing is dead
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, double a, double b) {
+  double x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = fma(x[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += x[i];
+  if (s == 12345.678) out[0] = s;     // practically never taken; keeps the chains live
+}
+
+cudaError_t measure_fp64_peak(int device, int iters, double* tflops, double* ms_out) {
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return e;
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  double* out = nullptr;
+  if ((e = cudaMalloc(&out, sizeof(double))) != cudaSuccess) return e;
+  const int blocks = nsm * 8, threads = 256;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fp64_peak_kernel<<<blocks, threads>>>(out, iters / 10 + 1, 0.999999, 1e-7);   // warm-up (clocks up)
+  cudaEventRecord(e0);
+  fp64_peak_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+  cudaEventRecord(e1);
+  e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (e != cudaSuccess) return e;
+  const double flops = 2.0 * 16.0 * (double)iters * blocks * threads;
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  *ms_out = ms;
+  return cudaSuccess;
+}
+}  // namespace bsde

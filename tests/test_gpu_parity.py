@@ -79,7 +79,7 @@ def test_library_exports_every_header_symbol():
     from paper_1909_13560_b200 import build as b, load_library, EXPORTS
     b.build()
     hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "bsde.h")).read()
-    declared = set(re.findall(r"\b(bsde_[a-z_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b(bsde_[a-z0-9_]+)\s*\(", hdr))
     assert declared == set(EXPORTS), declared ^ set(EXPORTS)
     lib = load_library()
     for name in declared:
