@@ -314,6 +314,10 @@ def tts_sweep(dev, oracle_budget_s=90.0):
 # accumulation, K L^d taps, + Picard + spline passes
 FLOPS_CFG4 = 4 * 64 * (24 + 3 + 6 + 10) + 2 * 64 + 30 * 8 + 3 * 2 * 21
 FLOPS_CFG5 = 3 * 512 * (32 + 4 + 18 + 14) + 2 * 512 + 30 * 22 + 4 * 3 * 21
+# cfg 4 through the affine separable path (aff2.cuh): per level and field an axis-0 operator
+# (L x (4 interpolation + 2 accumulation) FMA per output) and three axis-1 operators (L x (8 + 3)
+# FMA per point) + the combination (6 FMA); Picard 30 x 4 FMA; splines as above
+FLOPS_CFG4_AFF = 2 * (4 * 3 * (6 * 8 + 11 * 8 + 6) + 30 * 4) + 3 * 2 * 21
 
 
 def d23_configs(dev, stream):
@@ -322,8 +326,10 @@ def d23_configs(dev, stream):
     import torch
     from paper_1909_13560_b200 import Solver, workloads as W
     out = {}
-    for name, spec, steps, fl in (("cfg4", W.cfg4(), 3, FLOPS_CFG4), ("cfg5", W.basket_3d(3, 64, 8, P=512), 2, FLOPS_CFG5)):
-        with Solver(spec, device=dev, stream=stream) as s:
+    for name, spec, steps, fl, kv in (("cfg4", W.cfg4(), 3, FLOPS_CFG4_AFF, 0),
+                                      ("cfg4_per_tap", W.cfg4(), 3, FLOPS_CFG4, 2),
+                                      ("cfg5", W.basket_3d(3, 64, 8, P=512), 2, FLOPS_CFG5, 0)):
+        with Solver(spec, device=dev, stream=stream, kernel_variant=kv) as s:
             npts = 1
             for n in s.shape:
                 npts *= n
@@ -337,6 +343,8 @@ def d23_configs(dev, stream):
             ms = e0.elapsed_time(e1) / steps
         ups = npts / (ms * 1e-3)
         out[name] = {"workload": spec["name"], "points": npts, "ms_per_step": ms, "updates_per_s": ups,
+                     "path": {0: "default" + (" (affine separable, aff2.cuh)" if name == "cfg4" else " (quad3d)"),
+                              2: "per-tap quad2d"}[kv],
                      "flops_per_point_step": fl, "tflops": fl * ups / 1e12,
                      "frac_fp64_peak": fl * ups / 1e12 / peak_fp64_tflops(1965.0)}
     return out

@@ -101,10 +101,11 @@ typedef struct {
                                 NULL for an in-process group driven by bsde_group_step/solve */
   void*    stream;           /* cudaStream_t to run on; NULL -> library-owned stream        */
   int32_t  device;           /* CUDA device ordinal                                         */
-  int32_t  kernel_variant;   /* 0: auto (fastest available), 1: generic reference kernels;
+  int32_t  kernel_variant;   /* 0: auto (fastest available; d = 2 with f = 0 or affine f:
+                                the separable affine path), 1: generic reference kernels;
+                                2 (d = 2): the per-tap fused 2-D kernel for every driver;
                                 10 + v (d = 1): fused kernel variant v; any other value
-                                selects the generic kernels (d >= 2: fused 2-D kernel
-                                for 0 only)                                               */
+                                selects the generic kernels                               */
 } bsde_config;
 
 typedef struct {

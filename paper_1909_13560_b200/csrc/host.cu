@@ -46,6 +46,8 @@ cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& 
 cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
 cudaError_t init_device_attributes();
 cudaError_t launch_quad2d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, cudaStream_t st);
+cudaError_t launch_aff2(const StepArgs& s, const Grid& g, const Problem& pb, double* H, double* acc, cudaStream_t st,
+                        int64_t* launches);
 int fused2d_window(const AxisTap* host_taps, int K, int L);
 size_t fused2d_smem(int WC);
 int fused3d_window(const AxisTap* host_taps, int K, int L);
@@ -476,6 +478,12 @@ void localize_grid(Grid& g, int64_t lo_e, int64_t hi_e, int64_t r0, int64_t r1) 
 
 
 
+// the d = 2 affine-driver path (aff2.cuh) is the default for f = 0 and
+// affine f; kernel_variant 2 keeps the per-tap fused kernel
+bool use_aff2(const bsde_config* cfg) {
+  return cfg->d == 2 && cfg->kernel_variant == 0 && (cfg->driver_id == 0 || cfg->driver_id == 1);
+}
+
 struct Layout {
   size_t values, ring, tmp0, tmp1, a3, acc3, picard, bad, barrier, dres, total;
 };
@@ -483,8 +491,9 @@ struct Layout {
 // other CTAs write level n)
 
 // fused3d: the d = 3 fused path's per-level plane stacks (L x F x local planes) and the
-// 5 partial sums per owned point
-Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d) {
+// 5 partial sums per owned point; aff2: the d = 2 affine path's axis-0 operators (2 x F x
+// local rows) and its 4 partial sums per owned point (same regions)
+Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d, bool aff2) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   Layout L{};
   size_t off = 0;
@@ -492,9 +501,13 @@ Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d) {
   L.ring = off; off += al(sizeof(double) * (size_t)(K + 3) * F * g.cfield);
   L.tmp0 = off; off += g.d >= 2 ? al(sizeof(double) * g.cfield) : 0;
   L.tmp1 = off; off += g.d >= 3 ? al(sizeof(double) * g.cfield) : 0;
-  const bool f3 = g.d == 3 && fused3d;
-  L.a3 = off; off += f3 ? al(sizeof(double) * (size_t)nodes * F * g.P[0] * g.cstride[0]) : 0;
-  L.acc3 = off; off += f3 ? al(sizeof(double) * 5 * (size_t)g.nown0 * g.P[1] * g.P[2]) : 0;
+  const bool f3 = g.d == 3 && fused3d, a2 = g.d == 2 && aff2;
+  L.a3 = off;
+  off += f3 ? al(sizeof(double) * (size_t)nodes * F * g.P[0] * g.cstride[0])
+            : (a2 ? al(sizeof(double) * 2 * (size_t)F * g.nown0 * g.cstride[0]) : 0);
+  L.acc3 = off;
+  off += f3 ? al(sizeof(double) * 5 * (size_t)g.nown0 * g.P[1] * g.P[2])
+            : (a2 ? al(sizeof(double) * 4 * (size_t)g.nown0 * g.P[1]) : 0);
   L.picard = off; off += al(sizeof(int32_t) * g.npts);
   L.bad = off; off += 256;
   L.barrier = off; off += al(sizeof(unsigned) * 2 * 8192);      // fused-kernel progress flags
@@ -553,7 +566,9 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
     e = launch_spline(c->g, c->vbuf[c->cur], c->F, c->ring + (int64_t)slots[0] * c->F * c->g.cfield, c->tmp0,
                       c->tmp1, c->stream, &c->launches);
     if (e == cudaSuccess) {
-      if (c->d == 2 && variant == 0 && wc2 > 0 && c->pb.driver_id != 3)
+      if (c->d == 2 && variant == 0 && c->a3 && c->acc3 && (c->pb.driver_id == 0 || c->pb.driver_id == 1))
+        e = launch_aff2(s, c->g, c->pb, c->a3, c->acc3, c->stream, &c->launches);
+      else if (c->d == 2 && (variant == 0 || variant == 2) && wc2 > 0 && c->pb.driver_id != 3)
         e = launch_quad2d(s, c->g, c->pb, wc2, c->stream);
       else if (c->d == 3 && variant == 0 && wc2 > 0 && c->pb.driver_id != 3 && c->a3 && c->acc3)
         e = launch_step3d(s, c->g, c->pb, wc2, c->a3, c->acc3, c->stream, &c->launches);
@@ -735,7 +750,7 @@ bsde_status bsde_query_workspace(const bsde_config* cfg, size_t* bytes) {
   const int K = std::max(cfg->Ky, cfg->Kz);
   Grid g{};
   fill_grid(cfg, g, (cfg->T - cfg->t0) / cfg->N);
-  *bytes = layout(g, 1 + cfg->d, K, cfg->L, cfg->kernel_variant == 0).total;
+  *bytes = layout(g, 1 + cfg->d, K, cfg->L, cfg->kernel_variant == 0, use_aff2(cfg)).total;
   return BSDE_OK;
 }
 
@@ -806,7 +821,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     }
   }
   // memory
-  Layout lay = layout(c->g, c->F, c->K, c->L, cfg->kernel_variant == 0);
+  Layout lay = layout(c->g, c->F, c->K, c->L, cfg->kernel_variant == 0, use_aff2(cfg));
   if (d_workspace) {
     if (bytes < lay.total) {
       set_err(c, BSDE_ERR_RESOURCE_LIMIT, "workspace of %zu bytes < required %zu", bytes, lay.total);

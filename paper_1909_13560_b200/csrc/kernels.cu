@@ -548,6 +548,7 @@ __global__ void __launch_bounds__(256) quad_generic(StepArgs s, Grid g, Problem 
 // ------------------------------------------------------------------ 2-D fused quadrature kernel
 #include "fused2d.cuh"
 #include "fused3d.cuh"
+#include "aff2.cuh"
 
 template <int D, int DRV>
 static cudaError_t launch_generic(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st) {

@@ -529,13 +529,15 @@ def test_slab_group_rejects_single_solve():
 
 
 @gpu
+@pytest.mark.parametrize("variant", [0, 2], ids=["affine_separable", "per_tap_quad2d"])
 @pytest.mark.parametrize("spec", [W.ex4_2d(3, 8, npts=257), W.exchange_2d(4, 8, npts=333),
-                                  dict(W.ex4_2d(2, 6), npts=[45, 701])],
+                                  dict(W.ex4_2d(2, 6), npts=[45, 701]), W.heat_poly(2, 3, N=6, P=301, L=8)],
                          ids=lambda s: s["name"] + "_" + "x".join(map(str, s["npts"])))
-def test_2d_fused_matches_generic(spec):
-    """quad2d (separable row/column passes) vs the generic direct tensor stencil."""
+def test_2d_fused_matches_generic(spec, variant):
+    """The d = 2 fast paths vs the generic direct tensor stencil: the affine separable path
+    (aff2.cuh, default for f = 0 and affine f) and the per-tap quad2d kernel (variant 2)."""
     from paper_1909_13560_b200 import Solver
-    with Solver(spec, kernel_variant=0) as a, Solver(spec, kernel_variant=1) as b:
+    with Solver(spec, kernel_variant=variant) as a, Solver(spec, kernel_variant=1) as b:
         a.solve()
         b.solve()
         for f in range(3):
@@ -593,6 +595,14 @@ def test_cfg4_full_size_first_step_sampled():
     launch configuration of the fused 2-D kernel: the first backward step on every boundary-band
     point and 2e4 random interior points."""
     n = _first_step_sampled_parity(W.cfg4(), 20000)
+    assert n > 20000
+
+
+@gpu
+def test_cfg4_full_size_first_step_sampled_per_tap():
+    """The same with the per-tap quad2d kernel (kernel_variant 2) instead of the affine
+    separable path."""
+    n = _first_step_sampled_parity(W.cfg4(), 20000, variant=2)
     assert n > 20000
 
 
