@@ -46,8 +46,10 @@ cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& 
 cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
 cudaError_t init_device_attributes();
 cudaError_t launch_quad2d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, cudaStream_t st);
-cudaError_t launch_aff2(const StepArgs& s, const Grid& g, const Problem& pb, double* H, double* acc, cudaStream_t st,
+cudaError_t launch_aff2(const StepArgs& s, const Grid& g, const Problem& pb, double* H, int WC, cudaStream_t st,
                         int64_t* launches);
+int aff2_window(const AxisTap* host_taps, int K, int L);
+size_t aff2_smem(int WC);
 int fused2d_window(const AxisTap* host_taps, int K, int L);
 size_t fused2d_smem(int WC);
 int fused3d_window(const AxisTap* host_taps, int K, int L);
@@ -77,6 +79,7 @@ struct bsde_ctx {
   int cur = 0;                  // vbuf[cur] holds the newest level
   int fused_variant = 0;        // fused 1-D kernel variant (kernel_variant = 10 + v)
   int wc2 = 0, boot_wc2 = 0;    // 2-D / 3-D fused kernel column window (0: use the generic kernel)
+  int wca = 0;                  // d = 2 affine path column window (0: not used)
   int nsm = 148;
   double* ring = nullptr;       // (RS + 1) * F * cfield ; slot RS = scratch
   int RS = 3;                   // ring slots: K + 2 (level m in slot m % RS; the 2 spare slots let the
@@ -491,8 +494,8 @@ struct Layout {
 // other CTAs write level n)
 
 // fused3d: the d = 3 fused path's per-level plane stacks (L x F x local planes) and the
-// 5 partial sums per owned point; aff2: the d = 2 affine path's axis-0 operators (2 x F x
-// local rows) and its 4 partial sums per owned point (same regions)
+// 5 partial sums per owned point; aff2: the d = 2 affine path's axis-0 operators of every
+// level (K x 2 x F x owned rows, in the a3 region)
 Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d, bool aff2) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   Layout L{};
@@ -504,10 +507,10 @@ Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d, bool aff2) {
   const bool f3 = g.d == 3 && fused3d, a2 = g.d == 2 && aff2;
   L.a3 = off;
   off += f3 ? al(sizeof(double) * (size_t)nodes * F * g.P[0] * g.cstride[0])
-            : (a2 ? al(sizeof(double) * 2 * (size_t)F * g.nown0 * g.cstride[0]) : 0);
+            : (a2 ? al(sizeof(double) * 2 * (size_t)F * K * g.nown0 * g.cstride[0]) : 0);
   L.acc3 = off;
   off += f3 ? al(sizeof(double) * 5 * (size_t)g.nown0 * g.P[1] * g.P[2])
-            : (a2 ? al(sizeof(double) * 4 * (size_t)g.nown0 * g.P[1]) : 0);
+            : 0;
   L.picard = off; off += al(sizeof(int32_t) * g.npts);
   L.bad = off; off += 256;
   L.barrier = off; off += al(sizeof(unsigned) * 2 * 8192);      // fused-kernel progress flags
@@ -566,8 +569,8 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
     e = launch_spline(c->g, c->vbuf[c->cur], c->F, c->ring + (int64_t)slots[0] * c->F * c->g.cfield, c->tmp0,
                       c->tmp1, c->stream, &c->launches);
     if (e == cudaSuccess) {
-      if (c->d == 2 && variant == 0 && c->a3 && c->acc3 && (c->pb.driver_id == 0 || c->pb.driver_id == 1))
-        e = launch_aff2(s, c->g, c->pb, c->a3, c->acc3, c->stream, &c->launches);
+      if (c->d == 2 && variant == 0 && c->a3 && c->wca > 0 && (c->pb.driver_id == 0 || c->pb.driver_id == 1))
+        e = launch_aff2(s, c->g, c->pb, c->a3, c->wca, c->stream, &c->launches);
       else if (c->d == 2 && (variant == 0 || variant == 2) && wc2 > 0 && c->pb.driver_id != 3)
         e = launch_quad2d(s, c->g, c->pb, wc2, c->stream);
       else if (c->d == 3 && variant == 0 && wc2 > 0 && c->pb.driver_id != 3 && c->a3 && c->acc3)
@@ -867,6 +870,8 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   if (c->d == 2) {
     c->wc2 = fused2d_window(c->taps.data(), c->K, c->L);
     if (fused2d_smem(c->wc2) > 220 * 1024) c->wc2 = 0;
+    c->wca = aff2_window(c->taps.data(), c->K, c->L);
+    if (aff2_smem(c->wca) > 220 * 1024) c->wca = 0;
   }
   if (c->d == 3) {
     c->wc2 = fused3d_window(c->taps.data(), c->K, c->L);

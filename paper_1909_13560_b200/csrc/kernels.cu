@@ -594,6 +594,7 @@ cudaError_t init_device_attributes() {
   if (e == cudaSuccess) e = set_attr_drv<DRV_DIFF>();
   if (e == cudaSuccess) e = set_attr_2d();
   if (e == cudaSuccess) e = set_attr_3d();
+  if (e == cudaSuccess) e = set_attr_aff2();
   return e;
 }
 
