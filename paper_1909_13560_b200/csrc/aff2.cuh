@@ -18,7 +18,7 @@
 #pragma once
 
 constexpr int kA0Rows = 8;      // aff_axis0: consecutive rows per thread
-constexpr int kA1Pts = 3;       // aff_rows: consecutive points per thread (axis 1; odd: conflict-free LDS.64)
+constexpr int kA1Pts = 5;       // aff_rows: consecutive points per thread (axis 1; odd: conflict-free LDS.64)
 
 // (A) one level, one field (blockIdx.z): H[f][0|1][i0 - own0][e] for the owned rows i0 and the
 // storage columns e < P1 + 3
@@ -38,8 +38,8 @@ __global__ void __launch_bounds__(128) aff_axis0(const double* __restrict__ C, d
     const AxisTap& t = t0[l];
     const double w = t.w, ws = t.w * t.s;
     const int64_t c0 = r0 + g.off0 + t.q;                           // global cell of row r0
-    if (c0 >= 0 && c0 + kA0Rows - 1 <= g.Pg0 - 2) {                  // no clamping: 11 rows
-      double v[kA0Rows + 3];
+    if (c0 >= 0 && c0 + kA0Rows - 1 <= g.Pg0 - 2) {                  // no clamping: kA0Rows + 3 rows
+      double v[kA0Rows + 3];             // (kA0Rows + 3) row loads for kA0Rows outputs
       const double* p = Cf + (c0 - g.off0) * cs0;
 #pragma unroll
       for (int k = 0; k < kA0Rows + 3; ++k) v[k] = __ldg(p + k * cs0);
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(128) aff_axis0(const double* __restrict__ C, d
 // scheme weights, accumulated in registers; then z explicit (Eq. 20 line 2) and y by Picard
 // (Eq. 20 line 1).  The H rows of each (level, field) -- both kinds, the tile's column window
 // -- arrive in shared memory by bulk copies, one (level, field) ahead.
-constexpr int kA1Thr = 128;
+constexpr int kA1Thr = 64;
 constexpr int kA1TX = kA1Thr * kA1Pts;
 template <int DRV>
 __global__ void __launch_bounds__(kA1Thr) aff_rows(StepArgs s, Grid g, Problem pb, const double* __restrict__ H,
