@@ -705,13 +705,22 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         // s(x_0) = (c_{-1} + 4 c_0 + c_1)/6 and s(x_{P-1}), from shared memory
         // edge CTAs: the line's virtual boundary entries, the clamped boundary values
         // s(x_0) = (c_{-1} + 4 c_0 + c_1)/6 and s(x_{P-1}), from shared memory
+        // (16-byte stores: the pad [-cpad, 0) is 16-byte aligned, cpad even; the right pad
+        // starts at P + 3, its odd-aligned head and tail take 8-byte stores)
         if (k0 == -1 && !pp.nopad) {
           const double v = (1.0 / 6.0) * coef(-1) + (2.0 / 3.0) * coef(0) + (1.0 / 6.0) * coef(1);
-          for (int64_t i = tid; i < s.cpad; i += NT) rf[-1 - i] = v;
+          double2* q = reinterpret_cast<double2*>(rf - s.cpad);
+          for (int i = tid; i < (int)(s.cpad >> 1); i += NT) q[i] = make_double2(v, v);
         }
         if (k1 == P + 1 && !pp.nopad) {
           const double v = (1.0 / 6.0) * coef(P - 2) + (2.0 / 3.0) * coef(P - 1) + (1.0 / 6.0) * coef(P);
-          for (int64_t i = tid; i < s.cpad; i += NT) rf[P + 3 + i] = v;
+          double* r0 = rf + P + 3;
+          const int h = (int)((reinterpret_cast<uintptr_t>(r0) >> 3) & 1);     // 1: odd-aligned start
+          const int n2 = (int)((s.cpad - h) >> 1);
+          double2* q = reinterpret_cast<double2*>(r0 + h);
+          for (int i = tid; i < n2; i += NT) q[i] = make_double2(v, v);
+          if (tid == 0 && h) r0[0] = v;
+          if (tid == 1 && h + 2 * n2 < s.cpad) r0[s.cpad - 1] = v;
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
