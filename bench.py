@@ -350,12 +350,12 @@ def d23_configs(dev, stream):
     return out
 
 
-def _oracle_sample(max_seconds=15.0, steps_per_K=120):
+def _oracle_sample(max_seconds=15.0, steps_per_K=120, nthreads=None):
     """Time the oracle (as it stands) on a bounded sample of cfg 2: steps_per_K backward
     steps of each K after its (untimed) setup."""
     import oracle
     from paper_1909_13560_b200 import workloads as W
-    nthreads = os.cpu_count() or 1
+    nthreads = nthreads or os.cpu_count() or 1
     tot_t, tot_u = 0.0, 0
     for K in KS:
         o = oracle.Oracle(W.cfg2(K), nthreads=nthreads)
@@ -372,9 +372,13 @@ def _oracle_sample(max_seconds=15.0, steps_per_K=120):
 
 def cpu_baseline(args):
     v, u, t, nt = _oracle_sample()
+    v1, u1, t1, _ = _oracle_sample(max_seconds=5.0, steps_per_K=4, nthreads=1)
     return {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
             "sample": f"cfg2, up to 120 backward steps per K=1..6 after untimed setup, capped at 15 s "
-                      f"({u} updates in {t:.2f} s)"}
+                      f"({u} updates in {t:.2f} s)",
+            "one_thread": {"value": v1, "unit": UNIT, "cores": 1,
+                           "sample": f"cfg2, 4 backward steps per K=1..6 ({u1} updates in {t1:.2f} s); "
+                                     "comparable to the paper's serial CPU baseline (PAPER.md:458)"}}
 
 
 def run_reference(args):

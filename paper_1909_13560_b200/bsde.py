@@ -148,9 +148,9 @@ def measure_fp64_peak(device: int = 0, iters: int = 200000) -> dict:
     return {"tflops": tf.value, "ms": ms.value}
 
 
-def query_workspace(spec: dict) -> int:
+def query_workspace(spec: dict, kernel_variant: int = 0) -> int:
     lib = load_library()
-    cfg = make_config(spec)
+    cfg = make_config(spec, kernel_variant=kernel_variant)
     n = C.c_size_t()
     st = lib.bsde_query_workspace(C.byref(cfg), C.byref(n))
     if st != BSDE_OK:

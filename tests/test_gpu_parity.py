@@ -86,6 +86,21 @@ def test_library_exports_every_header_symbol():
         assert getattr(lib, name) is not None
 
 
+def test_workspace_of_the_affine_path_cpu():
+    """The d = 2 affine path (default for f = 0 / affine f) holds the axis-0 operators of every
+    level: K x 2 kinds x F fields x owned rows x padded row length doubles more than the
+    per-tap kernel (variant 2); non-affine drivers never reserve it (host-only query)."""
+    from paper_1909_13560_b200 import query_workspace
+    spec = W.cfg4()
+    P = spec["npts"][0]
+    row = ((P + 3 + 3) // 4) * 4
+    extra = 4 * 2 * 3 * P * row * 8
+    d = query_workspace(spec) - query_workspace(spec, kernel_variant=2)
+    assert extra <= d <= extra + 256, (d, extra)
+    nonaff = W.basket_3d(3, 8, 8, P=64)              # d = 3, differential rates: unaffected
+    assert query_workspace(nonaff) >= query_workspace(nonaff, kernel_variant=2)
+
+
 def test_query_workspace_and_validation_cpu():
     from paper_1909_13560_b200 import query_workspace, BsdeError
     n = query_workspace(W.cfg2(6))
