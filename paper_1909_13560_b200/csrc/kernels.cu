@@ -313,8 +313,9 @@ static cudaError_t run_pass(PassArgs pa, bool strided, cudaStream_t st, int64_t*
   pcr_constants(pa.alpha, &pa.inv_b);
   const int64_t n = pa.P + 2;                              // outputs per line (c_{-1} .. c_P)
   if (strided) {
-    // 8 adjacent lines per CTA (64-byte coalesced rows), tiles of ~256 outputs (halo 27 %)
-    constexpr int LN = 8;
+    // 4 adjacent lines per CTA (32-byte coalesced row segments: 6 CTAs per SM instead of 3
+    // with 8 lines; cfg 4 step 4.76 -> 4.66 ms), tiles of ~256 outputs (halo 27 %)
+    constexpr int LN = 4;
     const int64_t nt = (n + 255) / 256;
     pa.TS = (int)((n + nt - 1) / nt);
     dim3 grid((unsigned)nt, (unsigned)((pa.nb1 + LN - 1) / LN), (unsigned)pa.nb0);
@@ -585,7 +586,7 @@ cudaError_t launch_generic_step(const StepArgs& s, const Grid& g, const Problem&
 // opt in to > 48 KB dynamic shared memory on the current device (called per context)
 cudaError_t init_device_attributes() {
   const int lim = 200 * 1024;
-  cudaError_t e = cudaFuncSetAttribute(spline_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaError_t e = cudaFuncSetAttribute(spline_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = set_attr_drv<DRV_ZERO>();
   if (e == cudaSuccess) e = set_attr_drv<DRV_AFFINE>();
