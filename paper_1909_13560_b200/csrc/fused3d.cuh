@@ -27,7 +27,11 @@ constexpr int k3F = 4;             // fields y, z_0, z_1, z_2
 constexpr int k3Acc = 5;           // accumulators per point: Az_0..2, Af, Ay
 
 // (1) A[l][f][i0][e] = sum_a Bt_a(l, i0) C[f][crow(l, i0) + a][e] over the plane elements e
-__global__ void axis0_pass(const double* __restrict__ C, double* __restrict__ A, Grid g, int tap_off, int j, int L) {
+// NF = 1: the single field U = sum_f uc_f C_f (the nonlinearity's argument of a decomposed
+// driver, uc = (-1, pi_0, pi_1, pi_2) for differential rates) instead of the 4 fields
+template <int NF>
+__global__ void axis0_pass(const double* __restrict__ C, double* __restrict__ A, Grid g, int tap_off, int j, int L,
+                           double4 uc) {
   const int64_t plane = g.cstride[0];
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= plane) return;
@@ -37,17 +41,33 @@ __global__ void axis0_pass(const double* __restrict__ C, double* __restrict__ A,
   double Bt[4];
   const int64_t crow = clamp_cell(i0 + g.off0 + ta.q, g.Pg0, ta.B, Bt) - g.off0;
   const int64_t P0 = g.P[0];
+  if (NF == k3F) {
 #pragma unroll
-  for (int f = 0; f < k3F; ++f) {
-    const double* c = C + (int64_t)f * g.cfield + crow * plane + e;
-    const double v = fma(Bt[0], __ldcg(c), fma(Bt[1], __ldcg(c + plane), fma(Bt[2], __ldcg(c + 2 * plane),
-                                                                              Bt[3] * __ldcg(c + 3 * plane))));
-    A[(((int64_t)l * k3F + f) * P0 + i0) * plane + e] = v;
+    for (int f = 0; f < k3F; ++f) {
+      const double* c = C + (int64_t)f * g.cfield + crow * plane + e;
+      const double v = fma(Bt[0], __ldcg(c), fma(Bt[1], __ldcg(c + plane), fma(Bt[2], __ldcg(c + 2 * plane),
+                                                                                Bt[3] * __ldcg(c + 3 * plane))));
+      A[(((int64_t)l * k3F + f) * P0 + i0) * plane + e] = v;
+    }
+  } else {
+    const double ucf[k3F] = {uc.x, uc.y, uc.z, uc.w};
+    double u = 0.0;
+#pragma unroll
+    for (int f = 0; f < k3F; ++f) {
+      const double* c = C + (int64_t)f * g.cfield + crow * plane + e;
+      const double v = fma(Bt[0], __ldcg(c), fma(Bt[1], __ldcg(c + plane), fma(Bt[2], __ldcg(c + 2 * plane),
+                                                                                Bt[3] * __ldcg(c + 3 * plane))));
+      u = fma(ucf[f], v, u);
+    }
+    A[((int64_t)l * P0 + i0) * plane + e] = u;
   }
 }
 
-// (2) one level of taps for a 4 x 256 tile of plane i0 (own rows only)
-template <int DRV>
+// (2) one level of taps for a 4 x 192 tile of plane i0 (own rows only).  NF = 4: every field
+// interpolated per tap and the driver applied; NF = 1 (decomposed differential-rates driver,
+// f = -(r y + th.z) + (R - r) max(U, 0)): only U per tap and only the nonlinear part
+// g = (R - r) max(U, 0) accumulated (the affine part is separable: lin3.cuh)
+template <int DRV, int NF>
 __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb, int WC, const double* __restrict__ A,
                                                   double* __restrict__ acc, int j, int first) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -70,6 +90,7 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
 
   Driver<DRV, 3> drv(pb.dp);
   drv.at(s.t_level[j - 1]);
+  const double Rmr = pb.dp[1] - pb.dp[0];          // NF = 1: (R - r) of the differential-rates driver
   const double czj = s.czj[j - 1], gzj = s.gzj[j - 1], gyj = s.gyj[j - 1];
   const bool yj = (j == s.Ky);
   double Az[3][k3R], Af[k3R], Ay[k3R];
@@ -87,20 +108,20 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
 
   // raw axis-1 rows of the current (l0, l1) pair: storage rows c0 .. c0 + TY + 2 of plane i0
   // of A_l0, columns [s0, s0 + nraw), all fields; streamed by bulk copies one pair ahead
-  double* const raw = Rw + (size_t)k3F * k3TY * WC;              // [4 fields][TY + 3][WC]
-  uint64_t* const bar = reinterpret_cast<uint64_t*>(raw + (size_t)k3F * (k3TY + 3) * WC);
+  double* const raw = Rw + (size_t)NF * k3TY * WC;              // [4 fields][TY + 3][WC]
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(raw + (size_t)NF * (k3TY + 3) * WC);
   const int nraw = ((s1 - s0 + 1) + 1) & ~1;
   auto first_row = [&](int l1) -> int64_t {
     const int64_t c = y0 + t1[l1].q;
     return c < 0 ? 0 : (c > P1 - 1 ? P1 - 1 : c);
   };
   auto issue_rows = [&](int l0, int l1) {        // thread 0
-    const double* Al = A + (int64_t)l0 * k3F * Afield + i0 * plane + s0;
+    const double* Al = A + (int64_t)l0 * NF * Afield + i0 * plane + s0;
     const int64_t c0 = first_row(l1);
     const int nrows = (int)(P1 + 3 - c0 < k3TY + 3 ? P1 + 3 - c0 : k3TY + 3);
     const uint32_t bytes = (uint32_t)(nraw * sizeof(double));
-    mbar_expect_tx(bar, bytes * nrows * k3F);
-    for (int f = 0; f < k3F; ++f)
+    mbar_expect_tx(bar, bytes * nrows * NF);
+    for (int f = 0; f < NF; ++f)
       for (int a = 0; a < nrows; ++a)
         bulk_g2s(raw + ((size_t)f * (k3TY + 3) + a) * WC, Al + (int64_t)f * Afield + (c0 + a) * cs1, bytes, bar);
   };
@@ -125,13 +146,13 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
         const bool consecutive = cy >= 0 && cy + k3TY - 1 <= P1 - 2;
         mbar_wait(bar, phase);
         phase ^= 1u;
-        // (field, column) items spread evenly over the threads (k3F x ncol items)
+        // (field, column) items spread evenly over the threads (NF x ncol items)
         const int ncol = s1 - s0 + 1;
         int f = 0, k = tid;
         while (k >= ncol) { k -= ncol; ++f; }
-        for (; f < k3F; k += k3NT) {
+        for (; f < NF; k += k3NT) {
           while (k >= ncol) { k -= ncol; ++f; }
-          if (f >= k3F) break;
+          if (f >= NF) break;
           {
             const double* rc = raw + (size_t)f * (k3TY + 3) * WC + k;
             double* out = Rw + (size_t)f * k3TY * WC + (s0 - wv) + k;
@@ -163,10 +184,12 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
         }
       }
       // ---- axis-2 boundary: clamped values of every row, virtual window entries
-      double bl[k3F] = {0, 0, 0, 0}, br[k3F] = {0, 0, 0, 0};
+      double bl[NF], br[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) { bl[f] = 0.0; br[f] = 0.0; }
       if (left || right) {
 #pragma unroll
-        for (int f = 0; f < k3F; ++f) {
+        for (int f = 0; f < NF; ++f) {
           const double* row = Rw + (f * k3TY + r) * WC;
           if (left) bl[f] = (1.0 / 6.0) * row[-wv] + (2.0 / 3.0) * row[1 - wv] + (1.0 / 6.0) * row[2 - wv];
           if (right)
@@ -175,7 +198,7 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
         // virtual window entries of every row (one warp per row, no index division); they
         // are disjoint from the real entries the boundary values are read from
         const int nleft = left ? -wv : 0, kright = right ? (int)P2 + 3 - wv : nwin;
-        for (int fr = tid >> 5; fr < k3F * k3TY; fr += k3NT / 32) {
+        for (int fr = tid >> 5; fr < NF * k3TY; fr += k3NT / 32) {
           double* row = Rw + fr * WC;
           const int ln = tid & 31;
           if (left) {
@@ -197,9 +220,9 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
       for (int m = 0; m < L; ++m) {
         const AxisTap& tc = t2[m];
         const int q = tc.q;
-        double v[k3F][k3R];
+        double v[NF][k3R];
 #pragma unroll
-        for (int f = 0; f < k3F; ++f) {
+        for (int f = 0; f < NF; ++f) {
           const double* rp = Rw + (f * k3TY + r) * WC + rel0 + q;
           double c[k3R + 3];
 #pragma unroll
@@ -215,30 +238,44 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
             const int cell = cb + p;
             if (cell >= -3 && cell <= -1) {
 #pragma unroll
-              for (int f = 0; f < k3F; ++f) v[f][p] = bl[f];
+              for (int f = 0; f < NF; ++f) v[f][p] = bl[f];
             }
             if (cell >= P2 - 1 && cell <= P2 + 2) {
 #pragma unroll
-              for (int f = 0; f < k3F; ++f) v[f][p] = br[f];
+              for (int f = 0; f < NF; ++f) v[f][p] = br[f];
             }
           }
         }
         const double wm = tc.w;
         const double wcz = Wcz * wm, wgy = Wgy * wm, wg = Wgz * wm;
         const double wgz0 = wg * sa, wgz1 = wg * sb, wgz2 = wg * tc.s;
+        if constexpr (NF == k3F) {
 #pragma unroll
-        for (int p = 0; p < k3R; ++p) {
-          const double zz[3] = {v[1][p], v[2][p], v[3][p]};
-          const double f = drv(v[0][p], zz);
-          Az[0][p] = fma(wcz, v[1][p], fma(wgz0, f, Az[0][p]));
-          Az[1][p] = fma(wcz, v[2][p], fma(wgz1, f, Az[1][p]));
-          Az[2][p] = fma(wcz, v[3][p], fma(wgz2, f, Az[2][p]));
-          Af[p] = fma(wgy, f, Af[p]);
-        }
-        if (yj) {
-          const double wy = W01 * wm;
+          for (int p = 0; p < k3R; ++p) {
+            const double zz[3] = {v[1 % NF][p], v[2 % NF][p], v[3 % NF][p]};
+            const double f = drv(v[0][p], zz);
+            Az[0][p] = fma(wcz, v[1 % NF][p], fma(wgz0, f, Az[0][p]));
+            Az[1][p] = fma(wcz, v[2 % NF][p], fma(wgz1, f, Az[1][p]));
+            Az[2][p] = fma(wcz, v[3 % NF][p], fma(wgz2, f, Az[2][p]));
+            Af[p] = fma(wgy, f, Af[p]);
+          }
+          if (yj) {
+            const double wy = W01 * wm;
 #pragma unroll
-          for (int p = 0; p < k3R; ++p) Ay[p] = fma(wy, v[0][p], Ay[p]);
+            for (int p = 0; p < k3R; ++p) Ay[p] = fma(wy, v[0][p], Ay[p]);
+          }
+        } else {
+          // only the nonlinear part g = (R - r) max(U, 0) of the decomposed driver
+#pragma unroll
+          for (int p = 0; p < k3R; ++p) {
+            const double u = v[0][p];
+            const double gn = Rmr * (0.5 * (u + fabs(u)));
+            Az[0][p] = fma(wgz0, gn, Az[0][p]);
+            Az[1][p] = fma(wgz1, gn, Az[1][p]);
+            Az[2][p] = fma(wgz2, gn, Az[2][p]);
+            Af[p] = fma(wgy, gn, Af[p]);
+          }
+          (void)wcz;
         }
       }
       __syncthreads();                     // Rw is rewritten by the next row pass
@@ -294,7 +331,7 @@ __global__ void epilogue_zy3(StepArgs s, Grid g, Problem pb, const double* __res
 }
 
 // shared memory of quad3d for a column-window width WC (doubles)
-size_t fused3d_smem(int WC) { return (size_t)k3F * (2 * k3TY + 3) * WC * sizeof(double) + 16; }
+size_t fused3d_smem(int WC, int nf) { return (size_t)nf * (2 * k3TY + 3) * WC * sizeof(double) + 16; }
 
 // the widest axis-2 window over the levels: TX + (q_max - q_min) on axis 2 + 4 + 2
 int fused3d_window(const AxisTap* host_taps, int K, int L) {
@@ -306,20 +343,198 @@ int fused3d_window(const AxisTap* host_taps, int K, int L) {
   return (k3TX + span + 6 + 1) & ~1;            // even: 16-byte aligned raw rows
 }
 
-template <int DRV>
+// ---------------------------------------------------------------- decomposed driver (d = 3)
+// For f = -(r y + th.z) + (R - r) max(U, 0), U = pi.z - y (differential rates), the affine part
+// Lf = -(r y + th.z) is a fixed linear combination of the fields, so its expectations -- and
+// those of z_k and y -- are separable tensor operators (as in aff2.cuh): per level
+//   E[Lf], E[Lf dW_k] (k = 0..2), E[z_k], E[y]
+// by one strided pass per axis (lin_axis: axes 0 and 1, 8 rows per thread) and one contiguous
+// pass that also adds the scheme-weighted sums to acc (lin_axis2).  quad3d<DRV_DIFF, 1> adds
+// the nonlinear part.  Exact algebra (interpolation is linear in the data).
+struct LinAxis {
+  const double* X; int64_t xb, xr, xf; int nf; double coef[4];   // input rows: sum_f coef_f X_f
+  double* Yp; double* Ys; int64_t yb, yr;                         // outputs (plain, s-weighted or null)
+  int64_t ncols, nout, ibase, off, Pg;                            // columns, output rows, clamping
+  int tap_off, j, a, L;                                           // taps of level j, axis a (d = 3)
+};
+__global__ void __launch_bounds__(128) lin_axis(LinAxis p) {
+  constexpr int RA = 8;
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= p.ncols) return;
+  const int64_t b = blockIdx.z, i0 = (int64_t)blockIdx.y * RA;
+  const AxisTap* tp = axis_taps(p.tap_off) + ((size_t)(p.j - 1) * 3 + p.a) * p.L;
+  const double* Xb = p.X + b * p.xb + col;
+  auto row = [&](int64_t r) {          // sum_f coef_f X_f[b][r][col]
+    double v = 0.0;
+    for (int f = 0; f < p.nf; ++f) v = fma(p.coef[f], __ldg(Xb + f * p.xf + r * p.xr), v);
+    return v;
+  };
+  double h[RA], hs[RA];
+#pragma unroll
+  for (int r = 0; r < RA; ++r) { h[r] = 0.0; hs[r] = 0.0; }
+  for (int l = 0; l < p.L; ++l) {
+    const AxisTap& t = tp[l];
+    const double w = t.w, ws = t.w * t.s;
+    const int64_t c0 = p.ibase + i0 + p.off + t.q;                 // global cell of output row i0
+    if (c0 >= 0 && c0 + RA - 1 <= p.Pg - 2) {
+      double v[RA + 3];
+#pragma unroll
+      for (int k = 0; k < RA + 3; ++k) v[k] = row(c0 - p.off + k);
+#pragma unroll
+      for (int r = 0; r < RA; ++r) {
+        const double u = fma(t.B[0], v[r], fma(t.B[1], v[r + 1], fma(t.B[2], v[r + 2], t.B[3] * v[r + 3])));
+        h[r] = fma(w, u, h[r]);
+        hs[r] = fma(ws, u, hs[r]);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < RA; ++r) {
+        double Bt[4];
+        const int64_t cell = clamp_cell(c0 + r, p.Pg, t.B, Bt) - p.off;
+        const double u = fma(Bt[0], row(cell), fma(Bt[1], row(cell + 1), fma(Bt[2], row(cell + 2), Bt[3] * row(cell + 3))));
+        h[r] = fma(w, u, h[r]);
+        hs[r] = fma(ws, u, hs[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RA; ++r) {
+    if (i0 + r >= p.nout) break;
+    p.Yp[b * p.yb + (i0 + r) * p.yr + col] = h[r];
+    if (p.Ys) p.Ys[b * p.yb + (i0 + r) * p.yr + col] = hs[r];
+  }
+}
+
+// the contiguous axis (2) of the 7 axis-1 outputs [owned planes (stride cstride[0])][P1][cs1] and the level's
+// scheme-weighted sums added to acc: Az_k += czj E[z_k] + gzj E[Lf dW_k], Af += gyj E[Lf],
+// Ay += [j == Ky] E[y]  (arrays: 0 Lf_pp, 1 Lf_p s1, 2 Lf_s0 p, 3..5 z_k, 6 y)
+__global__ void __launch_bounds__(128) lin_axis2(StepArgs s, Grid g, const double* __restrict__ X, int64_t astride,
+                                                 double* __restrict__ acc, int j) {
+  constexpr int R = 3;
+  const int64_t P1 = g.P[1], P2 = g.P[2], cs1 = g.cstride[1];
+  const int64_t i2 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * R;
+  if (i2 >= P2) return;
+  const int64_t i1 = blockIdx.y, i0 = blockIdx.z;               // owned plane (relative)
+  const int L = s.L;
+  const AxisTap* tp = axis_taps(s.tap_off) + ((size_t)(j - 1) * 3 + 2) * L;
+  const double* Xr = X + i0 * g.cstride[0] + i1 * cs1;          // arrays: [owned plane][P1 rows][cs1]
+  double E[8][R];                          // Lf, Lf dW2, Lf dW1, Lf dW0, z0, z1, z2, y
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+#pragma unroll
+    for (int q = 0; q < R; ++q) E[k][q] = 0.0;
+  const bool yj = (j == s.Ky);
+  for (int m = 0; m < L; ++m) {
+    const AxisTap& t = tp[m];
+    const double w = t.w, ws = t.w * t.s;
+    const int64_t c0 = i2 + t.q;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      if (k == 6 && !yj) continue;
+      const double* xr = Xr + k * astride;
+      double u[R];
+      if (c0 >= 0 && c0 + R - 1 <= P2 - 2) {
+        double v[R + 3];
+#pragma unroll
+        for (int q = 0; q < R + 3; ++q) v[q] = __ldg(xr + c0 + q);
+#pragma unroll
+        for (int q = 0; q < R; ++q) u[q] = fma(t.B[0], v[q], fma(t.B[1], v[q + 1], fma(t.B[2], v[q + 2], t.B[3] * v[q + 3])));
+      } else {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          double Bt[4];
+          const int64_t cell = clamp_cell(c0 + q, P2, t.B, Bt);
+          u[q] = fma(Bt[0], __ldg(xr + cell), fma(Bt[1], __ldg(xr + cell + 1), fma(Bt[2], __ldg(xr + cell + 2), Bt[3] * __ldg(xr + cell + 3))));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (k == 0) { E[0][q] = fma(w, u[q], E[0][q]); E[1][q] = fma(ws, u[q], E[1][q]); }
+        else E[k + 1][q] = fma(w, u[q], E[k + 1][q]);
+      }
+    }
+  }
+  const double czj = s.czj[j - 1], gzj = s.gzj[j - 1], gyj = s.gyj[j - 1];
+  const int64_t nown = g.nown0 * P1 * P2;
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    if (i2 + q >= P2) break;
+    const int64_t o = (i0 * P1 + i1) * P2 + i2 + q;
+    acc[o] += czj * E[4][q] + gzj * E[3][q];                   // Az_0: E[z_0], E[Lf dW_0]
+    acc[nown + o] += czj * E[5][q] + gzj * E[2][q];            // Az_1
+    acc[2 * nown + o] += czj * E[6][q] + gzj * E[1][q];        // Az_2
+    acc[3 * nown + o] += gyj * E[0][q];                        // Af
+    if (yj) acc[4 * nown + o] += E[7][q];                      // Ay
+  }
+}
+
+// the affine part of a level: axis 0 from the ring slot C (6 arrays: Lf, Lf s0, z_0..2, y), axis 1
+// (7 arrays), axis 2 + accumulation; W0 / W1 hold 6 / 7 arrays of (owned planes) x cstride[0]
+static cudaError_t launch_lin3(const StepArgs& s, const Grid& g, const Problem& pb, const double* C, double* W0,
+                               double* W1, double* acc, int j, cudaStream_t st, int64_t* launches) {
+  const int64_t plane = g.cstride[0], cs1 = g.cstride[1], P1 = g.P[1], P2 = g.P[2];
+  const int64_t arr = g.nown0 * plane;                 // one array of W0 / W1
+  const double r = pb.dp[0], th0 = pb.dp[2], th1 = pb.dp[3], th2 = pb.dp[4];
+  // axis 0: rows = coefficient planes of the slab, columns = plane elements
+  auto ax0 = [&](int nf0, int nf, const double* cf, double* yp, double* ys) {
+    LinAxis p{};
+    p.X = C + (int64_t)nf0 * g.cfield; p.xb = 0; p.xr = plane; p.xf = g.cfield; p.nf = nf;
+    for (int f = 0; f < nf; ++f) p.coef[f] = cf[f];
+    p.Yp = yp; p.Ys = ys; p.yb = 0; p.yr = plane;
+    p.ncols = plane; p.nout = g.nown0; p.ibase = g.own0; p.off = g.off0; p.Pg = g.Pg0;
+    p.tap_off = s.tap_off; p.j = j; p.a = 0; p.L = s.L;
+    const dim3 gr((unsigned)((plane + 127) / 128), (unsigned)((g.nown0 + 7) / 8), 1);
+    lin_axis<<<gr, 128, 0, st>>>(p);
+  };
+  const double cLf[4] = {-r, -th0, -th1, -th2}, one[1] = {1.0};
+  ax0(0, 4, cLf, W0, W0 + arr);                        // Lf (plain, s0)
+  for (int k = 0; k < 3; ++k) ax0(1 + k, 1, one, W0 + (2 + k) * arr, nullptr);
+  const bool yj = (j == s.Ky);
+  if (yj) ax0(0, 1, one, W0 + 5 * arr, nullptr);
+  // axis 1: batch = owned plane, rows = axis-1 coefficient rows, columns = cs1
+  auto ax1 = [&](const double* x, double* yp, double* ys) {
+    LinAxis p{};
+    p.X = x; p.xb = plane; p.xr = cs1; p.xf = 0; p.nf = 1; p.coef[0] = 1.0;
+    p.Yp = yp; p.Ys = ys; p.yb = plane; p.yr = cs1;
+    p.ncols = cs1; p.nout = P1; p.ibase = 0; p.off = 0; p.Pg = P1;
+    p.tap_off = s.tap_off; p.j = j; p.a = 1; p.L = s.L;
+    const dim3 gr((unsigned)((cs1 + 127) / 128), (unsigned)((P1 + 7) / 8), (unsigned)g.nown0);
+    lin_axis<<<gr, 128, 0, st>>>(p);
+  };
+  ax1(W0, W1, W1 + arr);                               // Lf_pp, Lf_p s1
+  ax1(W0 + arr, W1 + 2 * arr, nullptr);                // Lf_s0 p
+  for (int k = 0; k < 3; ++k) ax1(W0 + (2 + k) * arr, W1 + (3 + k) * arr, nullptr);
+  if (yj) ax1(W0 + 5 * arr, W1 + 6 * arr, nullptr);
+  const dim3 g2((unsigned)((P2 + 3 * 128 - 1) / (3 * 128)), (unsigned)P1, (unsigned)g.nown0);
+  lin_axis2<<<g2, 128, 0, st>>>(s, g, W1, arr, acc, j);
+  if (launches) *launches += 4 + (yj ? 2 : 0) + 4 + 1;
+  return cudaGetLastError();
+}
+
+template <int DRV, int NF>
 static cudaError_t launch_step3d_t(const StepArgs& s, const Grid& g, const Problem& pb, int WC, double* A,
                                    double* acc, cudaStream_t st, int64_t* launches) {
-  const size_t smem = fused3d_smem(WC);
+  const size_t smem = fused3d_smem(WC, NF);
   const int64_t plane = g.cstride[0];
+  const double4 uc = make_double4(-1.0, pb.dp[5], pb.dp[6], pb.dp[7]);     // U = pi.z - y (NF = 1)
   for (int j = 1; j <= s.K; ++j) {
     const double* C = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
     dim3 ga((unsigned)((plane + 255) / 256), (unsigned)g.P[0], (unsigned)s.L);
-    axis0_pass<<<ga, 256, 0, st>>>(C, A, g, s.tap_off, j, s.L);
+    axis0_pass<NF><<<ga, 256, 0, st>>>(C, A, g, s.tap_off, j, s.L, uc);
     dim3 gq((unsigned)((g.P[2] + k3TX - 1) / k3TX), (unsigned)((g.P[1] + k3TY - 1) / k3TY), (unsigned)g.nown0);
-    quad3d<DRV><<<gq, k3NT, smem, st>>>(s, g, pb, WC, A, acc, j, j == 1 ? 1 : 0);
+    quad3d<DRV, NF><<<gq, k3NT, smem, st>>>(s, g, pb, WC, A, acc, j, j == 1 ? 1 : 0);
     if (launches) *launches += 2;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+  }
+  if (NF == 1) {       // the affine part of the decomposed driver (after the plane stacks' use)
+    double* W0 = A + (int64_t)s.L * g.P[0] * plane;
+    double* W1 = W0 + 6 * g.nown0 * plane;
+    for (int j = 1; j <= s.K; ++j) {
+      const double* C = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
+      cudaError_t e = launch_lin3(s, g, pb, C, W0, W1, acc, j, st, launches);
+      if (e != cudaSuccess) return e;
+    }
   }
   const int64_t nown = g.nown0 * g.P[1] * g.P[2];
   epilogue_zy3<DRV><<<(unsigned)((nown + 255) / 256), 256, 0, st>>>(s, g, pb, acc);
@@ -330,21 +545,24 @@ static cudaError_t launch_step3d_t(const StepArgs& s, const Grid& g, const Probl
 // one d = 3 step: K x (axis-0 pass + quad3d) + epilogue; A holds L x 4 plane stacks of the
 // local slab, acc 5 x (owned points) doubles
 cudaError_t launch_step3d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, double* A, double* acc,
-                          cudaStream_t st, int64_t* launches) {
-  if (fused3d_smem(WC) > 112 * 1024) return cudaErrorInvalidConfiguration;
+                          int decompose, cudaStream_t st, int64_t* launches) {
+  if (fused3d_smem(WC, k3F) > 112 * 1024) return cudaErrorInvalidConfiguration;
   switch (pb.driver_id) {
-    case DRV_ZERO: return launch_step3d_t<DRV_ZERO>(s, g, pb, WC, A, acc, st, launches);
-    case DRV_AFFINE: return launch_step3d_t<DRV_AFFINE>(s, g, pb, WC, A, acc, st, launches);
-    case DRV_EX1: return launch_step3d_t<DRV_EX1>(s, g, pb, WC, A, acc, st, launches);
-    case DRV_DIFF: return launch_step3d_t<DRV_DIFF>(s, g, pb, WC, A, acc, st, launches);
+    case DRV_ZERO: return launch_step3d_t<DRV_ZERO, k3F>(s, g, pb, WC, A, acc, st, launches);
+    case DRV_AFFINE: return launch_step3d_t<DRV_AFFINE, k3F>(s, g, pb, WC, A, acc, st, launches);
+    case DRV_EX1: return launch_step3d_t<DRV_EX1, k3F>(s, g, pb, WC, A, acc, st, launches);
+    case DRV_DIFF:
+      return decompose ? launch_step3d_t<DRV_DIFF, 1>(s, g, pb, WC, A, acc, st, launches)
+                       : launch_step3d_t<DRV_DIFF, k3F>(s, g, pb, WC, A, acc, st, launches);
   }
   return cudaErrorInvalidValue;
 }
 
 static cudaError_t set_attr_3d() {
-  cudaError_t e = cudaFuncSetAttribute(quad3d<DRV_ZERO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad3d<DRV_AFFINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad3d<DRV_EX1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad3d<DRV_DIFF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(quad3d<DRV_ZERO, k3F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad3d<DRV_AFFINE, k3F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad3d<DRV_EX1, k3F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad3d<DRV_DIFF, k3F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(quad3d<DRV_DIFF, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
   return e;
 }

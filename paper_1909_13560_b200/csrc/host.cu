@@ -53,9 +53,9 @@ size_t aff2_smem(int WC);
 int fused2d_window(const AxisTap* host_taps, int K, int L);
 size_t fused2d_smem(int WC);
 int fused3d_window(const AxisTap* host_taps, int K, int L);
-size_t fused3d_smem(int WC);
+size_t fused3d_smem(int WC, int nf);
 cudaError_t launch_step3d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, double* A, double* acc,
-                          cudaStream_t st, int64_t* launches);
+                          int decompose, cudaStream_t st, int64_t* launches);
 }  // namespace bsde
 
 using namespace bsde;
@@ -506,7 +506,9 @@ Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d, bool aff2) {
   L.tmp1 = off; off += g.d >= 3 ? al(sizeof(double) * g.cfield) : 0;
   const bool f3 = g.d == 3 && fused3d, a2 = g.d == 2 && aff2;
   L.a3 = off;
-  off += f3 ? al(sizeof(double) * (size_t)nodes * F * g.P[0] * g.cstride[0])
+  // d = 3: L x F plane stacks, or (decomposed differential-rates driver) L single-field stacks
+  // + the 13 arrays of its separable affine part
+  off += f3 ? al(sizeof(double) * (size_t)std::max(nodes * F, nodes + 13) * g.P[0] * g.cstride[0])
             : (a2 ? al(sizeof(double) * 2 * (size_t)F * K * g.nown0 * g.cstride[0]) : 0);
   L.acc3 = off;
   off += f3 ? al(sizeof(double) * 5 * (size_t)g.nown0 * g.P[1] * g.P[2])
@@ -573,8 +575,9 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
         e = launch_aff2(s, c->g, c->pb, c->a3, c->wca, c->stream, &c->launches);
       else if (c->d == 2 && (variant == 0 || variant == 2) && wc2 > 0 && c->pb.driver_id != 3)
         e = launch_quad2d(s, c->g, c->pb, wc2, c->stream);
-      else if (c->d == 3 && variant == 0 && wc2 > 0 && c->pb.driver_id != 3 && c->a3 && c->acc3)
-        e = launch_step3d(s, c->g, c->pb, wc2, c->a3, c->acc3, c->stream, &c->launches);
+      else if (c->d == 3 && (variant == 0 || variant == 2) && wc2 > 0 && c->pb.driver_id != 3 && c->a3 && c->acc3)
+        e = launch_step3d(s, c->g, c->pb, wc2, c->a3, c->acc3, variant == 0 && c->pb.driver_id == 4, c->stream,
+                          &c->launches);
       else
         e = launch_generic_step(s, c->g, c->pb, c->stream);
       ++c->launches;
@@ -753,7 +756,7 @@ bsde_status bsde_query_workspace(const bsde_config* cfg, size_t* bytes) {
   const int K = std::max(cfg->Ky, cfg->Kz);
   Grid g{};
   fill_grid(cfg, g, (cfg->T - cfg->t0) / cfg->N);
-  *bytes = layout(g, 1 + cfg->d, K, cfg->L, cfg->kernel_variant == 0, use_aff2(cfg)).total;
+  *bytes = layout(g, 1 + cfg->d, K, cfg->L, cfg->kernel_variant == 0 || cfg->kernel_variant == 2, use_aff2(cfg)).total;
   return BSDE_OK;
 }
 
@@ -824,7 +827,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     }
   }
   // memory
-  Layout lay = layout(c->g, c->F, c->K, c->L, cfg->kernel_variant == 0, use_aff2(cfg));
+  Layout lay = layout(c->g, c->F, c->K, c->L, cfg->kernel_variant == 0 || cfg->kernel_variant == 2, use_aff2(cfg));
   if (d_workspace) {
     if (bytes < lay.total) {
       set_err(c, BSDE_ERR_RESOURCE_LIMIT, "workspace of %zu bytes < required %zu", bytes, lay.total);
@@ -875,7 +878,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   }
   if (c->d == 3) {
     c->wc2 = fused3d_window(c->taps.data(), c->K, c->L);
-    if (fused3d_smem(c->wc2) > 112 * 1024) c->wc2 = 0;
+    if (fused3d_smem(c->wc2, 4) > 112 * 1024) c->wc2 = 0;
   }
   if (c->d == 1) {
     c->geo.ok = fused1d_geometry(c->g, c->K, c->L, c->qspan, c->nsm, c->fused_variant, c->geo.fz,
@@ -931,7 +934,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     }
     if (c->d == 3) {
       c->boot_wc2 = fused3d_window(bt.data(), 1, c->L);
-      if (fused3d_smem(c->boot_wc2) > 112 * 1024) c->boot_wc2 = 0;
+      if (fused3d_smem(c->boot_wc2, 4) > 112 * 1024) c->boot_wc2 = 0;
     }
     const double g1[2] = {0.5, 0.5};
     {

@@ -456,6 +456,23 @@ def test_3d_fused_matches_generic(spec):
 
 
 @gpu
+@pytest.mark.parametrize("spec", [W.basket_3d(K=3, N=6, L=8, P=40), dict(W.basket_3d(K=2, N=5, L=6, P=21), npts=[17, 23, 401])],
+                         ids=lambda s: s["name"] + "_" + "x".join(map(str, s["npts"])))
+def test_3d_decomposed_driver_matches_per_tap(spec):
+    """The decomposed differential-rates path (U = pi.z - y per tap, separable affine part;
+    default) vs the per-tap quad3d kernel (kernel_variant 2) and the generic kernel."""
+    from paper_1909_13560_b200 import Solver
+    with Solver(spec, kernel_variant=0) as a, Solver(spec, kernel_variant=2) as b, Solver(spec, kernel_variant=1) as c:
+        a.solve()
+        b.solve()
+        c.solve()
+        for f in range(4):
+            assert relerr(a.layer(f), b.layer(f)) <= 1e-13, f
+            assert relerr(a.layer(f), c.layer(f)) <= 1e-13, f
+        assert np.array_equal(a.picard_counts(), b.picard_counts())
+
+
+@gpu
 def test_determinism_bitwise():
     from paper_1909_13560_b200 import Solver
     spec = W.diff_rates(6, N=32, P=8193)
