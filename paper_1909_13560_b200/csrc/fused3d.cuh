@@ -357,6 +357,7 @@ struct LinAxis {
   int64_t ncols, nout, ibase, off, Pg;                            // columns, output rows, clamping
   int tap_off, j, a, L;                                           // taps of level j, axis a (d = 3)
 };
+template <int NFI>     // input fields combined per row (compile time: the row loads issue together)
 __global__ void __launch_bounds__(128) lin_axis(LinAxis p) {
   constexpr int RA = 8;
   const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -366,7 +367,8 @@ __global__ void __launch_bounds__(128) lin_axis(LinAxis p) {
   const double* Xb = p.X + b * p.xb + col;
   auto row = [&](int64_t r) {          // sum_f coef_f X_f[b][r][col]
     double v = 0.0;
-    for (int f = 0; f < p.nf; ++f) v = fma(p.coef[f], __ldg(Xb + f * p.xf + r * p.xr), v);
+#pragma unroll
+    for (int f = 0; f < NFI; ++f) v = fma(p.coef[f], __ldg(Xb + f * p.xf + r * p.xr), v);
     return v;
   };
   double h[RA], hs[RA];
@@ -484,7 +486,8 @@ static cudaError_t launch_lin3(const StepArgs& s, const Grid& g, const Problem& 
     p.ncols = plane; p.nout = g.nown0; p.ibase = g.own0; p.off = g.off0; p.Pg = g.Pg0;
     p.tap_off = s.tap_off; p.j = j; p.a = 0; p.L = s.L;
     const dim3 gr((unsigned)((plane + 127) / 128), (unsigned)((g.nown0 + 7) / 8), 1);
-    lin_axis<<<gr, 128, 0, st>>>(p);
+    if (nf == 4) lin_axis<4><<<gr, 128, 0, st>>>(p);
+    else lin_axis<1><<<gr, 128, 0, st>>>(p);
   };
   const double cLf[4] = {-r, -th0, -th1, -th2}, one[1] = {1.0};
   ax0(0, 4, cLf, W0, W0 + arr);                        // Lf (plain, s0)
@@ -499,7 +502,7 @@ static cudaError_t launch_lin3(const StepArgs& s, const Grid& g, const Problem& 
     p.ncols = cs1; p.nout = P1; p.ibase = 0; p.off = 0; p.Pg = P1;
     p.tap_off = s.tap_off; p.j = j; p.a = 1; p.L = s.L;
     const dim3 gr((unsigned)((cs1 + 127) / 128), (unsigned)((P1 + 7) / 8), (unsigned)g.nown0);
-    lin_axis<<<gr, 128, 0, st>>>(p);
+    lin_axis<1><<<gr, 128, 0, st>>>(p);
   };
   ax1(W0, W1, W1 + arr);                               // Lf_pp, Lf_p s1
   ax1(W0 + arr, W1 + 2 * arr, nullptr);                // Lf_s0 p
