@@ -318,6 +318,11 @@ FLOPS_CFG5 = 3 * 512 * (32 + 4 + 18 + 14) + 2 * 512 + 30 * 22 + 4 * 3 * 21
 # (L x (4 interpolation + 2 accumulation) FMA per output) and three axis-1 operators (L x (8 + 3)
 # FMA per point) + the combination (6 FMA); Picard 30 x 4 FMA; splines as above
 FLOPS_CFG4_AFF = 2 * (4 * 3 * (6 * 8 + 11 * 8 + 6) + 30 * 4) + 3 * 2 * 21
+# cfg 5 through the decomposed differential-rates path: per level the per-tap part on U alone
+# (L^3 x (4 interpolation + 4 accumulation FMA + 3 for the nonlinearity) + row-pass and
+# plane-stack shares) and the separable affine part (3 axis passes over 5 / 6 / 7 arrays);
+# Picard 30 x 22; splines 4 fields x 3 axes x 21
+FLOPS_CFG5_DEC = 3 * (19 * 512 + 683 + 320 + 197 * 8 + 12) + 30 * 22 + 4 * 3 * 21
 
 
 def d23_configs(dev, stream):
@@ -328,7 +333,8 @@ def d23_configs(dev, stream):
     out = {}
     for name, spec, steps, fl, kv in (("cfg4", W.cfg4(), 3, FLOPS_CFG4_AFF, 0),
                                       ("cfg4_per_tap", W.cfg4(), 3, FLOPS_CFG4, 2),
-                                      ("cfg5", W.basket_3d(3, 64, 8, P=512), 2, FLOPS_CFG5, 0)):
+                                      ("cfg5", W.basket_3d(3, 64, 8, P=512), 2, FLOPS_CFG5_DEC, 0),
+                                      ("cfg5_per_tap", W.basket_3d(3, 64, 8, P=512), 2, FLOPS_CFG5, 2)):
         with Solver(spec, device=dev, stream=stream, kernel_variant=kv) as s:
             npts = 1
             for n in s.shape:
@@ -343,8 +349,9 @@ def d23_configs(dev, stream):
             ms = e0.elapsed_time(e1) / steps
         ups = npts / (ms * 1e-3)
         out[name] = {"workload": spec["name"], "points": npts, "ms_per_step": ms, "updates_per_s": ups,
-                     "path": {0: "default" + (" (affine separable, aff2.cuh)" if name == "cfg4" else " (quad3d)"),
-                              2: "per-tap quad2d"}[kv],
+                     "path": {0: "default" + (" (affine separable, aff2.cuh)" if name == "cfg4"
+                                              else " (decomposed driver: quad3d on U + separable affine part)"),
+                              2: "per-tap " + ("quad2d" if name.startswith("cfg4") else "quad3d")}[kv],
                      "flops_per_point_step": fl, "tflops": fl * ups / 1e12,
                      "frac_fp64_peak": fl * ups / 1e12 / peak_fp64_tflops(1965.0)}
     return out
