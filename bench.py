@@ -319,10 +319,10 @@ FLOPS_CFG5 = 3 * 512 * (32 + 4 + 18 + 14) + 2 * 512 + 30 * 22 + 4 * 3 * 21
 # FMA per point) + the combination (6 FMA); Picard 30 x 4 FMA; splines as above
 FLOPS_CFG4_AFF = 2 * (4 * 3 * (6 * 8 + 11 * 8 + 6) + 30 * 4) + 3 * 2 * 21
 # cfg 5 through the decomposed differential-rates path: per level the per-tap part on U alone
-# (L^3 x (4 interpolation + 4 accumulation FMA + 3 for the nonlinearity) + row-pass and
-# plane-stack shares) and the separable affine part (3 axis passes over 5 / 6 / 7 arrays);
-# Picard 30 x 22; splines 4 fields x 3 axes x 21
-FLOPS_CFG5_DEC = 3 * (19 * 512 + 683 + 320 + 197 * 8 + 12) + 30 * 22 + 4 * 3 * 21
+# (L^3 x (4 interpolation FMA + 1 add for 2 max(U, 0) + 2 accumulation FMA; the pair weights
+# are applied once per (l0, l1)) + row-pass and plane-stack shares) and the separable affine
+# part (3 axis passes over 5 / 6 / 7 arrays); Picard 30 x 22; splines 4 fields x 3 axes x 21
+FLOPS_CFG5_DEC = 3 * (13 * 512 + 683 + 320 + 197 * 8 + 12) + 30 * 22 + 4 * 3 * 21
 
 
 def d23_configs(dev, stream):

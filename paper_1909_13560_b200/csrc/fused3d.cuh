@@ -217,6 +217,11 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
       const double Wcz = W01 * czj, Wgz = W01 * gzj, Wgy = W01 * gyj;
       const double sa = ta.s, sb = tb.s;
       const int rel0 = cx0 - wv;
+      // NF = 1: sums over the axis-2 nodes of w_m g' and w_m s_m g' (g' = U + |U| = 2 max(U, 0)),
+      // scaled once per (l0, l1) pair below
+      double Sg[k3R], Sgs[k3R];
+#pragma unroll
+      for (int p = 0; p < k3R; ++p) { Sg[p] = 0.0; Sgs[p] = 0.0; }
       for (int m = 0; m < L; ++m) {
         const AxisTap& tc = t2[m];
         const int q = tc.q;
@@ -266,16 +271,26 @@ __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb
           }
         } else {
           // only the nonlinear part g = (R - r) max(U, 0) of the decomposed driver
+          const double wms = wm * tc.s;
 #pragma unroll
           for (int p = 0; p < k3R; ++p) {
             const double u = v[0][p];
-            const double gn = Rmr * (0.5 * (u + fabs(u)));
-            Az[0][p] = fma(wgz0, gn, Az[0][p]);
-            Az[1][p] = fma(wgz1, gn, Az[1][p]);
-            Az[2][p] = fma(wgz2, gn, Az[2][p]);
-            Af[p] = fma(wgy, gn, Af[p]);
+            const double g2 = u + fabs(u);                 // 2 max(U, 0)
+            Sg[p] = fma(wm, g2, Sg[p]);
+            Sgs[p] = fma(wms, g2, Sgs[p]);
           }
-          (void)wcz;
+          (void)wcz; (void)wgy; (void)wgz0; (void)wgz1; (void)wgz2;
+        }
+      }
+      if constexpr (NF == 1) {             // the pair's share: weights W01 w_m, dW factors s_a, s_b, s_m
+        const double h = 0.5 * Rmr;
+        const double cg0 = Wgz * sa * h, cg1 = Wgz * sb * h, cg2 = Wgz * h, cgy = Wgy * h;
+#pragma unroll
+        for (int p = 0; p < k3R; ++p) {
+          Az[0][p] = fma(cg0, Sg[p], Az[0][p]);
+          Az[1][p] = fma(cg1, Sg[p], Az[1][p]);
+          Az[2][p] = fma(cg2, Sgs[p], Az[2][p]);
+          Af[p] = fma(cgy, Sg[p], Af[p]);
         }
       }
       __syncthreads();                     // Rw is rewritten by the next row pass
