@@ -63,6 +63,47 @@ __global__ void axis0_pass(const double* __restrict__ C, double* __restrict__ A,
   }
 }
 
+// (1') the plane stacks of U = sum_f uc_f C_f for the decomposed driver: a thread owns one
+// plane element and 8 consecutive planes and loops over the L axis-0 nodes, so each coefficient
+// row is fetched (11/8) times per node instead of 4 times per (node, plane) as in axis0_pass
+__global__ void __launch_bounds__(128) axis0_u(const double* __restrict__ C, double* __restrict__ A, Grid g,
+                                               int tap_off, int j, int L, double4 uc) {
+  constexpr int RA = 8;
+  const int64_t plane = g.cstride[0];
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= plane) return;
+  const int64_t i0 = (int64_t)blockIdx.y * RA;                   // first local plane
+  const int64_t P0 = g.P[0];
+  const AxisTap* t0 = axis_taps(tap_off) + (size_t)(j - 1) * 3 * L;
+  const double* Ce = C + e;
+  auto row = [&](int64_t r) {           // U at storage plane r, element e
+    const double* c = Ce + r * plane;
+    return fma(uc.x, __ldg(c), fma(uc.y, __ldg(c + g.cfield), fma(uc.z, __ldg(c + 2 * g.cfield), uc.w * __ldg(c + 3 * g.cfield))));
+  };
+  for (int l = 0; l < L; ++l) {
+    const AxisTap& t = t0[l];
+    const int64_t c0 = i0 + g.off0 + t.q;                          // global cell of plane i0
+    double out[RA];
+    if (c0 >= 0 && c0 + RA - 1 <= g.Pg0 - 2) {
+      double v[RA + 3];
+#pragma unroll
+      for (int k = 0; k < RA + 3; ++k) v[k] = row(c0 - g.off0 + k);
+#pragma unroll
+      for (int r = 0; r < RA; ++r) out[r] = fma(t.B[0], v[r], fma(t.B[1], v[r + 1], fma(t.B[2], v[r + 2], t.B[3] * v[r + 3])));
+    } else {
+#pragma unroll
+      for (int r = 0; r < RA; ++r) {
+        double Bt[4];
+        const int64_t cell = clamp_cell(c0 + r, g.Pg0, t.B, Bt) - g.off0;
+        out[r] = fma(Bt[0], row(cell), fma(Bt[1], row(cell + 1), fma(Bt[2], row(cell + 2), Bt[3] * row(cell + 3))));
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RA; ++r)
+      if (i0 + r < P0) A[((int64_t)l * P0 + i0 + r) * plane + e] = out[r];
+  }
+}
+
 // (2) one level of taps for a 4 x 192 tile of plane i0 (own rows only).  NF = 4: every field
 // interpolated per tap and the driver applied; NF = 1 (decomposed differential-rates driver,
 // f = -(r y + th.z) + (R - r) max(U, 0)): only U per tap and only the nonlinear part
@@ -537,8 +578,13 @@ static cudaError_t launch_step3d_t(const StepArgs& s, const Grid& g, const Probl
   const double4 uc = make_double4(-1.0, pb.dp[5], pb.dp[6], pb.dp[7]);     // U = pi.z - y (NF = 1)
   for (int j = 1; j <= s.K; ++j) {
     const double* C = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
-    dim3 ga((unsigned)((plane + 255) / 256), (unsigned)g.P[0], (unsigned)s.L);
-    axis0_pass<NF><<<ga, 256, 0, st>>>(C, A, g, s.tap_off, j, s.L, uc);
+    if (NF == 1) {
+      dim3 gu((unsigned)((plane + 127) / 128), (unsigned)((g.P[0] + 7) / 8), 1);
+      axis0_u<<<gu, 128, 0, st>>>(C, A, g, s.tap_off, j, s.L, uc);
+    } else {
+      dim3 ga((unsigned)((plane + 255) / 256), (unsigned)g.P[0], (unsigned)s.L);
+      axis0_pass<NF><<<ga, 256, 0, st>>>(C, A, g, s.tap_off, j, s.L, uc);
+    }
     dim3 gq((unsigned)((g.P[2] + k3TX - 1) / k3TX), (unsigned)((g.P[1] + k3TY - 1) / k3TY), (unsigned)g.nown0);
     quad3d<DRV, NF><<<gq, k3NT, smem, st>>>(s, g, pb, WC, A, acc, j, j == 1 ? 1 : 0);
     if (launches) *launches += 2;
