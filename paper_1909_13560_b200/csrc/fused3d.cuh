@@ -17,6 +17,10 @@
 // Exact algebra: per tap 4 FMA per field instead of the direct 64-term tricubic stencil
 // (DESIGN.md §4).  Axis-1 clamping is per row in the row pass, axis-2 clamping uses the
 // virtual-window extension of the 1-D and 2-D kernels.
+// The differential-rates driver (cfg 5) runs decomposed by default: its nonlinearity depends on
+// the single combination U = pi.z - y, so (1') `axis0_u` builds plane stacks of U alone and
+// quad3d<DRV_DIFF, 1> interpolates only U per tap; the affine remainder's expectations are
+// separable (`lin_axis`, `lin_axis2`, below).
 #pragma once
 
 constexpr int k3TY = 4;            // tile rows (axis 1)
@@ -27,11 +31,7 @@ constexpr int k3F = 4;             // fields y, z_0, z_1, z_2
 constexpr int k3Acc = 5;           // accumulators per point: Az_0..2, Af, Ay
 
 // (1) A[l][f][i0][e] = sum_a Bt_a(l, i0) C[f][crow(l, i0) + a][e] over the plane elements e
-// NF = 1: the single field U = sum_f uc_f C_f (the nonlinearity's argument of a decomposed
-// driver, uc = (-1, pi_0, pi_1, pi_2) for differential rates) instead of the 4 fields
-template <int NF>
-__global__ void axis0_pass(const double* __restrict__ C, double* __restrict__ A, Grid g, int tap_off, int j, int L,
-                           double4 uc) {
+__global__ void axis0_pass(const double* __restrict__ C, double* __restrict__ A, Grid g, int tap_off, int j, int L) {
   const int64_t plane = g.cstride[0];
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= plane) return;
@@ -41,25 +41,12 @@ __global__ void axis0_pass(const double* __restrict__ C, double* __restrict__ A,
   double Bt[4];
   const int64_t crow = clamp_cell(i0 + g.off0 + ta.q, g.Pg0, ta.B, Bt) - g.off0;
   const int64_t P0 = g.P[0];
-  if (NF == k3F) {
 #pragma unroll
-    for (int f = 0; f < k3F; ++f) {
-      const double* c = C + (int64_t)f * g.cfield + crow * plane + e;
-      const double v = fma(Bt[0], __ldcg(c), fma(Bt[1], __ldcg(c + plane), fma(Bt[2], __ldcg(c + 2 * plane),
-                                                                                Bt[3] * __ldcg(c + 3 * plane))));
-      A[(((int64_t)l * k3F + f) * P0 + i0) * plane + e] = v;
-    }
-  } else {
-    const double ucf[k3F] = {uc.x, uc.y, uc.z, uc.w};
-    double u = 0.0;
-#pragma unroll
-    for (int f = 0; f < k3F; ++f) {
-      const double* c = C + (int64_t)f * g.cfield + crow * plane + e;
-      const double v = fma(Bt[0], __ldcg(c), fma(Bt[1], __ldcg(c + plane), fma(Bt[2], __ldcg(c + 2 * plane),
-                                                                                Bt[3] * __ldcg(c + 3 * plane))));
-      u = fma(ucf[f], v, u);
-    }
-    A[((int64_t)l * P0 + i0) * plane + e] = u;
+  for (int f = 0; f < k3F; ++f) {
+    const double* c = C + (int64_t)f * g.cfield + crow * plane + e;
+    const double v = fma(Bt[0], __ldcg(c), fma(Bt[1], __ldcg(c + plane), fma(Bt[2], __ldcg(c + 2 * plane),
+                                                                              Bt[3] * __ldcg(c + 3 * plane))));
+    A[(((int64_t)l * k3F + f) * P0 + i0) * plane + e] = v;
   }
 }
 
@@ -578,12 +565,12 @@ static cudaError_t launch_step3d_t(const StepArgs& s, const Grid& g, const Probl
   const double4 uc = make_double4(-1.0, pb.dp[5], pb.dp[6], pb.dp[7]);     // U = pi.z - y (NF = 1)
   for (int j = 1; j <= s.K; ++j) {
     const double* C = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
-    if (NF == 1) {
+    if constexpr (NF == 1) {
       dim3 gu((unsigned)((plane + 127) / 128), (unsigned)((g.P[0] + 7) / 8), 1);
       axis0_u<<<gu, 128, 0, st>>>(C, A, g, s.tap_off, j, s.L, uc);
     } else {
       dim3 ga((unsigned)((plane + 255) / 256), (unsigned)g.P[0], (unsigned)s.L);
-      axis0_pass<NF><<<ga, 256, 0, st>>>(C, A, g, s.tap_off, j, s.L, uc);
+      axis0_pass<<<ga, 256, 0, st>>>(C, A, g, s.tap_off, j, s.L);
     }
     dim3 gq((unsigned)((g.P[2] + k3TX - 1) / k3TX), (unsigned)((g.P[1] + k3TY - 1) / k3TY), (unsigned)g.nown0);
     quad3d<DRV, NF><<<gq, k3NT, smem, st>>>(s, g, pb, WC, A, acc, j, j == 1 ? 1 : 0);
