@@ -18,7 +18,7 @@
 // (DESIGN.md §4).  Axis-1 clamping is per row in the row pass, axis-2 clamping uses the
 // virtual-window extension of the 1-D and 2-D kernels.
 // The differential-rates driver (cfg 5) runs decomposed by default: its nonlinearity depends on
-// the single combination U = pi.z - y, so (1') `axis0_u` builds plane stacks of U alone and
+// the single combination U = pi.z - y, so (1') `axis0_u_lin` builds plane stacks of U alone and
 // quad3d<DRV_DIFF, 1> interpolates only U per tap; the affine remainder's expectations are
 // separable (`lin_axis`, `lin_axis2`, below).
 #pragma once
@@ -50,11 +50,14 @@ __global__ void axis0_pass(const double* __restrict__ C, double* __restrict__ A,
   }
 }
 
-// (1') the plane stacks of U = sum_f uc_f C_f for the decomposed driver: a thread owns one
-// plane element and 8 consecutive planes and loops over the L axis-0 nodes, so each coefficient
-// row is fetched (11/8) times per node instead of 4 times per (node, plane) as in axis0_pass
-__global__ void __launch_bounds__(128) axis0_u(const double* __restrict__ C, double* __restrict__ A, Grid g,
-                                               int tap_off, int j, int L, double4 uc) {
+// (1') decomposed driver: the plane stacks of U = sum_f uc_f C_f together with the axis-0
+// operators of the affine part.  A thread owns one plane element and 8 consecutive planes and
+// loops over the L axis-0 nodes; the level's coefficient rows stream by (11 per node for 8
+// planes, every row feeding the outputs whose 4-row stencil covers it), and one pass writes
+// the U stacks (per node) and the six node-summed arrays Lf (plain, s-weighted), z_0..2, y.
+__global__ void __launch_bounds__(128) axis0_u_lin(const double* __restrict__ C, double* __restrict__ A,
+                                                   double* __restrict__ W0, Grid g, int tap_off, int j, int L,
+                                                   double4 uc, double4 lc) {
   constexpr int RA = 8;
   const int64_t plane = g.cstride[0];
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -63,31 +66,54 @@ __global__ void __launch_bounds__(128) axis0_u(const double* __restrict__ C, dou
   const int64_t P0 = g.P[0];
   const AxisTap* t0 = axis_taps(tap_off) + (size_t)(j - 1) * 3 * L;
   const double* Ce = C + e;
-  auto row = [&](int64_t r) {           // U at storage plane r, element e
-    const double* c = Ce + r * plane;
-    return fma(uc.x, __ldg(c), fma(uc.y, __ldg(c + g.cfield), fma(uc.z, __ldg(c + 2 * g.cfield), uc.w * __ldg(c + 3 * g.cfield))));
-  };
+  double lp[RA], ls[RA], z0[RA], z1[RA], z2[RA], yy[RA];
+#pragma unroll
+  for (int r = 0; r < RA; ++r) { lp[r] = 0.0; ls[r] = 0.0; z0[r] = 0.0; z1[r] = 0.0; z2[r] = 0.0; yy[r] = 0.0; }
   for (int l = 0; l < L; ++l) {
     const AxisTap& t = t0[l];
+    const double w = t.w, ws = t.w * t.s;
     const int64_t c0 = i0 + g.off0 + t.q;                          // global cell of plane i0
-    double out[RA];
+    double u[RA];
+#pragma unroll
+    for (int r = 0; r < RA; ++r) u[r] = 0.0;
+    // row k contributes B_a(theta) to output r = k - a; for a clamped output its own 4 rows
+    auto feed = [&](int r, double b, const double* c) {
+      const double f0 = __ldg(c), f1 = __ldg(c + g.cfield), f2 = __ldg(c + 2 * g.cfield), f3 = __ldg(c + 3 * g.cfield);
+      const double U = fma(uc.x, f0, fma(uc.y, f1, fma(uc.z, f2, uc.w * f3)));
+      const double Lf = fma(lc.x, f0, fma(lc.y, f1, fma(lc.z, f2, lc.w * f3)));
+      const double bw = b * w, bs = b * ws;
+      u[r] = fma(b, U, u[r]);
+      lp[r] = fma(bw, Lf, lp[r]); ls[r] = fma(bs, Lf, ls[r]);
+      z0[r] = fma(bw, f1, z0[r]); z1[r] = fma(bw, f2, z1[r]); z2[r] = fma(bw, f3, z2[r]); yy[r] = fma(bw, f0, yy[r]);
+    };
     if (c0 >= 0 && c0 + RA - 1 <= g.Pg0 - 2) {
-      double v[RA + 3];
+      const double* c = Ce + (c0 - g.off0) * plane;
 #pragma unroll
-      for (int k = 0; k < RA + 3; ++k) v[k] = row(c0 - g.off0 + k);
+      for (int k = 0; k < RA + 3; ++k)
 #pragma unroll
-      for (int r = 0; r < RA; ++r) out[r] = fma(t.B[0], v[r], fma(t.B[1], v[r + 1], fma(t.B[2], v[r + 2], t.B[3] * v[r + 3])));
+        for (int a = 0; a < 4; ++a)
+          if (k - a >= 0 && k - a < RA) feed(k - a, t.B[a], c + k * plane);
     } else {
 #pragma unroll
       for (int r = 0; r < RA; ++r) {
         double Bt[4];
         const int64_t cell = clamp_cell(c0 + r, g.Pg0, t.B, Bt) - g.off0;
-        out[r] = fma(Bt[0], row(cell), fma(Bt[1], row(cell + 1), fma(Bt[2], row(cell + 2), Bt[3] * row(cell + 3))));
+#pragma unroll
+        for (int a = 0; a < 4; ++a) feed(r, Bt[a], Ce + (cell + a) * plane);
       }
     }
 #pragma unroll
     for (int r = 0; r < RA; ++r)
-      if (i0 + r < P0) A[((int64_t)l * P0 + i0 + r) * plane + e] = out[r];
+      if (i0 + r < P0) A[((int64_t)l * P0 + i0 + r) * plane + e] = u[r];
+  }
+  // the affine part's axis-0 arrays for the owned planes: [Lf, Lf s0, z_0, z_1, z_2, y][owned][plane]
+  const int64_t arr = g.nown0 * plane;
+#pragma unroll
+  for (int r = 0; r < RA; ++r) {
+    const int64_t i = i0 + r - g.own0;
+    if (i < 0 || i >= g.nown0) continue;
+    double* o = W0 + i * plane + e;
+    o[0] = lp[r]; o[arr] = ls[r]; o[2 * arr] = z0[r]; o[3 * arr] = z1[r]; o[4 * arr] = z2[r]; o[5 * arr] = yy[r];
   }
 }
 
@@ -513,30 +539,14 @@ __global__ void __launch_bounds__(128) lin_axis2(StepArgs s, Grid g, const doubl
   }
 }
 
-// the affine part of a level: axis 0 from the ring slot C (6 arrays: Lf, Lf s0, z_0..2, y), axis 1
-// (7 arrays), axis 2 + accumulation; W0 / W1 hold 6 / 7 arrays of (owned planes) x cstride[0]
-static cudaError_t launch_lin3(const StepArgs& s, const Grid& g, const Problem& pb, const double* C, double* W0,
-                               double* W1, double* acc, int j, cudaStream_t st, int64_t* launches) {
+// the affine part of a level after its axis-0 arrays (axis0_u_lin: Lf, Lf s0, z_0..2, y in W0):
+// axis 1 (7 arrays into W1), axis 2 + accumulation; arrays of (owned planes) x cstride[0]
+static cudaError_t launch_lin3(const StepArgs& s, const Grid& g, const Problem& pb, double* W0, double* W1,
+                               double* acc, int j, cudaStream_t st, int64_t* launches) {
   const int64_t plane = g.cstride[0], cs1 = g.cstride[1], P1 = g.P[1], P2 = g.P[2];
   const int64_t arr = g.nown0 * plane;                 // one array of W0 / W1
-  const double r = pb.dp[0], th0 = pb.dp[2], th1 = pb.dp[3], th2 = pb.dp[4];
-  // axis 0: rows = coefficient planes of the slab, columns = plane elements
-  auto ax0 = [&](int nf0, int nf, const double* cf, double* yp, double* ys) {
-    LinAxis p{};
-    p.X = C + (int64_t)nf0 * g.cfield; p.xb = 0; p.xr = plane; p.xf = g.cfield; p.nf = nf;
-    for (int f = 0; f < nf; ++f) p.coef[f] = cf[f];
-    p.Yp = yp; p.Ys = ys; p.yb = 0; p.yr = plane;
-    p.ncols = plane; p.nout = g.nown0; p.ibase = g.own0; p.off = g.off0; p.Pg = g.Pg0;
-    p.tap_off = s.tap_off; p.j = j; p.a = 0; p.L = s.L;
-    const dim3 gr((unsigned)((plane + 127) / 128), (unsigned)((g.nown0 + 7) / 8), 1);
-    if (nf == 4) lin_axis<4><<<gr, 128, 0, st>>>(p);
-    else lin_axis<1><<<gr, 128, 0, st>>>(p);
-  };
-  const double cLf[4] = {-r, -th0, -th1, -th2}, one[1] = {1.0};
-  ax0(0, 4, cLf, W0, W0 + arr);                        // Lf (plain, s0)
-  for (int k = 0; k < 3; ++k) ax0(1 + k, 1, one, W0 + (2 + k) * arr, nullptr);
   const bool yj = (j == s.Ky);
-  if (yj) ax0(0, 1, one, W0 + 5 * arr, nullptr);
+  (void)pb;
   // axis 1: batch = owned plane, rows = axis-1 coefficient rows, columns = cs1
   auto ax1 = [&](const double* x, double* yp, double* ys) {
     LinAxis p{};
@@ -553,7 +563,7 @@ static cudaError_t launch_lin3(const StepArgs& s, const Grid& g, const Problem& 
   if (yj) ax1(W0 + 5 * arr, W1 + 6 * arr, nullptr);
   const dim3 g2((unsigned)((P2 + 3 * 128 - 1) / (3 * 128)), (unsigned)P1, (unsigned)g.nown0);
   lin_axis2<<<g2, 128, 0, st>>>(s, g, W1, arr, acc, j);
-  if (launches) *launches += 4 + (yj ? 2 : 0) + 4 + 1;
+  if (launches) *launches += 4 + (yj ? 1 : 0) + 1;
   return cudaGetLastError();
 }
 
@@ -563,11 +573,13 @@ static cudaError_t launch_step3d_t(const StepArgs& s, const Grid& g, const Probl
   const size_t smem = fused3d_smem(WC, NF);
   const int64_t plane = g.cstride[0];
   const double4 uc = make_double4(-1.0, pb.dp[5], pb.dp[6], pb.dp[7]);     // U = pi.z - y (NF = 1)
+  const double4 lc = make_double4(-pb.dp[0], -pb.dp[2], -pb.dp[3], -pb.dp[4]);   // Lf = -(r y + th.z)
   for (int j = 1; j <= s.K; ++j) {
     const double* C = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
     if constexpr (NF == 1) {
       dim3 gu((unsigned)((plane + 127) / 128), (unsigned)((g.P[0] + 7) / 8), 1);
-      axis0_u<<<gu, 128, 0, st>>>(C, A, g, s.tap_off, j, s.L, uc);
+      double* W0 = A + (int64_t)s.L * g.P[0] * plane + (int64_t)(j - 1) * 6 * g.nown0 * plane;
+      axis0_u_lin<<<gu, 128, 0, st>>>(C, A, W0, g, s.tap_off, j, s.L, uc, lc);
     } else {
       dim3 ga((unsigned)((plane + 255) / 256), (unsigned)g.P[0], (unsigned)s.L);
       axis0_pass<<<ga, 256, 0, st>>>(C, A, g, s.tap_off, j, s.L);
@@ -578,12 +590,11 @@ static cudaError_t launch_step3d_t(const StepArgs& s, const Grid& g, const Probl
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  if (NF == 1) {       // the affine part of the decomposed driver (after the plane stacks' use)
+  if (NF == 1) {       // the affine part: axes 1 and 2 of every level's axis-0 arrays
     double* W0 = A + (int64_t)s.L * g.P[0] * plane;
-    double* W1 = W0 + 6 * g.nown0 * plane;
+    double* W1 = W0 + (int64_t)s.K * 6 * g.nown0 * plane;
     for (int j = 1; j <= s.K; ++j) {
-      const double* C = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
-      cudaError_t e = launch_lin3(s, g, pb, C, W0, W1, acc, j, st, launches);
+      cudaError_t e = launch_lin3(s, g, pb, W0 + (int64_t)(j - 1) * 6 * g.nown0 * plane, W1, acc, j, st, launches);
       if (e != cudaSuccess) return e;
     }
   }

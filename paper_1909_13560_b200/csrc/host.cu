@@ -507,8 +507,8 @@ Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d, bool aff2) {
   const bool f3 = g.d == 3 && fused3d, a2 = g.d == 2 && aff2;
   L.a3 = off;
   // d = 3: L x F plane stacks, or (decomposed differential-rates driver) L single-field stacks
-  // + the 13 arrays of its separable affine part
-  off += f3 ? al(sizeof(double) * (size_t)std::max(nodes * F, nodes + 13) * g.P[0] * g.cstride[0])
+  // + the 6 K + 7 arrays of its separable affine part
+  off += f3 ? al(sizeof(double) * (size_t)std::max(nodes * F, nodes + 6 * K + 7) * g.P[0] * g.cstride[0])
             : (a2 ? al(sizeof(double) * 2 * (size_t)F * K * g.nown0 * g.cstride[0]) : 0);
   L.acc3 = off;
   off += f3 ? al(sizeof(double) * 5 * (size_t)g.nown0 * g.P[1] * g.P[2])
