@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(128) lin_axis(LinAxis p) {
 // the contiguous axis (2) of the 7 axis-1 outputs [owned planes (stride cstride[0])][P1][cs1] and the level's
 // scheme-weighted sums added to acc: Az_k += czj E[z_k] + gzj E[Lf dW_k], Af += gyj E[Lf],
 // Ay += [j == Ky] E[y]  (arrays: 0 Lf_pp, 1 Lf_p s1, 2 Lf_s0 p, 3..5 z_k, 6 y)
-__global__ void __launch_bounds__(128) lin_axis2(StepArgs s, Grid g, const double* __restrict__ X, int64_t astride,
+__global__ void __launch_bounds__(64) lin_axis2(StepArgs s, Grid g, const double* __restrict__ X, int64_t astride,
                                                  double* __restrict__ acc, int j) {
   constexpr int R = 3;
   const int64_t P1 = g.P[1], P2 = g.P[2], cs1 = g.cstride[1];
@@ -561,8 +561,9 @@ static cudaError_t launch_lin3(const StepArgs& s, const Grid& g, const Problem& 
   ax1(W0 + arr, W1 + 2 * arr, nullptr);                // Lf_s0 p
   for (int k = 0; k < 3; ++k) ax1(W0 + (2 + k) * arr, W1 + (3 + k) * arr, nullptr);
   if (yj) ax1(W0 + 5 * arr, W1 + 6 * arr, nullptr);
-  const dim3 g2((unsigned)((P2 + 3 * 128 - 1) / (3 * 128)), (unsigned)P1, (unsigned)g.nown0);
-  lin_axis2<<<g2, 128, 0, st>>>(s, g, W1, arr, acc, j);
+  // 64 threads x 3 points: 512 columns split 192 + 192 + 128 (128-thread CTAs: 384 + 128)
+  const dim3 g2((unsigned)((P2 + 3 * 64 - 1) / (3 * 64)), (unsigned)P1, (unsigned)g.nown0);
+  lin_axis2<<<g2, 64, 0, st>>>(s, g, W1, arr, acc, j);
   if (launches) *launches += 4 + (yj ? 1 : 0) + 1;
   return cudaGetLastError();
 }
