@@ -20,7 +20,7 @@
 // The differential-rates driver (cfg 5) runs decomposed by default: its nonlinearity depends on
 // the single combination U = pi.z - y, so (1') `axis0_u_lin` builds plane stacks of U alone and
 // quad3d<DRV_DIFF, 1> interpolates only U per tap; the affine remainder's expectations are
-// separable (`lin_axis`, `lin_axis2`, below).
+// separable (`lin_axis`, `lin_axis2s`, below).
 #pragma once
 
 constexpr int k3TY = 4;            // tile rows (axis 1)
@@ -418,7 +418,7 @@ int fused3d_window(const AxisTap* host_taps, int K, int L) {
 // those of z_k and y -- are separable tensor operators (as in aff2.cuh): per level
 //   E[Lf], E[Lf dW_k] (k = 0..2), E[z_k], E[y]
 // by one strided pass per axis (lin_axis: axes 0 and 1, 8 rows per thread) and one contiguous
-// pass that also adds the scheme-weighted sums to acc (lin_axis2).  quad3d<DRV_DIFF, 1> adds
+// pass that also adds the scheme-weighted sums to acc (lin_axis2s).  quad3d<DRV_DIFF, 1> adds
 // the nonlinear part.  Exact algebra (interpolation is linear in the data).
 struct LinAxis {
   const double* X; int64_t xb, xr, xf; int nf; double coef[4];   // input rows: sum_f coef_f X_f
@@ -476,25 +476,47 @@ __global__ void __launch_bounds__(128) lin_axis(LinAxis p) {
   }
 }
 
-// the contiguous axis (2) of the 7 axis-1 outputs [owned planes (stride cstride[0])][P1][cs1] and the level's
-// scheme-weighted sums added to acc: Az_k += czj E[z_k] + gzj E[Lf dW_k], Af += gyj E[Lf],
-// Ay += [j == Ky] E[y]  (arrays: 0 Lf_pp, 1 Lf_p s1, 2 Lf_s0 p, 3..5 z_k, 6 y)
-__global__ void __launch_bounds__(64) lin_axis2(StepArgs s, Grid g, const double* __restrict__ X, int64_t astride,
-                                                 double* __restrict__ acc, int j) {
-  constexpr int R = 3;
+// the contiguous axis (2) of the 7 axis-1 outputs [owned planes (stride cstride[0])][P1][cs1] and
+// the level's scheme-weighted sums added to acc: Az_k += czj E[z_k] + gzj E[Lf dW_k],
+// Af += gyj E[Lf], Ay += [j == Ky] E[y]  (arrays: 0 Lf_pp, 1 Lf_p s1, 2 Lf_s0 p, 3..5 z_k, 6 y).
+// One row (i0, i1) x 192 columns per 64-thread CTA; the tile's column window of the 7 rows
+// arrives in shared memory by bulk copies.
+constexpr int kL2Thr = 64, kL2R = 3, kL2TX = kL2Thr * kL2R;
+__global__ void __launch_bounds__(kL2Thr) lin_axis2s(StepArgs s, Grid g, const double* __restrict__ X, int64_t astride,
+                                                    double* __restrict__ acc, int j, int WC) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* const buf = reinterpret_cast<double*>(smem_raw);          // [7][WC]
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(buf + 7 * (size_t)WC);
   const int64_t P1 = g.P[1], P2 = g.P[2], cs1 = g.cstride[1];
-  const int64_t i2 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * R;
-  if (i2 >= P2) return;
-  const int64_t i1 = blockIdx.y, i0 = blockIdx.z;               // owned plane (relative)
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * kL2TX;
+  const int64_t i2 = x0 + tid * kL2R;
+  const int64_t i1 = blockIdx.y, i0 = blockIdx.z;
   const int L = s.L;
   const AxisTap* tp = axis_taps(s.tap_off) + ((size_t)(j - 1) * 3 + 2) * L;
-  const double* Xr = X + i0 * g.cstride[0] + i1 * cs1;          // arrays: [owned plane][P1 rows][cs1]
-  double E[8][R];                          // Lf, Lf dW2, Lf dW1, Lf dW0, z0, z1, z2, y
+  const bool yj = (j == s.Ky);
+  const int wa = x0 + tp[0].q;
+  const int wv = wa - (wa & 1);
+  const int we = x0 + kL2TX - 1 + tp[L - 1].q + 3;
+  const int s0 = max(wv, 0), s1 = min(we, (int)P2 + 2);
+  const int n = ((s1 - s0 + 1) + 1) & ~1;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    const int na = yj ? 7 : 6;
+    const uint32_t bytes = (uint32_t)(n * sizeof(double));
+    mbar_expect_tx(bar, bytes * na);
+    const double* src = X + i0 * g.cstride[0] + i1 * cs1 + s0;
+    for (int k = 0; k < na; ++k) bulk_g2s(buf + (size_t)k * WC + (s0 - wv), src + k * astride, bytes, bar);
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  if (i2 >= P2) return;
+  double E[8][kL2R];                      // Lf, Lf dW2, Lf dW1, Lf dW0, z0, z1, z2, y
 #pragma unroll
   for (int k = 0; k < 8; ++k)
 #pragma unroll
-    for (int q = 0; q < R; ++q) E[k][q] = 0.0;
-  const bool yj = (j == s.Ky);
+    for (int q = 0; q < kL2R; ++q) E[k][q] = 0.0;
   for (int m = 0; m < L; ++m) {
     const AxisTap& t = tp[m];
     const double w = t.w, ws = t.w * t.s;
@@ -502,24 +524,24 @@ __global__ void __launch_bounds__(64) lin_axis2(StepArgs s, Grid g, const double
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
       if (k == 6 && !yj) continue;
-      const double* xr = Xr + k * astride;
-      double u[R];
-      if (c0 >= 0 && c0 + R - 1 <= P2 - 2) {
-        double v[R + 3];
+      const double* xr = buf + (size_t)k * WC - wv;                 // xr[col] = X_k[i0][i1][col]
+      double u[kL2R];
+      if (c0 >= 0 && c0 + kL2R - 1 <= P2 - 2) {
+        double v[kL2R + 3];
 #pragma unroll
-        for (int q = 0; q < R + 3; ++q) v[q] = __ldg(xr + c0 + q);
+        for (int q = 0; q < kL2R + 3; ++q) v[q] = xr[c0 + q];
 #pragma unroll
-        for (int q = 0; q < R; ++q) u[q] = fma(t.B[0], v[q], fma(t.B[1], v[q + 1], fma(t.B[2], v[q + 2], t.B[3] * v[q + 3])));
+        for (int q = 0; q < kL2R; ++q) u[q] = fma(t.B[0], v[q], fma(t.B[1], v[q + 1], fma(t.B[2], v[q + 2], t.B[3] * v[q + 3])));
       } else {
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
+        for (int q = 0; q < kL2R; ++q) {
           double Bt[4];
           const int64_t cell = clamp_cell(c0 + q, P2, t.B, Bt);
-          u[q] = fma(Bt[0], __ldg(xr + cell), fma(Bt[1], __ldg(xr + cell + 1), fma(Bt[2], __ldg(xr + cell + 2), Bt[3] * __ldg(xr + cell + 3))));
+          u[q] = fma(Bt[0], xr[cell], fma(Bt[1], xr[cell + 1], fma(Bt[2], xr[cell + 2], Bt[3] * xr[cell + 3])));
         }
       }
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
+      for (int q = 0; q < kL2R; ++q) {
         if (k == 0) { E[0][q] = fma(w, u[q], E[0][q]); E[1][q] = fma(ws, u[q], E[1][q]); }
         else E[k + 1][q] = fma(w, u[q], E[k + 1][q]);
       }
@@ -528,21 +550,21 @@ __global__ void __launch_bounds__(64) lin_axis2(StepArgs s, Grid g, const double
   const double czj = s.czj[j - 1], gzj = s.gzj[j - 1], gyj = s.gyj[j - 1];
   const int64_t nown = g.nown0 * P1 * P2;
 #pragma unroll
-  for (int q = 0; q < R; ++q) {
+  for (int q = 0; q < kL2R; ++q) {
     if (i2 + q >= P2) break;
     const int64_t o = (i0 * P1 + i1) * P2 + i2 + q;
-    acc[o] += czj * E[4][q] + gzj * E[3][q];                   // Az_0: E[z_0], E[Lf dW_0]
-    acc[nown + o] += czj * E[5][q] + gzj * E[2][q];            // Az_1
-    acc[2 * nown + o] += czj * E[6][q] + gzj * E[1][q];        // Az_2
-    acc[3 * nown + o] += gyj * E[0][q];                        // Af
-    if (yj) acc[4 * nown + o] += E[7][q];                      // Ay
+    acc[o] += czj * E[4][q] + gzj * E[3][q];
+    acc[nown + o] += czj * E[5][q] + gzj * E[2][q];
+    acc[2 * nown + o] += czj * E[6][q] + gzj * E[1][q];
+    acc[3 * nown + o] += gyj * E[0][q];
+    if (yj) acc[4 * nown + o] += E[7][q];
   }
 }
 
 // the affine part of a level after its axis-0 arrays (axis0_u_lin: Lf, Lf s0, z_0..2, y in W0):
 // axis 1 (7 arrays into W1), axis 2 + accumulation; arrays of (owned planes) x cstride[0]
 static cudaError_t launch_lin3(const StepArgs& s, const Grid& g, const Problem& pb, double* W0, double* W1,
-                               double* acc, int j, cudaStream_t st, int64_t* launches) {
+                               double* acc, int j, int WC, cudaStream_t st, int64_t* launches) {
   const int64_t plane = g.cstride[0], cs1 = g.cstride[1], P1 = g.P[1], P2 = g.P[2];
   const int64_t arr = g.nown0 * plane;                 // one array of W0 / W1
   const bool yj = (j == s.Ky);
@@ -561,9 +583,11 @@ static cudaError_t launch_lin3(const StepArgs& s, const Grid& g, const Problem& 
   ax1(W0 + arr, W1 + 2 * arr, nullptr);                // Lf_s0 p
   for (int k = 0; k < 3; ++k) ax1(W0 + (2 + k) * arr, W1 + (3 + k) * arr, nullptr);
   if (yj) ax1(W0 + 5 * arr, W1 + 6 * arr, nullptr);
-  // 64 threads x 3 points: 512 columns split 192 + 192 + 128 (128-thread CTAs: 384 + 128)
-  const dim3 g2((unsigned)((P2 + 3 * 64 - 1) / (3 * 64)), (unsigned)P1, (unsigned)g.nown0);
-  lin_axis2<<<g2, 64, 0, st>>>(s, g, W1, arr, acc, j);
+  // 64 threads x 3 points: 512 columns split 192 + 192 + 128; the tile's window of the 7 rows in
+  // shared memory (bulk copies)
+  static_assert(kL2TX == k3TX, "lin_axis2s shares quad3d's column window width");
+  const dim3 g2((unsigned)((P2 + kL2TX - 1) / kL2TX), (unsigned)P1, (unsigned)g.nown0);
+  lin_axis2s<<<g2, kL2Thr, (size_t)7 * WC * sizeof(double) + 16, st>>>(s, g, W1, arr, acc, j, WC);
   if (launches) *launches += 4 + (yj ? 1 : 0) + 1;
   return cudaGetLastError();
 }
@@ -595,7 +619,7 @@ static cudaError_t launch_step3d_t(const StepArgs& s, const Grid& g, const Probl
     double* W0 = A + (int64_t)s.L * g.P[0] * plane;
     double* W1 = W0 + (int64_t)s.K * 6 * g.nown0 * plane;
     for (int j = 1; j <= s.K; ++j) {
-      cudaError_t e = launch_lin3(s, g, pb, W0 + (int64_t)(j - 1) * 6 * g.nown0 * plane, W1, acc, j, st, launches);
+      cudaError_t e = launch_lin3(s, g, pb, W0 + (int64_t)(j - 1) * 6 * g.nown0 * plane, W1, acc, j, WC, st, launches);
       if (e != cudaSuccess) return e;
     }
   }
