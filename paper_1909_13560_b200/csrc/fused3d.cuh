@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(128) axis0_u_lin(const double* __restrict__ C,
 // (2) one level of taps for a 4 x 192 tile of plane i0 (own rows only).  NF = 4: every field
 // interpolated per tap and the driver applied; NF = 1 (decomposed differential-rates driver,
 // f = -(r y + th.z) + (R - r) max(U, 0)): only U per tap and only the nonlinear part
-// g = (R - r) max(U, 0) accumulated (the affine part is separable: lin3.cuh)
+// g = (R - r) max(U, 0) accumulated (the affine part is separable: lin_axis / lin_axis2s below)
 template <int DRV, int NF>
 __global__ void __launch_bounds__(k3NT, 2) quad3d(StepArgs s, Grid g, Problem pb, int WC, const double* __restrict__ A,
                                                   double* __restrict__ acc, int j, int first) {
