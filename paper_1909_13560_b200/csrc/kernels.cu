@@ -312,11 +312,14 @@ void pcr_constants(double* alpha, double* inv_b) {
 static cudaError_t run_pass(PassArgs pa, bool strided, cudaStream_t st, int64_t* launches) {
   pcr_constants(pa.alpha, &pa.inv_b);
   const int64_t n = pa.P + 2;                              // outputs per line (c_{-1} .. c_P)
-  if (strided) {
+  // short contiguous lines (d = 3: 514 outputs) also go 4 lines per CTA, one tile per line:
+  // one 256-thread CTA per short line spends its time in barriers and launch overhead
+  const bool short_lines = !strided && n <= 1024 && pa.nb1 >= 4;
+  if (strided || short_lines) {
     // 4 adjacent lines per CTA (32-byte coalesced row segments: 6 CTAs per SM instead of 3
     // with 8 lines; cfg 4 step 4.76 -> 4.66 ms), tiles of ~256 outputs (halo 27 %)
     constexpr int LN = 4;
-    const int64_t nt = (n + 255) / 256;
+    const int64_t nt = short_lines ? 1 : (n + 255) / 256;
     pa.TS = (int)((n + nt - 1) / nt);
     dim3 grid((unsigned)nt, (unsigned)((pa.nb1 + LN - 1) / LN), (unsigned)pa.nb0);
     spline_pass<LN><<<grid, 256, spline_smem(pa.TS, LN), st>>>(pa);
