@@ -37,7 +37,7 @@ typedef enum {
   BSDE_ERR_SINGULAR = 3,         /* reserved (the spline matrix is never singular)          */
   BSDE_ERR_NUMERICAL_DOMAIN = 4, /* a non-finite y or z was produced (details: last_error)  */
   BSDE_ERR_CUDA = 5,             /* a CUDA runtime error (message in last_error)            */
-  BSDE_ERR_COMM = 6,             /* reserved for the multi-GPU halo exchange                */
+  BSDE_ERR_COMM = 6,             /* an NCCL failure of the multi-GPU halo exchange          */
   BSDE_ERR_STATE = 7             /* e.g. bsde_step at n == 0                                */
 } bsde_status;
 
@@ -66,9 +66,33 @@ typedef enum {
   BSDE_TERM_EXCHANGE_W = 6,   /* S_k = p[k] exp((p[2+k] - s_k^2/2) T + (A w)_k), s = (p4, p5),
                                  rho = p6, A = [[s1, 0], [rho s2, s2 sqrt(1-rho^2)]],
                                  g = (S_1 - S_2)^+                               (Eq. 36)   */
-  BSDE_TERM_GEO_BASKET_W = 7  /* S_k = p[k] exp((p4 - s_k^2/2) T + s_k w_k), s_k = p[5+k],
+  BSDE_TERM_GEO_BASKET_W = 7, /* S_k = p[k] exp((p4 - s_k^2/2) T + s_k w_k), s_k = p[5+k],
                                  G = (prod_k S_k)^{1/d}, g = (G - p3)^+     (BASELINE cfg 5) */
+  BSDE_TERM_CALL_X = 8        /* forward-SDE problems (sde_id != 0): g(x) = (x_0 - p1)^+ in the
+                                 state variable x = X_T itself (e.g. a stock price)          */
 } bsde_terminal_id;
+
+/* Forward process X of the FBSDE (Eq. 1): dX = a(X) dt + b(X) dW with a
+ * diagonal b, approximated by one Euler step per level ("e.g. by using the Euler-Scheme",
+ * PAPER.md:50): from grid point x_i the level-j sample is
+ *     X = x_i + a(x_i) j dt + b(x_i) sqrt(2 j dt) a_Lambda        (per axis k),
+ * so the stencil is no longer translation-invariant (per-point cell location).
+ * z is the BSDE's z = b^T grad u; the terminal layer is z_T = b(x) grad g(x).
+ * Parameters p = sde_params; p[9..11] = X_0 = x_0 is the evaluation point of (y_0, z_0)
+ * (the spline of layer 0 there).  sde_id 0 is Eq. 2 (X = W) and uses the stencil kernels. */
+typedef enum {
+  BSDE_SDE_BROWNIAN = 0,      /* a = 0, b = 1 (X = W, Eq. 2)                                 */
+  BSDE_SDE_GBM = 1,           /* a_k = p[k] x_k, b_k = p[3+k] x_k (geometric Brownian motion) */
+  BSDE_SDE_OU = 2             /* a_k = p[k] (p[3+k] - x_k), b_k = p[6+k] (Ornstein-Uhlenbeck)  */
+} bsde_sde_id;
+
+/* Spatial interpolation of the levels. */
+typedef enum {
+  BSDE_INTERP_SPLINE = 0,     /* tensor-product not-a-knot cubic spline (north_star; R14)     */
+  BSDE_INTERP_FD_BICUBIC = 1  /* d = 2 only: the paper's bicubic interpolation with first and
+                                 mixed derivatives by 4th-order finite differences (central,
+                                 one-sided within 2 nodes of the box edge)      */
+} bsde_interp_id;
 
 typedef struct {
   uint32_t struct_size;      /* caller sets sizeof(bsde_config) (ABI versioning)          */
@@ -106,16 +130,28 @@ typedef struct {
                                 2 (d = 2): the per-tap fused 2-D kernel for every driver;
                                 10 + v (d = 1): fused kernel variant v; any other value
                                 selects the generic kernels                               */
+  int32_t  interp;           /* interpolation, a bsde_interp_id value; 0 = tensor spline   */
+  int32_t  sde_id;           /* forward SDE, a bsde_sde_id value; 0 = X = W                */
+  double   sde_params[12];
+  int32_t  timing;           /* 1: per-stage CUDA-event timers (t_spline_s, t_quad_s, t_comm_s
+                                of bsde_result); 0: only setup / bootstrap / sweep times   */
 } bsde_config;
 
 typedef struct {
   double  y0, z0[3];         /* solution at t0 and x = 0 (grid value if x = 0 is a grid point,
                                 else the spline of layer 0 at 0; R4)             */
-  double  t_setup_s;         /* bsde_setup wall time (host clock)                          */
-  double  t_sweep_s;         /* backward sweep n = N-K..0 (CUDA events on the stream)      */
-  double  t_total_s;         /* setup + sweep + result read-back                           */
-  int64_t updates;           /* npts_total * (number of sweep steps performed)              */
+  double  t_setup_s;         /* bsde_setup wall time (host clock; includes the bootstrap)   */
+  double  t_sweep_s;         /* backward sweep of this call (CUDA events on the stream)    */
+  double  t_total_s;         /* t_setup_s + wall time of this call incl. result read-back   */
+  int64_t updates;           /* points this rank owns * sweep steps performed by this call  */
   int32_t picard_max_used;
+  double  t_bootstrap_s;     /* device time of the K-1 initial layers (closed form or the
+                                one-step bootstrap), CUDA events inside bsde_setup          */
+  double  t_spline_s;        /* cfg.timing = 1: device time of the spline builds of this call
+                                (0 where the spline is fused into the quadrature kernel:
+                                the d = 1 persistent kernel)                                */
+  double  t_quad_s;          /* cfg.timing = 1: quadrature + z + Picard kernels             */
+  double  t_comm_s;          /* cfg.timing = 1: halo exchange (NCCL or peer copies)         */
 } bsde_result;
 
 typedef struct bsde_ctx bsde_ctx;
@@ -132,11 +168,15 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
 
 /* One backward step n+1 -> n (Eq. 20): fused quadrature/z/Picard kernel, then the
  * spline build of the new level into the ring slot of level n+K.  Asynchronous.
- * Errors: STATE at n == 0; CUDA on a launch failure.                                  */
+ * Errors: STATE at n == 0 and for a member of an in-process slab group (use
+ * bsde_group_step, which also refreshes the halos); CUDA on a launch failure.          */
 bsde_status bsde_step(bsde_ctx* ctx);
 
 /* Remaining steps to n = 0, then the evaluation point; synchronises the stream and
- * checks the device non-finite flag (NUMERICAL_DOMAIN).  res may be NULL.             */
+ * checks the device non-finite flag (NUMERICAL_DOMAIN; last_error names the level n, the
+ * point index i, t_n, x_i and the y, z found there).  res may be NULL.  Multi-process
+ * NCCL ranks (nranks > 1 with an nccl_unique_id) always run the evaluation-point
+ * all-reduce, so every rank must call bsde_solve; res may differ per rank.             */
 bsde_status bsde_solve(bsde_ctx* ctx, bsde_result* res);
 
 /* Batched solve of n (1..8) independent d = 1 problems on one device: the remaining steps

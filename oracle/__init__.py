@@ -7,5 +7,5 @@ with it.  See ``oracle/bsde_oracle.h`` for the passages each routine follows.
 """
 from .oracle import (  # noqa: F401
     OracleError, build_oracle, gauss_hermite, gamma_row, balance_npts,
-    spline_moments, spline_eval, thomas, Oracle, terminal, exact, driver,
+    spline_moments, spline_eval, thomas, Oracle, terminal, exact, driver, fd_weights, fd_deriv,
 )

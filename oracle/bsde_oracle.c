@@ -331,6 +331,10 @@ int orc_terminal(const orc_config* cfg, const double* w, double* y, double* z) {
       } else *y = 0.0;
       return ORC_OK;
     }
+    case ORC_TERM_CALL_X: {          /* payoff in the state variable of Eq. 1: g(x) = (x_0 - K)^+ */
+      if (w[0] > p[1]) { *y = w[0] - p[1]; z[0] = 1.0; } else *y = 0.0;
+      return ORC_OK;                 /* z = grad g here; fill_layer applies b (z = b^T grad u) */
+    }
   }
   return fail(ORC_ERR_ARG, "unknown terminal id %d", cfg->terminal_id);
 }
@@ -353,6 +357,8 @@ int orc_exact(const orc_config* cfg, double t, const double* w, double* y, doubl
   double T = cfg->T, tau = T - t;
   int tid = cfg->terminal_id, did = cfg->driver_id;
   for (int k = 0; k < d; ++k) z[k] = 0.0;
+  if (cfg->sde_id != ORC_SDE_BROWNIAN && !(tid == ORC_TERM_CONST && did == ORC_DRV_ZERO))
+    return fail(ORC_ERR_UNSUPPORTED, "no closed form for a forward-SDE problem: use bootstrap = 1");
   if (tau == 0.0) return orc_terminal(cfg, w, y, z);
   if (tid == ORC_TERM_CONST && (did == ORC_DRV_ZERO || (did == ORC_DRV_AFFINE && q[1] == 0 && q[2] == 0 && q[3] == 0))) {
     double a = did == ORC_DRV_ZERO ? 0.0 : q[0], c0 = did == ORC_DRV_ZERO ? 0.0 : q[4];
@@ -524,10 +530,69 @@ static int kinked(int tid) {
 }
 
 /* ------------------------------------------------------------------------- */
+/* Forward SDE of Eq. 1, diagonal: drift a_k(x) and diffusion b_k(x). */
+static void sde_coef(const orc_config* cfg, int k, double x, double* a, double* b) {
+  const double* q = cfg->sp;
+  switch (cfg->sde_id) {
+    case ORC_SDE_GBM: *a = q[k] * x; *b = q[3 + k] * x; return;
+    case ORC_SDE_OU: *a = q[k] * (q[3 + k] - x); *b = q[6 + k]; return;
+  }
+  *a = 0.0; *b = 1.0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* 4th-order finite differences ("finite difference schemes of the fourth order
+ * of accuracy (central, forward and backward)").  The weights of the derivative at offset 0 of
+ * the degree-4 interpolating polynomial through the 5 nodes `off` are the solution of
+ * sum_k w_k off_k^m = [m == 1], m = 0..4 (the definition, solved by Gaussian elimination).   */
+int orc_fd_weights(const int* off, double* w) {
+  double A[5][6];
+  for (int m = 0; m < 5; ++m) {
+    for (int k = 0; k < 5; ++k) {
+      double v = 1.0;
+      for (int e = 0; e < m; ++e) v *= (double)off[k];
+      A[m][k] = v;
+    }
+    A[m][5] = m == 1 ? 1.0 : 0.0;
+  }
+  for (int c = 0; c < 5; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < 5; ++r) if (fabs(A[r][c]) > fabs(A[piv][c])) piv = r;
+    if (A[piv][c] == 0.0) return fail(ORC_ERR_SINGULAR, "fd weights: repeated offsets");
+    for (int k = 0; k < 6; ++k) { double t = A[c][k]; A[c][k] = A[piv][k]; A[piv][k] = t; }
+    for (int r = 0; r < 5; ++r) {
+      if (r == c) continue;
+      double f = A[r][c] / A[c][c];
+      for (int k = c; k < 6; ++k) A[r][k] -= f * A[c][k];
+    }
+  }
+  for (int k = 0; k < 5; ++k) w[k] = A[k][5] / A[k][k];
+  return ORC_OK;
+}
+
+/* first derivative of a line: central 5-point stencil (-2..2) in the interior, one-sided
+ * 5-point stencils at the two nodes nearest each end (0..4, -1..3 and mirrored) */
+static int fd_line(const double* f, int64_t fs, int64_t P, double h, double* df, int64_t ds) {
+  static const int offs[5][5] = {{0, 1, 2, 3, 4}, {-1, 0, 1, 2, 3}, {-2, -1, 0, 1, 2}, {-3, -2, -1, 0, 1}, {-4, -3, -2, -1, 0}};
+  double w[5][5];
+  if (P < 5) return fail(ORC_ERR_ARG, "4th-order differences need >= 5 nodes (P=%lld)", (long long)P);
+  for (int s = 0; s < 5; ++s) { int e = orc_fd_weights(offs[s], w[s]); if (e) return e; }
+  for (int64_t i = 0; i < P; ++i) {
+    int s = i == 0 ? 0 : (i == 1 ? 1 : (i == P - 2 ? 3 : (i == P - 1 ? 4 : 2)));
+    double acc = 0.0;
+    for (int k = 0; k < 5; ++k) acc += w[s][k] * f[(i + offs[s][k]) * fs];
+    df[i * ds] = acc / h;
+  }
+  return ORC_OK;
+}
+
+int orc_fd_deriv(const double* f, int64_t P, double h, double* df) { return fd_line(f, 1, P, h, df, 1); }
+
+/* ------------------------------------------------------------------------- */
 /* Solver state.  A layer's spline is stored as 2^d arrays per field:
  * D[mask] = moments along every axis in `mask` applied to the values (tensor
  * product, successive 1-D Thomas passes), D[0] = values.                      */
-typedef struct { double* D[8]; } field_spline;
+typedef struct { double* D[8]; double* bic; } field_spline;   /* bic: 16 coefficients per cell (interp 1) */
 typedef struct { field_spline f[4]; } layer_spline;
 
 struct orc_ctx {
@@ -537,6 +602,7 @@ struct orc_ctx {
   double dx[3], dt;
   double gh_a[64], gh_w[64];
   double gy[7], gz[7];
+  double binv[16][16];    /* bicubic: Hermite data (16 corner values) -> power coefficients */
   layer_spline* ring;     /* K slots; level m lives in slot m % K */
   double* values;         /* F * npts, newest level */
   int32_t* picard;        /* npts */
@@ -552,16 +618,100 @@ static void coords(const orc_ctx* c, int64_t idx, double* x) {
 
 static int alloc_spline(orc_ctx* c, layer_spline* s) {
   memset(s, 0, sizeof *s);
-  for (int f = 0; f < c->F; ++f)
-    for (int m = 0; m < (1 << c->d); ++m) {
+  const int bic = c->cfg.interp == ORC_INTERP_BICUBIC;
+  for (int f = 0; f < c->F; ++f) {
+    for (int m = 0; m < (bic ? 1 : (1 << c->d)); ++m) {
       s->f[f].D[m] = (double*)malloc(sizeof(double) * (size_t)c->npts);
       if (!s->f[f].D[m]) return fail(ORC_ERR_RESOURCE, "oom: %lld points", (long long)c->npts);
     }
+    if (bic) {
+      s->f[f].bic = (double*)malloc(sizeof(double) * 16 * (size_t)((c->P[0] - 1) * (c->P[1] - 1)));
+      if (!s->f[f].bic) return fail(ORC_ERR_RESOURCE, "oom: bicubic coefficients");
+    }
+  }
   return ORC_OK;
 }
 static void free_spline(orc_ctx* c, layer_spline* s) {
-  for (int f = 0; f < 4; ++f) for (int m = 0; m < 8; ++m) free(s->f[f].D[m]);
+  for (int f = 0; f < 4; ++f) {
+    for (int m = 0; m < 8; ++m) free(s->f[f].D[m]);
+    free(s->f[f].bic);
+  }
   (void)c;
+}
+
+/* The paper's 2-D interpolation: first and mixed derivatives by 4th-order finite
+ * differences (f_xy = the axis-1 difference of f_x), then per cell the 16 coefficients
+ * a_mn of p(t0, t1) = sum a_mn t0^m t1^n on the unit cell by the 16x16 matrix-vector product
+ * binv * (f, f_x h0, f_y h1, f_xy h0 h1 at the 4 corners).                                   */
+static void bicubic_matrix(double binv[16][16]) {
+  /* A[r][k]: condition r = 4 q + corner (q: value, d/dt0, d/dt1, d2/dt0dt1; corner = c0 + 2 c1)
+     applied to the monomial k = 4 m + n (t0^m t1^n); binv = A^{-1} by Gauss-Jordan */
+  double A[16][32];
+  for (int q = 0; q < 4; ++q)
+    for (int cr = 0; cr < 4; ++cr) {
+      const int r = 4 * q + cr, c0 = cr & 1, c1 = cr >> 1;
+      for (int m = 0; m < 4; ++m)
+        for (int n = 0; n < 4; ++n) {
+          const int dm = (q == 1 || q == 3), dn = (q == 2 || q == 3);
+          double v = 0.0;
+          if (m >= dm && n >= dn) {
+            v = (dm ? m : 1) * (dn ? n : 1);
+            for (int e = 0; e < m - dm; ++e) v *= c0;
+            for (int e = 0; e < n - dn; ++e) v *= c1;
+          }
+          A[r][4 * m + n] = v;
+        }
+      for (int k = 0; k < 16; ++k) A[r][16 + k] = k == r ? 1.0 : 0.0;
+    }
+  for (int col = 0; col < 16; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < 16; ++r) if (fabs(A[r][col]) > fabs(A[piv][col])) piv = r;
+    for (int k = 0; k < 32; ++k) { double t = A[col][k]; A[col][k] = A[piv][k]; A[piv][k] = t; }
+    const double d = A[col][col];
+    for (int k = 0; k < 32; ++k) A[col][k] /= d;
+    for (int r = 0; r < 16; ++r) {
+      if (r == col || A[r][col] == 0.0) continue;
+      const double f = A[r][col];
+      for (int k = 0; k < 32; ++k) A[r][k] -= f * A[col][k];
+    }
+  }
+  for (int i = 0; i < 16; ++i) for (int k = 0; k < 16; ++k) binv[i][k] = A[i][16 + k];
+}
+
+static int build_bicubic(orc_ctx* c, const double* vals, layer_spline* s) {
+  const int64_t P0 = c->P[0], P1 = c->P[1], n = c->npts;
+  const double h0 = c->dx[0], h1 = c->dx[1];
+  double* fx = (double*)malloc(sizeof(double) * (size_t)n);
+  double* fy = (double*)malloc(sizeof(double) * (size_t)n);
+  double* fxy = (double*)malloc(sizeof(double) * (size_t)n);
+  int e = (fx && fy && fxy) ? ORC_OK : fail(ORC_ERR_RESOURCE, "oom");
+  for (int f = 0; f < c->F && !e; ++f) {
+    const double* F = vals + (size_t)f * n;
+    memcpy(s->f[f].D[0], F, sizeof(double) * (size_t)n);
+    for (int64_t j = 0; j < P1 && !e; ++j) e = fd_line(F + j, P1, P0, h0, fx + j, P1);      /* d/dx_0 */
+    for (int64_t i = 0; i < P0 && !e; ++i) e = fd_line(F + i * P1, 1, P1, h1, fy + i * P1, 1);   /* d/dx_1 */
+    for (int64_t i = 0; i < P0 && !e; ++i) e = fd_line(fx + i * P1, 1, P1, h1, fxy + i * P1, 1);
+    if (e) break;
+    for (int64_t i = 0; i < P0 - 1; ++i)
+      for (int64_t j = 0; j < P1 - 1; ++j) {
+        double v[16];
+        for (int cr = 0; cr < 4; ++cr) {
+          const int64_t idx = (i + (cr & 1)) * P1 + j + (cr >> 1);
+          v[cr] = F[idx];
+          v[4 + cr] = fx[idx] * h0;
+          v[8 + cr] = fy[idx] * h1;
+          v[12 + cr] = fxy[idx] * h0 * h1;
+        }
+        double* a = s->f[f].bic + 16 * (i * (P1 - 1) + j);
+        for (int k = 0; k < 16; ++k) {
+          double acc = 0.0;
+          for (int r = 0; r < 16; ++r) acc += c->binv[k][r] * v[r];
+          a[k] = acc;
+        }
+      }
+  }
+  free(fx); free(fy); free(fxy);
+  return e;
 }
 
 /* moments along axis a of src into dst, for every line of the tensor grid */
@@ -591,6 +741,7 @@ static int axis_pass(orc_ctx* c, const double* src, double* dst, int a) {
 
 static int build_spline(orc_ctx* c, const double* vals, layer_spline* s) {
   int d = c->d;
+  if (c->cfg.interp == ORC_INTERP_BICUBIC) return build_bicubic(c, vals, s);
   for (int f = 0; f < c->F; ++f) {
     memcpy(s->f[f].D[0], vals + (size_t)f * c->npts, sizeof(double) * (size_t)c->npts);
     for (int m = 1; m < (1 << d); ++m) {
@@ -607,6 +758,21 @@ static void eval_spline(const orc_ctx* c, const layer_spline* s, const double* X
   int d = c->d;
   int64_t cell[3];
   double phi[3][2], psi[3][2];
+  if (c->cfg.interp == ORC_INTERP_BICUBIC) {        /* clamp, locate, Horner on the cell's cubic */
+    double t[2];
+    for (int a = 0; a < 2; ++a) cell[a] = locate(X[a], c->cfg.xlo[a], c->cfg.xhi[a], c->dx[a], c->P[a], &t[a]);
+    for (int f = 0; f < c->F; ++f) {
+      const double* A = s->f[f].bic + 16 * (cell[0] * (c->P[1] - 1) + cell[1]);
+      double acc = 0.0;
+      for (int m = 3; m >= 0; --m) {
+        double row = 0.0;
+        for (int n = 3; n >= 0; --n) row = row * t[1] + A[4 * m + n];
+        acc = acc * t[0] + row;
+      }
+      out[f] = acc;
+    }
+    return;
+  }
   for (int a = 0; a < d; ++a) {
     double t;
     double xhi = c->cfg.xhi[a];
@@ -652,7 +818,12 @@ static int point_step(const orc_ctx* c, const layer_spline* const* lv, int K, in
       for (int a = 0; a < d; ++a) {
         wL *= c->gh_w[lam[a]];
         dW[a] = sj * c->gh_a[lam[a]];
-        X[a] = x[a] + dW[a];
+        if (c->cfg.sde_id == ORC_SDE_BROWNIAN) X[a] = x[a] + dW[a];
+        else {                     /* one Euler step of size j dt of Eq. 1 */
+          double aa, bb;
+          sde_coef(&c->cfg, a, x[a], &aa, &bb);
+          X[a] = x[a] + aa * (j * dt) + bb * dW[a];
+        }
       }
       eval_spline(c, lv[j - 1], X, v);
       double f = orc_driver(&c->cfg, tj, v[0], v + 1);
@@ -726,6 +897,8 @@ static int fill_layer(orc_ctx* c, int m, double* vals) {
     if (m == c->N) {
       e = orc_terminal(&c->cfg, x, &y, z);
       if (!e && smooth && kink_in_cell(&c->cfg, x, c->dx)) smooth_point(&c->cfg, x, c->dx, &y, z);
+      if (c->cfg.sde_id != ORC_SDE_BROWNIAN)          /* z = b^T grad u for Eq. 1 */
+        for (int a = 0; a < c->d; ++a) { double aa, bb; sde_coef(&c->cfg, a, x[a], &aa, &bb); z[a] *= bb; }
     } else e = orc_exact(&c->cfg, t, x, &y, z);
     if (e) {
 #pragma omp critical
@@ -764,6 +937,11 @@ int orc_create(const orc_config* cfg, orc_ctx** out) {
   }
   c->stride[c->d - 1] = 1;
   for (int a = c->d - 2; a >= 0; --a) c->stride[a] = c->stride[a + 1] * c->P[a + 1];
+  if (cfg->interp == ORC_INTERP_BICUBIC) {
+    if (c->d != 2) { free(c); return fail(ORC_ERR_ARG, "bicubic interpolation is 2-D (PAPER.md:406)"); }
+    if (c->P[0] < 5 || c->P[1] < 5) { free(c); return fail(ORC_ERR_ARG, "bicubic: >= 5 points per axis"); }
+    bicubic_matrix(c->binv);
+  }
   int e = orc_gauss_hermite(c->L, c->gh_a, c->gh_w);
   if (!e) e = orc_gamma(c->Ky, 0, c->gy);
   if (!e) e = orc_gamma(c->Kz, 1, c->gz);
@@ -837,8 +1015,9 @@ int orc_solve(orc_ctx* c, double* y0, double* z0) {
     int e = orc_step(c);
     if (e) return e;
   }
-  /* evaluation point x = 0 (reading R4): the grid point if the grid has one, else the spline */
-  int on_grid = 1;
+  /* evaluation point x = 0 (reading R4): the grid point if the grid has one, else the spline;
+     forward-SDE problems: X_0 = x_0 = sp[9..11] (Eq. 1), by the spline of layer 0            */
+  int on_grid = c->cfg.sde_id == ORC_SDE_BROWNIAN;
   int64_t idx = 0;
   for (int a = 0; a < c->d; ++a) {
     if (!(c->cfg.xlo[a] == -c->cfg.xhi[a] && (c->P[a] % 2) == 1)) on_grid = 0;
@@ -849,6 +1028,7 @@ int orc_solve(orc_ctx* c, double* y0, double* z0) {
     for (int f = 0; f < c->F; ++f) out[f] = c->values[(size_t)f * c->npts + idx];
   } else {
     double x[3] = {0, 0, 0};
+    if (c->cfg.sde_id != ORC_SDE_BROWNIAN) for (int a = 0; a < c->d; ++a) x[a] = c->cfg.sp[9 + a];
     orc_eval_newest(c, x, out);
   }
   *y0 = out[0];

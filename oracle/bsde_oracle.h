@@ -17,6 +17,9 @@
  *   cell location         PAPER.md:391-392 (int((X-x_min)/dx))
  *   backward sweep        Eq. 20; z first, then y by Picard
  *                         (p = 30 fixed)
+ *   forward SDE           Eq. 1, by "the Euler-Scheme"
+ *   2-D bicubic           PAPER.md:406: first / mixed derivatives by 4th-order finite
+ *                         differences, 16 coefficients per cell by a 16x16 mat-vec
  * Every function below cites the passage it follows.
  */
 #ifndef BSDE_ORACLE_H
@@ -47,8 +50,19 @@ enum { ORC_TERM_CONST = 0,     /* g = p0                                        
        ORC_TERM_SIN_SUM = 5,   /* g = sin(sum_a w_a + T)                   (Eq. 34)        */
        ORC_TERM_EXCHANGE_W = 6,/* S_k = p[k] exp((p[2+k] - s_k^2/2) T + (A w)_k), s=(p4,p5), rho=p6,
                                   g = (S_1 - S_2)^+                        (Eq. 36)        */
-       ORC_TERM_GEO_BASKET_W = 7 /* S_k = p[k] exp((p4 - s_k^2/2) T + s_k w_k), s_k = p[5+k],
-                                  G = (prod S_k)^(1/d), g = (G - p3)^+    (BASELINE cfg 5) */ };
+       ORC_TERM_GEO_BASKET_W = 7,/* S_k = p[k] exp((p4 - s_k^2/2) T + s_k w_k), s_k = p[5+k],
+                                  G = (prod S_k)^(1/d), g = (G - p3)^+    (BASELINE cfg 5) */
+       ORC_TERM_CALL_X = 8     /* forward-SDE payoff in the state x: g = (x_0 - p1)^+        */ };
+
+/* forward process X of Eq. 1, diagonal diffusion, parameters sp;
+   sp[9..11] = X_0 = x_0, the evaluation point of the solution (y_0, z_0) */
+enum { ORC_SDE_BROWNIAN = 0,   /* a = 0, b = 1: X = W (Eq. 2)                              */
+       ORC_SDE_GBM = 1,        /* a_k = sp[k] x_k, b_k = sp[3+k] x_k                       */
+       ORC_SDE_OU = 2          /* a_k = sp[k] (sp[3+k] - x_k), b_k = sp[6+k]               */ };
+
+/* spatial interpolation of a layer */
+enum { ORC_INTERP_SPLINE = 0,  /* tensor not-a-knot cubic spline (Thomas)                  */
+       ORC_INTERP_BICUBIC = 1  /* d = 2: FD (4th order) derivatives + 16-coefficient bicubic */ };
 
 typedef struct {
   int32_t d;                 /* 1..3 */
@@ -66,6 +80,9 @@ typedef struct {
   int32_t bootstrap_substeps;
   int32_t smoothing;         /* 0 off, 1 cell average at the payoff kink (R11) */
   int32_t nthreads;          /* OpenMP threads; 0 -> runtime default */
+  int32_t sde_id;            /* ORC_SDE_*; 0: X = W */
+  double  sp[12];
+  int32_t interp;            /* ORC_INTERP_* */
 } orc_config;
 
 typedef struct orc_ctx orc_ctx;
@@ -80,6 +97,12 @@ int  orc_thomas(int64_t n, const double* a, const double* b, const double* c, co
 int  orc_terminal(const orc_config* cfg, const double* w, double* y, double* z);
 int  orc_exact(const orc_config* cfg, double t, const double* w, double* y, double* z);
 double orc_driver(const orc_config* cfg, double t, double y, const double* z);
+/* weights of the derivative at offset 0 of the degree-4 interpolant through the 5 nodes
+   offsets[0..4] (unit spacing): exact for polynomials of degree <= 4 */
+int  orc_fd_weights(const int* offsets, double* w);
+/* 4th-order first derivative of a line of P >= 5 samples with spacing h (central in the
+   interior, one-sided within 2 nodes of the ends) */
+int  orc_fd_deriv(const double* f, int64_t P, double h, double* df);
 
 /* ---- the solver ---- */
 int  orc_create(const orc_config* cfg, orc_ctx** out);

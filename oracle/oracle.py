@@ -20,7 +20,9 @@ _lib = None
 
 DRIVERS = {"zero": 0, "affine": 1, "ex1": 2, "ex2": 3, "diff_rates": 4}
 TERMINALS = {"const": 0, "poly": 1, "logistic": 2, "ex2": 3, "call_w": 4, "sin_sum": 5,
-             "exchange_w": 6, "geo_basket_w": 7}
+             "exchange_w": 6, "geo_basket_w": 7, "call_x": 8}
+SDES = {"brownian": 0, "gbm": 1, "ou": 2}
+INTERPS = {"spline": 0, "fd_bicubic": 1}
 
 
 class OracleError(RuntimeError):
@@ -48,7 +50,8 @@ class _Cfg(C.Structure):
                 ("terminal_id", C.c_int32), ("tp", C.c_double * 12),
                 ("picard_max", C.c_int32), ("picard_tol", C.c_double),
                 ("bootstrap", C.c_int32), ("bootstrap_substeps", C.c_int32),
-                ("smoothing", C.c_int32), ("nthreads", C.c_int32)]
+                ("smoothing", C.c_int32), ("nthreads", C.c_int32),
+                ("sde_id", C.c_int32), ("sp", C.c_double * 12), ("interp", C.c_int32)]
 
 
 def _load():
@@ -69,6 +72,8 @@ def _load():
             lib.orc_exact.argtypes = [C.POINTER(_Cfg), C.c_double, D, D, D]
             lib.orc_driver.argtypes = [C.POINTER(_Cfg), C.c_double, C.c_double, D]
             lib.orc_driver.restype = C.c_double
+            lib.orc_fd_weights.argtypes = [C.POINTER(C.c_int), D]
+            lib.orc_fd_deriv.argtypes = [D, I64, C.c_double, D]
             lib.orc_create.argtypes = [C.POINTER(_Cfg), C.POINTER(C.c_void_p)]
             lib.orc_step.argtypes = [C.c_void_p]
             lib.orc_solve.argtypes = [C.c_void_p, D, D]
@@ -125,6 +130,11 @@ def make_cfg(spec: dict, nthreads: int = 0) -> _Cfg:
     c.bootstrap_substeps = int(spec.get("bootstrap_substeps", 1))
     c.smoothing = int(spec.get("smoothing", 0))
     c.nthreads = int(nthreads)
+    c.sde_id = SDES[spec.get("sde", "brownian")]
+    sp = list(spec.get("sde_params", [])) + [0.0] * 12
+    for k in range(12):
+        c.sp[k] = float(sp[k])
+    c.interp = INTERPS[spec.get("interp", "spline")]
     return c
 
 
@@ -166,6 +176,20 @@ def thomas(a, b, c, r):
     x = np.zeros_like(r)
     _check(_load().orc_thomas(len(r), _dp(a), _dp(b), _dp(c), _dp(r), _dp(x)))
     return x
+
+
+def fd_weights(offsets):
+    off = (C.c_int * 5)(*[int(o) for o in offsets])
+    w = np.zeros(5)
+    _check(_load().orc_fd_weights(off, _dp(w)))
+    return w
+
+
+def fd_deriv(f, h):
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    df = np.zeros_like(f)
+    _check(_load().orc_fd_deriv(_dp(f), len(f), float(h), _dp(df)))
+    return df
 
 
 def terminal(spec, w):

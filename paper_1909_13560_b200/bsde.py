@@ -21,7 +21,9 @@ STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "RESOURCE_LIMIT", 3: "SINGULAR", 4:
           5: "CUDA", 6: "COMM", 7: "STATE"}
 DRIVERS = {"zero": 0, "affine": 1, "ex1": 2, "ex2": 3, "diff_rates": 4}
 TERMINALS = {"const": 0, "poly": 1, "logistic": 2, "ex2": 3, "call_w": 4, "sin_sum": 5,
-             "exchange_w": 6, "geo_basket_w": 7}
+             "exchange_w": 6, "geo_basket_w": 7, "call_x": 8}
+SDES = {"brownian": 0, "gbm": 1, "ou": 2}
+INTERPS = {"spline": 0, "fd_bicubic": 1}
 
 # every symbol include/bsde.h declares
 EXPORTS = ["bsde_query_workspace", "bsde_setup", "bsde_step", "bsde_solve", "bsde_level", "bsde_get_layer",
@@ -47,13 +49,16 @@ class bsde_config(C.Structure):
                 ("picard_max", C.c_int32), ("picard_tol", C.c_double),
                 ("bootstrap", C.c_int32), ("bootstrap_substeps", C.c_int32), ("smoothing", C.c_int32),
                 ("nranks", C.c_int32), ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p),
-                ("stream", C.c_void_p), ("device", C.c_int32), ("kernel_variant", C.c_int32)]
+                ("stream", C.c_void_p), ("device", C.c_int32), ("kernel_variant", C.c_int32),
+                ("interp", C.c_int32), ("sde_id", C.c_int32), ("sde_params", C.c_double * 12),
+                ("timing", C.c_int32)]
 
 
 class bsde_result(C.Structure):
     _fields_ = [("y0", C.c_double), ("z0", C.c_double * 3), ("t_setup_s", C.c_double),
                 ("t_sweep_s", C.c_double), ("t_total_s", C.c_double), ("updates", C.c_int64),
-                ("picard_max_used", C.c_int32)]
+                ("picard_max_used", C.c_int32), ("t_bootstrap_s", C.c_double), ("t_spline_s", C.c_double),
+                ("t_quad_s", C.c_double), ("t_comm_s", C.c_double)]
 
 
 _lock = threading.Lock()
@@ -104,7 +109,7 @@ def _dp(a):
 
 
 def make_config(spec: dict, device: int = 0, stream: int | None = None, kernel_variant: int = 0,
-                nranks: int = 1, rank: int = 0, nccl_id=None) -> bsde_config:
+                nranks: int = 1, rank: int = 0, nccl_id=None, timing: int = 0) -> bsde_config:
     c = bsde_config()
     c.struct_size = C.sizeof(bsde_config)
     d = int(spec["d"])
@@ -135,6 +140,12 @@ def make_config(spec: dict, device: int = 0, stream: int | None = None, kernel_v
     c.stream = stream
     c.device = int(device)
     c.kernel_variant = int(kernel_variant)
+    c.interp = INTERPS[spec.get("interp", "spline")]
+    c.sde_id = SDES[spec.get("sde", "brownian")]
+    sp = list(spec.get("sde_params", [])) + [0.0] * 12
+    for k in range(12):
+        c.sde_params[k] = float(sp[k])
+    c.timing = int(timing)
     return c
 
 
@@ -184,11 +195,12 @@ class Solver:
     selects the multi-process NCCL mode, None an in-process group (see ``GroupSolver``)."""
 
     def __init__(self, spec: dict, device: int = 0, stream: int | None = None, workspace=None,
-                 kernel_variant: int = 0, nranks: int = 1, rank: int = 0, nccl_id: bytes | None = None):
+                 kernel_variant: int = 0, nranks: int = 1, rank: int = 0, nccl_id: bytes | None = None,
+                 timing: int = 0):
         self._lib = load_library()
         self.spec = dict(spec)
         self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        self.cfg = make_config(spec, device, stream, kernel_variant, nranks, rank, self._id)
+        self.cfg = make_config(spec, device, stream, kernel_variant, nranks, rank, self._id, timing)
         h = C.c_void_p()
         ptr, nbytes = None, 0
         if workspace is not None:          # caller-owned device memory (e.g. a torch uint8 tensor)

@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kA1Thr) aff_rows(StepArgs s, Grid g, Problem p
     s.values[g.npts + pidx] = z[0];
     s.values[2 * g.npts + pidx] = z[1];
     s.picard[pidx] = it;
-    if (!isfinite(y) || !isfinite(z[0]) || !isfinite(z[1])) atomicMin(s.bad, (unsigned long long)pidx);
+    if (!isfinite(y) || !isfinite(z[0]) || !isfinite(z[1])) atomicMin(s.bad, bad_key(s.n, pidx));
   }
 }
 

@@ -43,6 +43,8 @@ struct Problem {
   double tp[12];
   double T, t0, dt;
   int32_t N;
+  int32_t sde_id;          // forward SDE (bsde_sde_id; 0: X = W)
+  double sp[12];           // its parameters
 };
 
 struct Grid {
@@ -81,14 +83,23 @@ struct StepArgs {
   int32_t tap_off;         // byte offset of the AxisTap table (K x d x L) in the constant arena
   int32_t tap1_off;        // byte offset of the Tap1D table (K x L, d = 1) in the constant arena
   double gz0, ky_dt_gy0, ky_dt, tn;
+  double dt;               // step size of this step (the bootstrap's sub-step size inside bsde_setup)
   int32_t picard_max;
   double picard_tol;
   const double* values_in; // level n+1 values (input of the level-1 spline)
   double* values;          // out: F * npts (level n)
   int32_t* picard;         // out: npts
-  unsigned long long* bad; // min index of a non-finite output
+  unsigned long long* bad; // first non-finite output: min of bad_key(n, point) (bsde_internal.h)
+  int32_t n;               // index of the level this step computes (ring_mode 0 launches)
   unsigned long long* phase_ns;  // optional (debug): per-CTA %globaltimer stamps of the fused kernel
 };
+
+// Non-finite diagnostic key: the sweep runs n = N-K .. 0, so the smallest key is the first
+// (largest n) non-finite point; decoded by the host (bsde_last_error names n, i, t, x, y, z).
+constexpr int kBadShift = 40;
+__host__ __device__ inline unsigned long long bad_key(int n, long long point) {
+  return ((unsigned long long)(0xFFFFFu - (unsigned)n) << kBadShift) | (unsigned long long)point;
+}
 
 // Geometry of the fused 1-D step kernel (kernels.cu, quad1d_fused).
 struct Fused1D {
@@ -117,8 +128,8 @@ struct Persist1D {
   unsigned* done_flag;
   int D[kMaxK + 1];  // D[j]: CTA distance of level j's window (j >= 1); D[0]: values halo of phase A
   int DK;            // max of D
-  int nowait;        // debug (BSDE_DEBUG_NOWAIT): skip every flag wait -- wrong results, busy time only
-  int nopad;         // debug (BSDE_DEBUG_NOPAD): skip the edge CTAs' pad fill -- wrong results
+  int nowait;        // debug build only (-DBSDE_DEBUG, BSDE_DEBUG_NOWAIT): skip every flag wait -- wrong results, busy time only
+  int nopad;         // debug build only (-DBSDE_DEBUG, BSDE_DEBUG_NOPAD): skip the edge CTAs' pad fill -- wrong results
 };
 
 // One problem of a fused launch and the launch itself.  All problems of a launch share the

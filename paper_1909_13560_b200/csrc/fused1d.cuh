@@ -55,11 +55,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// per-CTA phase stamps: a debug build only (-DBSDE_DEBUG); the product library compiles them out
+#ifdef BSDE_DEBUG
 #define PHASE_STAMP(i)                                                                          \
   do {                                                                                          \
     if (s.phase_ns != nullptr && threadIdx.x == 0)                                              \
       s.phase_ns[((size_t)it_stamp * gridDim.x + blockIdx.x) * 32 + (i)] = gtimer();              \
   } while (0)
+#define DBG_FLAG(x) (x)
+#else
+#define PHASE_STAMP(i) do { (void)it_stamp; } while (0)
+#define DBG_FLAG(x) 0
+#endif
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   unsigned v;
@@ -221,7 +228,7 @@ __device__ __forceinline__ void issue_window(const FusedProb& fp, const int* sp,
 // Level n+j was written by pass 2 of round it-j by the CTAs within D[j]: levels >= 2 are
 // covered by the ring flags of round it-2 within DK, level 1 needs round it-1 within D[1].
 __device__ __forceinline__ void ring_wait(const FusedProb& fp, unsigned* mk, int it, int j, int bid, int nb) {
-  if (it == 0 || fp.pp.nowait) return;
+  if (it == 0 || DBG_FLAG(fp.pp.nowait)) return;
   const Persist1D& pp = fp.pp;
   if (j == 1) wait_flags(pp.ring_flag, mk, bid, pp.D[1], pp.DK, nb, (unsigned)it);
   else if (it >= 2) wait_flags(pp.ring_flag, mk, bid, pp.DK, pp.DK, nb, (unsigned)(it - 1));
@@ -555,7 +562,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         vout[p] = y;
         vout[P + p] = z;
         s.picard[p] = itp;
-        if (!isfinite(y) || !isfinite(z)) atomicMin(s.bad, (unsigned long long)p);
+        if (!isfinite(y) || !isfinite(z)) atomicMin(s.bad, bad_key(pp.ring_mode ? pp.n0 - it : s.n, p));
       }
       PHASE_STAMP(18);
       // generic-proxy accesses of the level buffers before later bulk copies into them
@@ -586,7 +593,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       PHASE_STAMP(10);
       // the CTAs within D[0] wrote their level-n values (done flag it+1); the CTAs within DK
       // finished pass 1 of round it-2, the last reader of ring slot n (level n + K + 2)
-      if (warp == 0 && !pp.nowait) {
+      if (warp == 0 && !DBG_FLAG(pp.nowait)) {
         unsigned* mk = marks + 4 * ip + 2;
         if (it >= 2) wait_flags(pp.done_flag, mk, bid, pp.DK, pp.DK, nb, (unsigned)(it - 1));
         wait_flags(pp.done_flag, mk, bid, pp.D[0], pp.DK, nb, (unsigned)it + 1);
@@ -707,12 +714,12 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         // s(x_0) = (c_{-1} + 4 c_0 + c_1)/6 and s(x_{P-1}), from shared memory
         // (16-byte stores: the pad [-cpad, 0) is 16-byte aligned, cpad even; the right pad
         // starts at P + 3, its odd-aligned head and tail take 8-byte stores)
-        if (k0 == -1 && !pp.nopad) {
+        if (k0 == -1 && !DBG_FLAG(pp.nopad)) {
           const double v = (1.0 / 6.0) * coef(-1) + (2.0 / 3.0) * coef(0) + (1.0 / 6.0) * coef(1);
           double2* q = reinterpret_cast<double2*>(rf - s.cpad);
           for (int i = tid; i < (int)(s.cpad >> 1); i += NT) q[i] = make_double2(v, v);
         }
-        if (k1 == P + 1 && !pp.nopad) {
+        if (k1 == P + 1 && !DBG_FLAG(pp.nopad)) {
           const double v = (1.0 / 6.0) * coef(P - 2) + (2.0 / 3.0) * coef(P - 1) + (1.0 / 6.0) * coef(P);
           double* r0 = rf + P + 3;
           const int h = (int)((reinterpret_cast<uintptr_t>(r0) >> 3) & 1);     // 1: odd-aligned start
@@ -863,8 +870,10 @@ cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& 
   for (int i = 0; i < nprob; ++i) {
     bt.prob[i] = probs[order[i]];
     if (bt.prob[i].pp.nsteps > bt.max_steps) bt.max_steps = bt.prob[i].pp.nsteps;
-    if (getenv("BSDE_DEBUG_NOWAIT")) bt.prob[i].pp.nowait = 1;
+#ifdef BSDE_DEBUG
+    if (getenv("BSDE_DEBUG_NOWAIT")) bt.prob[i].pp.nowait = 1;   // timing experiments only: wrong results
     if (getenv("BSDE_DEBUG_NOPAD")) bt.prob[i].pp.nopad = 1;
+#endif
     cudaError_t e = cudaMemsetAsync(probs[i].pp.ring_flag, 0, sizeof(unsigned) * 2 * (size_t)blocks, st);
     if (e != cudaSuccess) return e;
   }

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(k2NT, 1) quad2d(StepArgs s, Grid g, Problem pb
     s.values[g.npts + pidx] = z[0];
     s.values[2 * g.npts + pidx] = z[1];
     s.picard[pidx] = it;
-    if (!isfinite(y) || !isfinite(z[0]) || !isfinite(z[1])) atomicMin(s.bad, (unsigned long long)pidx);
+    if (!isfinite(y) || !isfinite(z[0]) || !isfinite(z[1])) atomicMin(s.bad, bad_key(s.n, pidx));
   }
 }
 

@@ -396,7 +396,7 @@ __global__ void epilogue_zy3(StepArgs s, Grid g, Problem pb, const double* __res
   s.values[2 * g.npts + pidx] = z[1];
   s.values[3 * g.npts + pidx] = z[2];
   s.picard[pidx] = it;
-  if (!isfinite(y) || !isfinite(z[0]) || !isfinite(z[1]) || !isfinite(z[2])) atomicMin(s.bad, (unsigned long long)pidx);
+  if (!isfinite(y) || !isfinite(z[0]) || !isfinite(z[1]) || !isfinite(z[2])) atomicMin(s.bad, bad_key(s.n, pidx));
 }
 
 // shared memory of quad3d for a column-window width WC (doubles)

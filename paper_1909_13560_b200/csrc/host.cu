@@ -54,6 +54,10 @@ int fused2d_window(const AxisTap* host_taps, int K, int L);
 size_t fused2d_smem(int WC);
 int fused3d_window(const AxisTap* host_taps, int K, int L);
 size_t fused3d_smem(int WC, int nf);
+cudaError_t launch_fsde_step(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st);
+cudaError_t launch_hermite(const Grid& g, const double* values, int F, double* slot, cudaStream_t st, int64_t* launches);
+cudaError_t launch_bicubic_step(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st);
+cudaError_t launch_eval_bicubic(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
 cudaError_t launch_step3d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, double* A, double* acc,
                           int decompose, cudaStream_t st, int64_t* launches);
 }  // namespace bsde
@@ -115,7 +119,17 @@ struct bsde_ctx {
   bool grouped = false;             // in-process group mode (bsde_group_*)
   std::string err;
   bool closed_form = true;
+  // timing: host-clock setup time; CUDA-event stage timers (bootstrap always, the others with
+  // cfg.timing = 1), accumulated until the next bsde_solve collects them
+  double t_setup = 0;
+  bool in_setup = false;              // bootstrap steps inside bsde_setup count as t_bootstrap_s only
+  struct Stage { int kind; cudaEvent_t a, b; };
+  std::vector<Stage> stages;
+  std::vector<cudaEvent_t> ev_free;
+  double t_stage[4] = {0, 0, 0, 0};   // 0 spline, 1 quadrature, 2 comm, 3 bootstrap
 };
+
+enum { ST_SPLINE = 0, ST_QUAD = 1, ST_COMM = 2, ST_BOOT = 3 };
 
 static bsde_status set_err(bsde_ctx* c, bsde_status st, const char* fmt, ...) {
   char buf[1024];
@@ -134,6 +148,36 @@ static bsde_status set_err(bsde_ctx* c, bsde_status st, const char* fmt, ...) {
     if (_e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "%s: %s (%s:%d)", #call,         \
                                           cudaGetErrorString(_e), __FILE__, __LINE__);        \
   } while (0)
+
+// ------------------------------------------------------------------ stage timers
+static cudaEvent_t tmark(bsde_ctx* c) {
+  cudaEvent_t e = nullptr;
+  if (!c->ev_free.empty()) { e = c->ev_free.back(); c->ev_free.pop_back(); }
+  else if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  cudaEventRecord(e, c->stream);
+  return e;
+}
+static void tstage(bsde_ctx* c, int kind, cudaEvent_t a) {
+  if (!a) return;
+  cudaEvent_t b = tmark(c);
+  if (b) c->stages.push_back({kind, a, b});
+}
+// after the stream has been synchronised: accumulate and recycle the events
+static void tcollect(bsde_ctx* c) {
+  for (auto& st : c->stages) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, st.a, st.b) == cudaSuccess) c->t_stage[st.kind] += ms * 1e-3;
+    c->ev_free.push_back(st.a);
+    c->ev_free.push_back(st.b);
+  }
+  c->stages.clear();
+}
+static void tfree(bsde_ctx* c) {
+  for (auto& st : c->stages) { c->ev_free.push_back(st.a); c->ev_free.push_back(st.b); }
+  c->stages.clear();
+  for (cudaEvent_t e : c->ev_free) cudaEventDestroy(e);
+  c->ev_free.clear();
+}
 
 // ------------------------------------------------------------------ constant-arena allocator
 namespace {
@@ -272,6 +316,15 @@ void bspline_basis(long double t, double* B) {
   B[3] = (double)(t * t * t / 6.0L);
 }
 
+// cubic Hermite basis at theta (FD-bicubic interpolation, bicubic.cuh): H00, H10, H01, H11
+void hermite_basis(long double t, double* H) {
+  const long double t2 = t * t, t3 = t2 * t;
+  H[0] = (double)(2.0L * t3 - 3.0L * t2 + 1.0L);
+  H[1] = (double)(t3 - 2.0L * t2 + t);
+  H[2] = (double)(-2.0L * t3 + 3.0L * t2);
+  H[3] = (double)(t3 - t2);
+}
+
 // tap table of levels 1..K for step dt: X = x_i + s, s = sqrt(2 j dt) a_l
 void build_taps(const bsde_ctx* c, int K, double dt, std::vector<AxisTap>& out, int* qspan, int* qspan1) {
   const int d = c->d, L = c->L;
@@ -286,7 +339,8 @@ void build_taps(const bsde_ctx* c, int K, double dt, std::vector<AxisTap>& out, 
         const long double u = s / (long double)c->g.dx[a];
         const long double q = floorl(u);
         t.q = (int32_t)q;
-        bspline_basis(u - q, t.B);
+        if (c->cfg.interp == BSDE_INTERP_FD_BICUBIC) hermite_basis(u - q, t.B);
+        else bspline_basis(u - q, t.B);
         t.w = (double)((long double)c->gh_w[l] * rpi);
         t.s = (double)s;
       }
@@ -375,6 +429,8 @@ bsde_status plan_partition(bsde_ctx* c) {
 bool closed_form_supported(const bsde_config& cfg) {
   const int t = cfg.terminal_id, f = cfg.driver_id, d = cfg.d;
   const double* q = cfg.driver_params;
+  if (cfg.sde_id != BSDE_SDE_BROWNIAN)        // forward SDE: only the constant solution is known
+    return t == BSDE_TERM_CONST && f == BSDE_DRV_ZERO;
   if (t == BSDE_TERM_CONST) return f == BSDE_DRV_ZERO || (f == BSDE_DRV_AFFINE && q[1] == 0 && q[2] == 0 && q[3] == 0);
   if (t == BSDE_TERM_POLY)
     return f == BSDE_DRV_ZERO || (f == BSDE_DRV_AFFINE && q[1] == 0 && q[2] == 0 && q[3] == 0 && q[4] == 0);
@@ -402,7 +458,22 @@ bsde_status validate(const bsde_config* cfg, bsde_ctx* c) {
   if (cfg->N < K) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "N=%d < K=%d", cfg->N, K);
   if (cfg->picard_max < 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "picard_max < 1");
   if (cfg->driver_id < 0 || cfg->driver_id > 4) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "driver_id");
-  if (cfg->terminal_id < 0 || cfg->terminal_id > 7) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "terminal_id");
+  if (cfg->terminal_id < 0 || cfg->terminal_id > 8) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "terminal_id");
+  if (cfg->sde_id < 0 || cfg->sde_id > 2) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "sde_id %d outside 0..2", cfg->sde_id);
+  if (cfg->terminal_id == BSDE_TERM_CALL_X && cfg->sde_id == BSDE_SDE_BROWNIAN)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "terminal CALL_X is a payoff of a forward SDE: set sde_id");
+  if (cfg->sde_id != BSDE_SDE_BROWNIAN && cfg->terminal_id != BSDE_TERM_CALL_X && cfg->terminal_id != BSDE_TERM_POLY &&
+      cfg->terminal_id != BSDE_TERM_CONST)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "forward-SDE problems take the terminal CALL_X, POLY or CONST");
+  if (cfg->sde_id != BSDE_SDE_BROWNIAN && cfg->driver_id == BSDE_DRV_EX2)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "the Ex. 2 driver is defined for X = W only");
+  if (cfg->sde_id != BSDE_SDE_BROWNIAN && cfg->nranks > 1)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "forward-SDE problems run on one rank");
+  if (cfg->sde_id != BSDE_SDE_BROWNIAN && cfg->smoothing)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "terminal smoothing is defined for X = W payoffs only (R11)");
+  if (cfg->interp < 0 || cfg->interp > 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "interp %d outside 0..1", cfg->interp);
+  if (cfg->interp == BSDE_INTERP_FD_BICUBIC && (cfg->d != 2 || cfg->sde_id != BSDE_SDE_BROWNIAN || cfg->nranks > 1))
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "FD-bicubic interpolation is the paper's 2-D scheme: d = 2, X = W, one rank");
   if (cfg->driver_id == BSDE_DRV_EX2 && cfg->d != 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "EX2 driver is 1-D");
   if (cfg->terminal_id == BSDE_TERM_EXCHANGE_W && cfg->d != 2)
     return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "exchange payoff needs d=2");
@@ -410,11 +481,20 @@ bsde_status validate(const bsde_config* cfg, bsde_ctx* c) {
     return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "nranks > 1 needs d >= 2 (1-D runs as replicas, DESIGN.md)");
   if (cfg->nranks > 1 && (cfg->rank < 0 || cfg->rank >= cfg->nranks))
     return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "rank %d outside 0..%d", cfg->rank, cfg->nranks - 1);
+  // an in-process group refreshes halos only in bsde_group_step: the one-step bootstrap inside
+  // bsde_setup would build slab splines from stale halo rows
+  if (cfg->nranks > 1 && cfg->nccl_unique_id == nullptr && cfg->bootstrap == 1 && std::max(cfg->Ky, cfg->Kz) > 1)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT,
+                   "in-process slab groups need closed-form initial layers (bootstrap = 0) or K = 1; "
+                   "the NCCL multi-process mode supports the bootstrap");
   for (int a = 0; a < cfg->d; ++a) {
     if (!(cfg->xhi[a] > cfg->xlo[a])) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "empty box on axis %d", a);
     if (cfg->npts[a] != 0 && cfg->npts[a] < 4)
       return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "npts[%d]=%lld < 4 (not-a-knot needs 4 points)", a,
                      (long long)cfg->npts[a]);
+    if (cfg->interp == BSDE_INTERP_FD_BICUBIC && cfg->npts[a] != 0 && cfg->npts[a] < 6)
+      return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "npts[%d]=%lld < 6 (4th-order one-sided differences need 5 nodes "
+                     "on a side of every node)", a, (long long)cfg->npts[a]);
   }
   if (cfg->bootstrap == 0 && K > 1 && !closed_form_supported(*cfg))
     return set_err(c, BSDE_ERR_INVALID_ARGUMENT,
@@ -453,6 +533,7 @@ void fill_grid(const bsde_config* cfg, Grid& g, double dt) {
     g.cfield += 2 * g.cpad;
   }
   for (int a = d; a < 3; ++a) { g.vstride[a] = 0; g.cstride[a] = 0; }
+  if (cfg->interp == BSDE_INTERP_FD_BICUBIC) g.cfield = 4 * g.npts;   // f, h0 f_x, h1 f_y, h0 h1 f_xy
   g.off0 = 0;
   g.Pg0 = g.P[0];
   g.own0 = 0;
@@ -484,7 +565,12 @@ void localize_grid(Grid& g, int64_t lo_e, int64_t hi_e, int64_t r0, int64_t r1) 
 // the d = 2 affine-driver path (aff2.cuh) is the default for f = 0 and
 // affine f; kernel_variant 2 keeps the per-tap fused kernel
 bool use_aff2(const bsde_config* cfg) {
-  return cfg->d == 2 && cfg->kernel_variant == 0 && (cfg->driver_id == 0 || cfg->driver_id == 1);
+  return cfg->d == 2 && cfg->kernel_variant == 0 && (cfg->driver_id == 0 || cfg->driver_id == 1) &&
+         cfg->interp == BSDE_INTERP_SPLINE && cfg->sde_id == BSDE_SDE_BROWNIAN;
+}
+// the d = 3 fused path (plane stacks) serves X = W problems
+bool use_fused3d(const bsde_config* cfg) {
+  return (cfg->kernel_variant == 0 || cfg->kernel_variant == 2) && cfg->sde_id == BSDE_SDE_BROWNIAN;
 }
 
 struct Layout {
@@ -527,6 +613,15 @@ double now_s() {
 
 bsde_status exchange_nccl(bsde_ctx* c);
 
+// interpolant of the newest values into ring slot `slot`: tensor not-a-knot spline (B-spline
+// coefficients), or the Hermite data of the FD-bicubic surfaces (interp = 1)
+cudaError_t build_level(bsde_ctx* c, int slot) {
+  double* dst = c->ring + (int64_t)slot * c->F * c->g.cfield;
+  if (c->cfg.interp == BSDE_INTERP_FD_BICUBIC)
+    return launch_hermite(c->g, c->vbuf[c->cur], c->F, dst, c->stream, &c->launches);
+  return launch_spline(c->g, c->vbuf[c->cur], c->F, dst, c->tmp0, c->tmp1, c->stream, &c->launches);
+}
+
 // One step of the scheme (Eq. 20) from the newest values (level n+1) and the ring slots of
 // levels n+2..n+K: slots[0] receives the spline of the newest values.  Output -> the other
 // value buffer, which becomes the newest.
@@ -555,6 +650,7 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
   s.ky_dt = Kyl * dtl;
   s.ky_dt_gy0 = Kyl * dtl * gyl[0];
   s.tn = tn;
+  s.dt = dtl;
   s.picard_max = c->cfg.picard_max;
   s.picard_tol = c->cfg.picard_tol;
   s.values_in = c->vbuf[c->cur];
@@ -562,16 +658,26 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
   s.picard = c->picard;
   s.bad = c->bad;
   s.phase_ns = c->phase_ns;
+  s.n = (int)std::floor((tn - c->cfg.t0) / c->dt + 0.5);      // level index (bootstrap: nearest level)
+  const bool timing = c->cfg.timing != 0 && !c->in_setup;
   cudaError_t e;
-  if (c->d == 1 && (variant == 0 || variant >= 10) && geo.ok && tap1_off >= 0) {
+  if (c->d == 1 && (variant == 0 || variant >= 10) && geo.ok && tap1_off >= 0 && c->pb.sde_id == 0) {
+    cudaEvent_t t0 = timing ? tmark(c) : nullptr;            // spline fused into the kernel
     e = launch_fused1d_steps(s, c->g, c->pb, geo.fz, 0, 1, 0, c->cur, 0.0, 0.0, c->vbuf[0], c->vbuf[1], c->barrier,
                              geo.D, geo.DK, geo.threads, geo.blocks, geo.smem, c->stream);
     ++c->launches;
+    if (timing) tstage(c, ST_QUAD, t0);
   } else {
-    e = launch_spline(c->g, c->vbuf[c->cur], c->F, c->ring + (int64_t)slots[0] * c->F * c->g.cfield, c->tmp0,
-                      c->tmp1, c->stream, &c->launches);
+    cudaEvent_t t0 = timing ? tmark(c) : nullptr;
+    e = build_level(c, slots[0]);
+    if (timing) tstage(c, ST_SPLINE, t0);
+    cudaEvent_t t1 = timing ? tmark(c) : nullptr;
     if (e == cudaSuccess) {
-      if (c->d == 2 && variant == 0 && c->a3 && c->wca > 0 && (c->pb.driver_id == 0 || c->pb.driver_id == 1))
+      if (c->pb.sde_id != 0)                                   // forward SDE: per-point Euler samples
+        e = launch_fsde_step(s, c->g, c->pb, c->stream);
+      else if (c->cfg.interp == BSDE_INTERP_FD_BICUBIC)        // the paper's 2-D interpolation
+        e = launch_bicubic_step(s, c->g, c->pb, c->stream);
+      else if (c->d == 2 && variant == 0 && c->a3 && c->wca > 0 && (c->pb.driver_id == 0 || c->pb.driver_id == 1))
         e = launch_aff2(s, c->g, c->pb, c->a3, c->wca, c->stream, &c->launches);
       else if (c->d == 2 && (variant == 0 || variant == 2) && wc2 > 0 && c->pb.driver_id != 3)
         e = launch_quad2d(s, c->g, c->pb, wc2, c->stream);
@@ -582,6 +688,7 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
         e = launch_generic_step(s, c->g, c->pb, c->stream);
       ++c->launches;
     }
+    if (timing) tstage(c, ST_QUAD, t1);
   }
   if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "step kernels: %s", cudaGetErrorString(e));
   c->cur ^= 1;
@@ -616,6 +723,7 @@ int64_t row_len(const bsde_ctx* c) { return c->g.npts / c->g.P[0]; }
 
 bsde_status exchange_nccl(bsde_ctx* c) {
   if (c->nranks <= 1 || c->grouped) return BSDE_OK;
+  cudaEvent_t t0 = c->cfg.timing && !c->in_setup ? tmark(c) : nullptr;
   const HaloPlan hp = halo_plan(c);
   const int64_t rl = row_len(c);
   double* v = c->vbuf[c->cur];
@@ -634,14 +742,14 @@ bsde_status exchange_nccl(bsde_ctx* c) {
     }
   }
   ncclResult_t ne = ncclGroupEnd();
+  tstage(c, ST_COMM, t0);
   if (nr != ncclSuccess || ne != ncclSuccess)
     return set_err(c, BSDE_ERR_COMM, "halo exchange: %s", ncclGetErrorString(nr != ncclSuccess ? nr : ne));
   return BSDE_OK;
 }
 
 bsde_status spline_into(bsde_ctx* c, int slot) {
-  cudaError_t e = launch_spline(c->g, c->vbuf[c->cur], c->F, c->ring + (int64_t)slot * c->F * c->g.cfield, c->tmp0,
-                                c->tmp1, c->stream, &c->launches);
+  cudaError_t e = build_level(c, slot);
   if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "spline kernel: %s", cudaGetErrorString(e));
   return BSDE_OK;
 }
@@ -655,11 +763,16 @@ void release(bsde_ctx* c) {
   if (c->boot_tap1_off >= 0) arena_free(dev, c->boot_tap1_off);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->phase_ns) cudaFree(c->phase_ns);
+  tfree(c);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
 }  // namespace
+
+extern "C" {
+static bsde_status bsde_eval_internal(bsde_ctx* c, const double* x, double* out);
+}
 
 // The evaluation point x = 0 (reading R4): the grid value if 0 is a grid node, else the
 // spline of the newest level at 0.  With a slab partition the rank owning the cell of x = 0
@@ -667,6 +780,9 @@ void release(bsde_ctx* c) {
 // Leaves out[] on the host (synchronises c->stream).
 bsde_status eval_point(bsde_ctx* c, double* out) {
   for (int f = 0; f < 4; ++f) out[f] = 0.0;
+  if (c->pb.sde_id != 0) {                 // forward SDE: X_0 = x_0 (Eq. 1), one rank (validate)
+    return bsde_eval_internal(c, c->pb.sp + 9, out);
+  }
   bool on_grid = true;
   for (int a = 0; a < c->d; ++a)
     if (!(c->g.xlo[a] == -c->g.xhi[a] && ((a == 0 ? c->P0g : c->g.P[a]) % 2) == 1)) on_grid = false;
@@ -687,7 +803,9 @@ bsde_status eval_point(bsde_ctx* c, double* out) {
       const double x[3] = {0, 0, 0};
       bsde_status st = spline_into(c, c->RS);                 // newest level -> scratch slot
       if (st) return st;
-      cudaError_t e = launch_eval(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, x, c->dres, c->stream);
+      cudaError_t e = c->cfg.interp == BSDE_INTERP_FD_BICUBIC
+                          ? launch_eval_bicubic(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, x, c->dres, c->stream)
+                          : launch_eval(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, x, c->dres, c->stream);
       ++c->launches;
       if (e == cudaSuccess) e = cudaMemcpyAsync(out, c->dres, sizeof(double) * c->F, cudaMemcpyDeviceToHost, c->stream);
       if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "eval: %s", cudaGetErrorString(e));
@@ -719,6 +837,7 @@ bsde_status group_exchange(bsde_ctx** cs, int n) {
     const HaloPlan hp = halo_plan(c);
     const int64_t rl = row_len(c);
     cudaSetDevice(c->cfg.device);
+    cudaEvent_t t0 = c->cfg.timing && !c->in_setup ? tmark(c) : nullptr;
     for (int side = 0; side < 2; ++side) {
       const int nbr = side == 0 ? r - 1 : r + 1;
       if (nbr < 0 || nbr >= n) continue;
@@ -737,6 +856,7 @@ bsde_status group_exchange(bsde_ctx** cs, int n) {
         if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "halo copy: %s", cudaGetErrorString(e));
       }
     }
+    tstage(c, ST_COMM, t0);
   }
   for (int r = 0; r < n; ++r) {
     cudaSetDevice(cs[r]->cfg.device);
@@ -756,7 +876,7 @@ bsde_status bsde_query_workspace(const bsde_config* cfg, size_t* bytes) {
   const int K = std::max(cfg->Ky, cfg->Kz);
   Grid g{};
   fill_grid(cfg, g, (cfg->T - cfg->t0) / cfg->N);
-  *bytes = layout(g, 1 + cfg->d, K, cfg->L, cfg->kernel_variant == 0 || cfg->kernel_variant == 2, use_aff2(cfg)).total;
+  *bytes = layout(g, 1 + cfg->d, K, cfg->L, use_fused3d(cfg), use_aff2(cfg)).total;
   return BSDE_OK;
 }
 
@@ -786,6 +906,8 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   for (int k = 0; k < 12; ++k) { c->pb.dp[k] = cfg->driver_params[k]; c->pb.tp[k] = cfg->terminal_params[k]; }
   c->pb.T = cfg->T;
   c->pb.t0 = cfg->t0;
+  c->pb.sde_id = cfg->sde_id;
+  for (int k = 0; k < 12; ++k) c->pb.sp[k] = cfg->sde_params[k];
   c->pb.dt = c->dt;
   c->pb.N = cfg->N;
   for (int j = 0; j <= c->Ky; ++j) c->gy[j] = (double)kTab1[c->Ky - 1][j];
@@ -827,7 +949,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     }
   }
   // memory
-  Layout lay = layout(c->g, c->F, c->K, c->L, cfg->kernel_variant == 0 || cfg->kernel_variant == 2, use_aff2(cfg));
+  Layout lay = layout(c->g, c->F, c->K, c->L, use_fused3d(cfg), use_aff2(cfg));
   if (d_workspace) {
     if (bytes < lay.total) {
       set_err(c, BSDE_ERR_RESOURCE_LIMIT, "workspace of %zu bytes < required %zu", bytes, lay.total);
@@ -857,14 +979,19 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   c->bad = (unsigned long long*)(c->ws + lay.bad);
   c->barrier = (unsigned*)(c->ws + lay.barrier);
   c->dres = (double*)(c->ws + lay.dres);
-  if (getenv("BSDE_PHASE_TIMING")) {
+#ifdef BSDE_DEBUG
+  if (getenv("BSDE_PHASE_TIMING")) {      // debug build only: per-CTA phase stamps of the fused 1-D kernel
     if (cudaMalloc((void**)&c->phase_ns, (size_t)8 * 32 * 600 * 1100) != cudaSuccess) c->phase_ns = nullptr;
     else cudaMemset(c->phase_ns, 0, (size_t)8 * 32 * 600 * 1100);
   }
+#endif
   // zero the whole ring once: the padding entry c_{P+1} of every line is read with weight 0
   ce = cudaMemsetAsync(c->ring - c->g.cpad, 0, sizeof(double) * (size_t)(c->RS + 1) * c->F * c->g.cfield, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->picard, 0, sizeof(int32_t) * c->g.npts, c->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(c->bad, 0xff, sizeof(unsigned long long), c->stream);
+  // both value buffers: halo rows of a slab are defined before the first exchange
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->vbuf[0], 0, sizeof(double) * (size_t)c->F * c->g.npts, c->stream);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(c->vbuf[1], 0, sizeof(double) * (size_t)c->F * c->g.npts, c->stream);
   if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "memset: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
 
   // tap tables -> constant arena
@@ -880,11 +1007,12 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     c->wc2 = fused3d_window(c->taps.data(), c->K, c->L);
     if (fused3d_smem(c->wc2, 4) > 112 * 1024) c->wc2 = 0;
   }
-  if (c->d == 1) {
+  if (c->d == 1 && cfg->sde_id == BSDE_SDE_BROWNIAN) {
     c->geo.ok = fused1d_geometry(c->g, c->K, c->L, c->qspan, c->nsm, c->fused_variant, c->geo.fz,
                                  c->geo.threads, c->geo.blocks, c->geo.smem);
     set_distances(c, c->taps, c->K, c->geo);
   }
+  if (cfg->sde_id != BSDE_SDE_BROWNIAN || cfg->interp != BSDE_INTERP_SPLINE) { c->wc2 = 0; c->wca = 0; }
   c->tap_count = (int)c->taps.size();
   {
     const int bytes = (int)(sizeof(AxisTap) * c->taps.size());
@@ -917,13 +1045,15 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "layer: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
   if ((st = spline_into(c, N % c->RS))) return fail(st);
   c->level = N;
+  cudaEvent_t tb0 = tmark(c);                  // device time of the K-1 initial layers (t_bootstrap_s)
+  c->in_setup = true;
   if (K > 1 && cfg->bootstrap == 1) {
     // one-step scheme (K = 1) on S_b sub-steps per coarse interval (reading R9)
     const int Sb = cfg->bootstrap_substeps > 0 ? cfg->bootstrap_substeps : 1;
     const double db = c->dt / Sb;
     std::vector<AxisTap> bt;
     build_taps(c, 1, db, bt, &c->boot_qspan, &c->boot_qspan1);
-    if (c->d == 1) {
+    if (c->d == 1 && cfg->sde_id == BSDE_SDE_BROWNIAN) {
       c->boot_geo.ok = fused1d_geometry(c->g, 1, c->L, c->boot_qspan, c->nsm, c->fused_variant,
                                         c->boot_geo.fz, c->boot_geo.threads, c->boot_geo.blocks, c->boot_geo.smem);
       set_distances(c, bt, 1, c->boot_geo);
@@ -975,15 +1105,16 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
       c->level = m;
     }
   }
+  tstage(c, ST_BOOT, tb0);
+  c->in_setup = false;
   ce = cudaMemsetAsync(c->picard, 0, sizeof(int32_t) * c->g.npts, c->stream);
   if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "memset: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
-  (void)t_start;
+  c->t_setup = now_s() - t_start;
   *out = c;
   return BSDE_OK;
 }
 
-bsde_status bsde_step(bsde_ctx* c) {
-  if (!c) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "ctx is NULL");
+static bsde_status step_internal(bsde_ctx* c) {
   if (c->level <= 0) return set_err(c, BSDE_ERR_STATE, "already at n = 0");
   cudaSetDevice(c->cfg.device);
   const int n = c->level - 1;
@@ -996,14 +1127,36 @@ bsde_status bsde_step(bsde_ctx* c) {
   return BSDE_OK;
 }
 
+bsde_status bsde_step(bsde_ctx* c) {
+  if (!c) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (c->grouped && c->nranks > 1)
+    return set_err(c, BSDE_ERR_STATE, "member of an in-process slab group: use bsde_group_step (halo refresh)");
+  return step_internal(c);
+}
+
+// device non-finite flag: the first (largest n) non-finite point, with (n, i, t_n, x_i) and the
+// y, z values the newest level holds there
 static bsde_status check_bad(bsde_ctx* c) {
   unsigned long long bad = 0;
   cudaError_t e = cudaMemcpyAsync(&bad, c->bad, sizeof bad, cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
-  if (bad != ~0ULL)
-    return set_err(c, BSDE_ERR_NUMERICAL_DOMAIN, "non-finite y or z at point %llu (level <= %d)", bad, c->level + 1);
-  return BSDE_OK;
+  if (bad == ~0ULL) return BSDE_OK;
+  const int n = (int)(0xFFFFFu - (unsigned)(bad >> kBadShift));
+  const int64_t p = (int64_t)(bad & ((1ULL << kBadShift) - 1));
+  double x[3] = {0, 0, 0}, v[4] = {0, 0, 0, 0};
+  int64_t q = p;
+  for (int a = c->d - 1; a >= 0; --a) {
+    const int64_t i = q % c->g.P[a] + (a == 0 ? c->g.off0 : 0);
+    q /= c->g.P[a];
+    x[a] = c->g.xlo[a] + (double)i * c->g.dx[a];
+  }
+  for (int f = 0; f < c->F && p < c->g.npts; ++f)
+    cudaMemcpy(&v[f], c->vbuf[c->cur] + (int64_t)f * c->g.npts + p, sizeof(double), cudaMemcpyDeviceToHost);
+  return set_err(c, BSDE_ERR_NUMERICAL_DOMAIN,
+                 "non-finite y or z: first at level n = %d (t = %.6g), point i = %lld (x = %.6g, %.6g, %.6g); the newest "
+                 "level (n = %d) holds y = %g, z = (%g, %g, %g) there", n, c->cfg.t0 + n * c->dt, (long long)p, x[0], x[1],
+                 x[2], c->level, v[0], v[1], v[2], v[3]);
 }
 
 // StepArgs of a persistent fused launch (ring_mode 1: the kernel derives the per-step slots,
@@ -1029,15 +1182,22 @@ static StepArgs persistent_args(const bsde_ctx* c) {
   return s;
 }
 
-static void fill_result(bsde_ctx* c, bsde_result* res, const double out[4], double t_sweep, double t_total,
+static void fill_result(bsde_ctx* c, bsde_result* res, const double out[4], double t_sweep, double t_call,
                         int64_t steps) {
   memset(res, 0, sizeof *res);
   res->y0 = out[0];
   for (int a = 0; a < c->d; ++a) res->z0[a] = out[1 + a];
+  res->t_setup_s = c->t_setup;
   res->t_sweep_s = t_sweep;
-  res->t_total_s = t_total;
+  res->t_total_s = c->t_setup + t_call;
   res->updates = c->g.nown0 * row_len(c) * steps;
   res->picard_max_used = c->cfg.picard_max;
+  tcollect(c);                                   // the stream is synchronised by now
+  res->t_spline_s = c->t_stage[ST_SPLINE];
+  res->t_quad_s = c->t_stage[ST_QUAD];
+  res->t_comm_s = c->t_stage[ST_COMM];
+  res->t_bootstrap_s = c->t_stage[ST_BOOT];
+  c->t_stage[ST_SPLINE] = c->t_stage[ST_QUAD] = c->t_stage[ST_COMM] = 0.0;   // per call
 }
 
 bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
@@ -1053,14 +1213,16 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
   bsde_status st = BSDE_OK;
   // d = 1 fused path: all remaining steps in one cooperative (persistent) launch
   const bool fused = c->d == 1 && (c->cfg.kernel_variant == 0 || c->cfg.kernel_variant >= 10) && c->geo.ok &&
-                     c->tap1_off >= 0 && getenv("BSDE_NO_PERSISTENT") == nullptr;
+                     c->tap1_off >= 0;
   if (fused && c->level >= 2) {
     const StepArgs s = persistent_args(c);
     const int ns = c->level;
+    cudaEvent_t tq = c->cfg.timing ? tmark(c) : nullptr;
     cudaError_t e = launch_fused1d_steps(s, c->g, c->pb, c->geo.fz, c->level - 1, ns, 1, c->cur, c->cfg.t0, c->dt, c->vbuf[0],
                                c->vbuf[1], c->barrier, c->geo.D, c->geo.DK, c->geo.threads, c->geo.blocks,
                                c->geo.smem, c->stream);
     ++c->launches;
+    tstage(c, ST_QUAD, tq);
     if (e != cudaSuccess) st = set_err(c, BSDE_ERR_CUDA, "persistent step kernel: %s", cudaGetErrorString(e));
     else {
       c->cur ^= (ns & 1);
@@ -1069,7 +1231,7 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
     }
   }
   while (st == BSDE_OK && c->level > 0) {
-    if ((st = bsde_step(c))) break;
+    if ((st = step_internal(c))) break;
     ++steps;
   }
   cudaEventRecord(e1, c->stream);
@@ -1079,12 +1241,13 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  if (res) {
+  // the evaluation point is a collective in the NCCL mode: every rank takes part
+  if (res || c->comm) {
     double out[4] = {0, 0, 0, 0};
     if ((st = eval_point(c, out))) return st;
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
-    fill_result(c, res, out, ms * 1e-3, now_s() - t0, steps);
+    if (res) fill_result(c, res, out, ms * 1e-3, now_s() - t0, steps);
   }
   return BSDE_OK;
 }
@@ -1276,7 +1439,7 @@ bsde_status bsde_group_step(bsde_ctx** cs, int32_t n) {
     if (!cs[r] || cs[r]->rank != r || cs[r]->nranks != n || (n > 1 && !cs[r]->grouped))
       return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "group member %d is not rank %d of %d (in-process mode)", r, r, n);
   for (int r = 0; r < n; ++r) {
-    bsde_status st = bsde_step(cs[r]);
+    bsde_status st = step_internal(cs[r]);
     if (st) return st;
   }
   return n > 1 ? group_exchange(cs, n) : BSDE_OK;
@@ -1302,11 +1465,21 @@ bsde_status bsde_group_solve(bsde_ctx** cs, int32_t n, bsde_result* res) {
     for (int f = 0; f < 4; ++f) out[f] += o[f];
   }
   if (res) {
-    memset(res, 0, sizeof *res);
+    fill_result(cs[0], res, out, 0.0, 0.0, steps);
+    for (int r = 1; r < n; ++r) {                    // stage times: the slowest rank
+      tcollect(cs[r]);
+      res->t_spline_s = std::max(res->t_spline_s, cs[r]->t_stage[ST_SPLINE]);
+      res->t_quad_s = std::max(res->t_quad_s, cs[r]->t_stage[ST_QUAD]);
+      res->t_comm_s = std::max(res->t_comm_s, cs[r]->t_stage[ST_COMM]);
+      cs[r]->t_stage[ST_SPLINE] = cs[r]->t_stage[ST_QUAD] = cs[r]->t_stage[ST_COMM] = 0.0;
+    }
     res->y0 = out[0];
     for (int a = 0; a < cs[0]->d; ++a) res->z0[a] = out[1 + a];
-    res->t_total_s = now_s() - t0;
-    res->t_sweep_s = res->t_total_s;
+    double tset = 0;
+    for (int r = 0; r < n; ++r) tset = std::max(tset, cs[r]->t_setup);
+    res->t_setup_s = tset;
+    res->t_sweep_s = now_s() - t0;               // host clock: the group synchronises every step
+    res->t_total_s = tset + res->t_sweep_s;
     int64_t pts = 0;
     for (int r = 0; r < n; ++r) pts += cs[r]->g.nown0 * row_len(cs[r]);
     res->updates = pts * steps;
@@ -1333,12 +1506,18 @@ bsde_status bsde_query_taps(const bsde_ctx* cc, int32_t level, int32_t axis, int
 
 bsde_status bsde_eval(bsde_ctx* c, const double* x, double* out) {
   if (!c || !x || !out) return BSDE_ERR_INVALID_ARGUMENT;
+  return bsde_eval_internal(c, x, out);
+}
+
+static bsde_status bsde_eval_internal(bsde_ctx* c, const double* x, double* out) {
   cudaSetDevice(c->cfg.device);
   double xx[3] = {0, 0, 0};
   for (int a = 0; a < c->d; ++a) xx[a] = x[a];
   bsde_status st = spline_into(c, c->RS);                        // newest level -> scratch slot
   if (st) return st;
-  CU(launch_eval(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, xx, c->dres, c->stream));
+  CU(c->cfg.interp == BSDE_INTERP_FD_BICUBIC
+         ? launch_eval_bicubic(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, xx, c->dres, c->stream)
+         : launch_eval(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, xx, c->dres, c->stream));
   ++c->launches;
   CU(cudaMemcpyAsync(out, c->dres, sizeof(double) * c->F, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
@@ -1364,12 +1543,15 @@ bsde_status bsde_kernel_launches(const bsde_ctx* c, int64_t* count) {
   return BSDE_OK;
 }
 
-// debug only (not in bsde.h): per-CTA phase stamps of the last fused step
+#ifdef BSDE_DEBUG
+// debug build only (not in bsde.h, not in the product library): per-CTA phase stamps of the
+// last fused step
 int bsde_internal_phase_times(const bsde_ctx* c, unsigned long long* host, int n) {
   if (!c || !c->phase_ns) return 1;
   cudaStreamSynchronize(c->stream);
   return cudaMemcpy(host, c->phase_ns, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess;
 }
+#endif
 
 const char* bsde_last_error(const bsde_ctx* c) { return c ? c->err.c_str() : g_setup_error.c_str(); }
 

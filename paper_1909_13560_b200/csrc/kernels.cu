@@ -123,6 +123,8 @@ __global__ void layer_kernel(Problem pb, Grid g, double t, int terminal, double*
         }
       }
     }
+    if (pb.sde_id != SDE_BROWNIAN)           // z = b^T grad u (forward-SDE problems, Eq. 1)
+      for (int a = 0; a < d; ++a) z[a] *= sde_diffusion(pb, a, x[a]);
   } else {
     exact_eval(pb, t, x, y, z);
   }
@@ -476,7 +478,7 @@ __device__ inline void epilogue(const StepArgs& s, int64_t p, int64_t npts, doub
     bad |= !isfinite(z[a]);
   }
   s.picard[p] = it;
-  if (bad) atomicMin(s.bad, (unsigned long long)p);
+  if (bad) atomicMin(s.bad, bad_key(s.n, p));
 }
 
 // ------------------------------------------------------------------ generic fused kernel
@@ -553,6 +555,8 @@ __global__ void __launch_bounds__(256) quad_generic(StepArgs s, Grid g, Problem 
 #include "fused2d.cuh"
 #include "fused3d.cuh"
 #include "aff2.cuh"
+#include "fsde.cuh"
+#include "bicubic.cuh"
 
 template <int D, int DRV>
 static cudaError_t launch_generic(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st) {

@@ -9,7 +9,16 @@ namespace bsde {
 
 enum { DRV_ZERO = 0, DRV_AFFINE = 1, DRV_EX1 = 2, DRV_EX2 = 3, DRV_DIFF = 4 };
 enum { TRM_CONST = 0, TRM_POLY = 1, TRM_LOGISTIC = 2, TRM_EX2 = 3, TRM_CALL = 4, TRM_SIN = 5,
-       TRM_EXCHANGE = 6, TRM_GEO = 7 };
+       TRM_EXCHANGE = 6, TRM_GEO = 7, TRM_CALLX = 8 };
+enum { SDE_BROWNIAN = 0, SDE_GBM = 1, SDE_OU = 2 };
+
+// diffusion coefficient b_a(x) of the forward SDE (diagonal; bsde.h bsde_sde_id): the terminal
+// layer of a forward-SDE problem is z_T = b(x) grad g(x) (z = b^T grad u)
+__device__ inline double sde_diffusion(const Problem& pb, int a, double x) {
+  if (pb.sde_id == SDE_GBM) return pb.sp[3 + a] * x;
+  if (pb.sde_id == SDE_OU) return pb.sp[6 + a];
+  return 1.0;
+}
 
 // ---------------------------------------------------------------- drivers f(t, y, z)
 template <int DRV, int D> struct Driver;
@@ -165,6 +174,11 @@ __device__ inline void terminal_eval(const Problem& pb, const double* w, double&
       const double G = exp(lg / d);
       if (G > p[3]) { y = G - p[3]; for (int k = 0; k < d; ++k) z[k] = G * p[5 + k] / d; }
       else y = 0.0;
+      return;
+    }
+    case TRM_CALLX: {                      // (x_0 - K)^+ in the state variable; grad g only
+      y = w[0] > p[1] ? w[0] - p[1] : 0.0;
+      z[0] = w[0] > p[1] ? 1.0 : 0.0;
       return;
     }
   }

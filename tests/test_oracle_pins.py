@@ -333,41 +333,47 @@ def test_P7_picard_closed_form(oracle_mod):
 
 
 # --------------------------------------------------------------------------- P9/P10 printed rows
-def _rows(example, maxN):
-    return [r for r in _golden("printed_errors.txt") if r[0] == example and int(r[2]) <= maxN]
+def _rows(example, maxN, minN=0):
+    """Gated rows of tests/golden/printed_tables.txt (every printed row of Tables 4, 5, 9 with the
+    reason of each exclusion: R10 for K = 2, the rounding floor for y < 1e-12, Table 9 K=1 N=8 z)."""
+    return [r for r in _golden("printed_tables.txt")
+            if r[0] == example and minN <= int(r[2]) <= maxN and r[7] != "-"]
 
 
-@pytest.mark.parametrize("row", _rows("ex1", 256) + _rows("ex2", 256), ids=lambda r: f"{r[0]}_K{r[1]}_N{r[2]}")
+def _check_row(row, ey, ez):
+    _, K, N, M, ye, ze, line, gate, _ = row
+    if "y" in gate:
+        assert abs(ey / float(ye) - 1) <= 0.03, (ey, ye, line)
+    if "z" in gate:
+        assert abs(ez / float(ze) - 1) <= 0.03, (ez, ze, line)
+
+
+@pytest.mark.parametrize("row", _rows("ex1", 128) + _rows("ex2", 128) +
+                         [r for r in _rows("ex1", 256, 256) + _rows("ex2", 256, 256) if r[1] == "1"],
+                         ids=lambda r: f"{r[0]}_K{r[1]}_N{r[2]}")
 def test_P9_printed_rows_1d(oracle_mod, row):
+    """Printed rows of Tables 4 and 5 (Ex. 1, Ex. 2) reproduced to 3 % by the oracle (the CPU suite
+    runs N <= 128 and the K = 1, N = 256 rows; the GPU suite runs every gated row)."""
     from paper_1909_13560_b200 import workloads as W
-    ex, K, N, M, ye, ze, _ = row
-    K, N = int(K), int(N)
-    if N > 512 and K > 1:
-        pytest.skip("too slow for the CPU suite")
+    ex, K, N, M = row[0], int(row[1]), int(row[2]), int(row[3])
     spec = (W.ex1 if ex == "ex1" else W.ex2)(K, N)
     o = oracle_mod.Oracle(spec, nthreads=os.cpu_count())
-    assert o.shape == (int(M) + 1,)
+    assert o.shape == (M + 1,)
     y0, z0 = o.solve()
     ref = W.reference_solution(spec)
-    ey, ez = abs(y0 - ref[0]), abs(z0[0] - ref[1][0])
-    assert abs(ey / float(ye) - 1) <= 0.03, (ey, ye)
-    assert abs(ez / float(ze) - 1) <= 0.03, (ez, ze)
+    _check_row(row, abs(y0 - ref[0]), abs(z0[0] - ref[1][0]))
 
 
 @pytest.mark.parametrize("row", _rows("ex4", 16), ids=lambda r: f"{r[0]}_K{r[1]}_N{r[2]}")
 def test_P10_printed_rows_2d(oracle_mod, row):
+    """Table 9 (Ex. 4) with the tensor spline (north_star, reading R14)."""
     from paper_1909_13560_b200 import workloads as W
-    _, K, N, M, ye, ze, _ = row
-    K, N = int(K), int(N)
+    K, N, M = int(row[1]), int(row[2]), int(row[3])
     spec = W.ex4_2d(K, N)
     o = oracle_mod.Oracle(spec, nthreads=os.cpu_count())
-    assert o.shape == (int(M) + 1,) * 2
+    assert o.shape == (M + 1,) * 2
     y0, z0 = o.solve()
-    ey = abs(y0 - 0.0)
-    ez = float(np.linalg.norm(np.asarray(z0) - 1.0))   # Euclidean norm (reading R15)
-    tol_z = 0.05 if K == 1 else 0.03
-    assert abs(ey / float(ye) - 1) <= 0.03, (ey, ye)
-    assert abs(ez / float(ze) - 1) <= tol_z, (ez, ze)
+    _check_row(row, abs(y0 - 0.0), float(np.linalg.norm(np.asarray(z0) - 1.0)))   # Euclidean z (R15)
 
 
 # --------------------------------------------------------------------------- P12 orders
@@ -443,3 +449,346 @@ def test_smoothing_is_the_cell_average(oracle_mod):
     g2 = lambda b, a: oracle_mod.terminal(spec2, [a, b])[0]  # noqa: E731
     avg = dblquad(g2, x[i] - h / 2, x[i] + h / 2, x[j] - h / 2, x[j] + h / 2, epsabs=1e-12)[0] / h ** 2
     assert abs(y2[i, j] - avg) < 2e-4 * abs(avg)
+
+
+# --------------------------------------------------------------------------- d = 3 pins
+# The 3-D oracle path (tensor spline by successive Thomas passes in build_spline /
+# eval_spline, the L^3 tensor tap loop of point_step, the GL16^3 smoothing box_avg) is
+# pinned against: exact polynomial solutions (P6), the constant invariant (P8), the 1-D
+# oracle on data that vary along one axis only (the tensor spline of such data is the 1-D
+# spline, the tensor GH rule of such a function is the 1-D rule), scipy's tensor-product
+# not-a-knot B-spline interpolant (library), and nested scipy quad of the payoff (smoothing).
+
+def _poly3_spec(K, factors, N=4, P=17, T=0.25, box=4.0, L=4):
+    """f = 0, g = prod_a p_a(x_a) with cubic factors p_a (coefficients c0..c3 per axis)."""
+    from paper_1909_13560_b200 import workloads as W
+    s = W.heat_poly(3, K, N=N, P=P, T=T, box=box, L=L)
+    s["terminal_params"] = [float(c) for f in factors for c in f]
+    return s
+
+
+def _heat_cubic(c, x, tau):
+    """E[p(x + W_tau)] and its x-derivative for a cubic p (W_tau ~ N(0, tau)):
+    E[(x+W)^2] = x^2 + tau, E[(x+W)^3] = x^3 + 3 x tau."""
+    v = c[0] + c[1] * x + c[2] * (x * x + tau) + c[3] * (x ** 3 + 3 * x * tau)
+    dv = c[1] + 2 * c[2] * x + 3 * c[3] * (x * x + tau)
+    return v, dv
+
+
+@pytest.mark.parametrize("K", [1, 2, 3])
+def test_P6_heat_polynomial_exact_3d(oracle_mod, K):
+    """P6, d = 3: f = 0, g = p1(x1) p2(x2) p3(x3) with factors of degree 3, 2, 3 (distinct per
+    axis, so a swapped axis, stride or corner weight breaks exactness).  The tensor not-a-knot
+    spline reproduces g, the L = 4 tensor Gauss-Hermite rule integrates degree <= 7 per axis
+    exactly, so y = prod_a E[p_a(x_a + W)] and z_a = dE[p_a]/dx_a prod_{b != a} E[p_b] hold to
+    rounding at every point whose taps stay inside the box (Eq. 20-21).
+    N = K: one sweep step from K exact levels (closed-form initial layers, reading R9), so the
+    clamped boundary taps of earlier steps cannot leak inward through the spline's global
+    coupling (0.268^k per cell); multi-step propagation in 3-D is pinned by the 1-D embedding
+    test below."""
+    factors = [[0.0, 0.0, 0.0, 1.0], [0.5, 1.0, 1.0, 0.0], [0.0, -2.0, 0.0, 1.0]]
+    spec = _poly3_spec(K, factors, N=K)
+    o = oracle_mod.Oracle(spec, nthreads=os.cpu_count())
+    o.solve()
+    x = np.linspace(-4.0, 4.0, 17)
+    tau = spec["T"]
+    vals = [_heat_cubic(f, x, tau) for f in factors]
+    m = np.abs(x) <= 2.5                                   # taps reach sqrt(2 T) a_max = 1.17 < 4 - 2.5
+    X = np.ix_(m, m, m)
+    v = [vals[a][0][m] for a in range(3)]
+    dv = [vals[a][1][m] for a in range(3)]
+    y_ex = np.einsum("i,j,k->ijk", v[0], v[1], v[2])
+    z_ex = [np.einsum("i,j,k->ijk", dv[0], v[1], v[2]), np.einsum("i,j,k->ijk", v[0], dv[1], v[2]),
+            np.einsum("i,j,k->ijk", v[0], v[1], dv[2])]
+    L = o.layers()
+    assert np.max(np.abs(L[0][X] - y_ex)) <= 1e-12 * np.max(np.abs(y_ex))
+    for a in range(3):
+        assert np.max(np.abs(L[1 + a][X] - z_ex[a])) <= 1e-12 * np.max(np.abs(z_ex[a])), a
+
+
+@pytest.mark.parametrize("Ky,Kz", [(1, 1), (1, 3), (3, 1), (2, 2), (3, 3), (2, 4)])
+def test_P8_constant_solution_invariant_3d(oracle_mod, Ky, Kz):
+    """P8, d = 3: f = 0, g = c gives y = c, z = 0 at every point, boundary included."""
+    from paper_1909_13560_b200 import workloads as W
+    spec = dict(W.constant(3, Ky, Kz, N=6, P=6, c=2.5, L=3), npts=[5, 6, 7])
+    o = oracle_mod.Oracle(spec, nthreads=2)
+    o.solve()
+    L = o.layers()
+    assert np.max(np.abs(L[0] - 2.5)) <= 1e-14
+    assert np.max(np.abs(L[1:])) <= 1e-14
+
+
+def _embedded_pair(K, Ky, Kz, axis, driver):
+    """A 1-D problem and the same problem embedded in 3-D along `axis` (data constant along
+    the other two axes, transverse sizes 5 and 6)."""
+    from paper_1909_13560_b200 import workloads as W
+    if driver == "diff_rates":                     # z-dependent nonlinear driver, call payoff (x_0 only)
+        s1 = W.diff_rates(K, N=6, P=41, L=6, smoothing=0)
+    else:                                          # Ex. 1 driver, bounded cubic terminal
+        s1 = dict(W.ex1(K, 6, L=6, npts=41), terminal="poly", terminal_params=[0.5, 0.08, 0.004, -0.0015])
+    s1 = dict(s1, Ky=Ky, Kz=Kz, T=0.5, xlo=[-6.0], xhi=[6.0], bootstrap=1, bootstrap_substeps=2)
+    shape = [5, 6, 6]
+    shape[axis] = 41
+    s3 = dict(s1, d=3, npts=shape, xlo=[-3.0, -2.0, -4.0], xhi=[3.0, 2.5, 4.0])
+    s3["xlo"][axis], s3["xhi"][axis] = -6.0, 6.0
+    if driver == "diff_rates":
+        dp = list(s1["driver_params"])
+        s3["driver_params"] = [dp[0], dp[1], dp[2], 0.0, 0.0, dp[5], 0.0, 0.0]
+    else:
+        tp = [1.0, 0.0, 0.0, 0.0] * 3
+        tp[4 * axis:4 * axis + 4] = s1["terminal_params"][:4]
+        s3["terminal_params"] = tp
+    return s1, s3
+
+
+@pytest.mark.parametrize("driver,axis,K,Ky,Kz", [("diff_rates", 0, 3, 3, 3), ("ex1", 0, 2, 2, 1),
+                                                  ("ex1", 1, 3, 2, 3), ("ex1", 2, 3, 3, 3),
+                                                  ("ex1", 2, 1, 1, 1)])
+def test_3d_oracle_equals_1d_oracle_on_axis_data(oracle_mod, driver, axis, K, Ky, Kz):
+    """Data varying along one axis only: the tensor spline (moments of constant lines are 0)
+    is the 1-D spline of that axis, and the L^3 tensor Gauss-Hermite rule of a function of
+    x_axis is the 1-D rule times sum_b w_b sum_c w_c / pi = 1.  So every layer of the 3-D
+    oracle restricted to one transverse line equals the 1-D oracle's layer (to rounding), z of
+    the other two axes vanishes, and this holds for a nonlinear, z-dependent driver (Eq. 20
+    with Eq. 21), the bootstrap and Ky != Kz.  A mask -> axis, stride, corner
+    weight or dW-axis mistake in the 3-D path shows up as an O(1) difference."""
+    s1, s3 = _embedded_pair(K, Ky, Kz, axis, driver)
+    o1 = oracle_mod.Oracle(s1, nthreads=os.cpu_count())
+    o1.solve()
+    o3 = oracle_mod.Oracle(s3, nthreads=os.cpu_count())
+    o3.solve()
+    L1, L3 = o1.layers(), o3.layers()
+    y3 = np.moveaxis(L3[0], axis, -1).reshape(-1, 41)
+    z3 = np.moveaxis(L3[1 + axis], axis, -1).reshape(-1, 41)
+    for row in range(y3.shape[0]):
+        assert np.max(np.abs(y3[row] - L1[0])) <= 1e-13 * np.max(np.abs(L1[0])), row
+        assert np.max(np.abs(z3[row] - L1[1])) <= 1e-13 * np.max(np.abs(L1[1])), row
+    for b in range(3):
+        if b != axis:
+            assert np.max(np.abs(L3[1 + b])) <= 1e-13 * np.max(np.abs(L1[1]))
+
+
+def test_P3_spline_3d_equals_scipy_tensor_not_a_knot(oracle_mod):
+    """The oracle's 3-D tensor spline (values + moments, successive Thomas passes) equals
+    scipy's tensor-product not-a-knot cubic B-spline interpolant (make_interp_spline along each
+    axis, NdBSpline), on a non-cubic grid with distinct sizes and boxes per axis, at random
+    points inside and outside the box (clamped per coordinate)."""
+    from scipy.interpolate import make_interp_spline, NdBSpline
+    from paper_1909_13560_b200 import workloads as W
+    spec = dict(W.ex1_3d(K=1, N=4, L=2, P=9), npts=[9, 11, 13], xlo=[-4.0, -3.0, -5.0], xhi=[4.0, 2.0, 3.0])
+    o = oracle_mod.Oracle(spec, nthreads=2)
+    V = o.layers()
+    axes = [np.linspace(lo, hi, n) for lo, hi, n in zip(spec["xlo"], spec["xhi"], spec["npts"])]
+    rng = np.random.Generator(np.random.PCG64(1909135600))
+    pts = [[rng.uniform(lo - 1, hi + 1) for lo, hi in zip(spec["xlo"], spec["xhi"])] for _ in range(100)]
+    got = np.array([o.eval_newest(x) for x in pts])
+    for f in range(4):
+        c, ts = V[f], []
+        for a in range(3):
+            sp = make_interp_spline(axes[a], c, k=3, axis=a)      # not-a-knot for k = 3
+            c = np.moveaxis(sp.c, 0, a)
+            ts.append(sp.t)
+        nd = NdBSpline(tuple(ts), c, 3)
+        ref = nd(np.clip(pts, spec["xlo"], spec["xhi"]))
+        assert np.max(np.abs(got[:, f] - ref)) <= 1e-13 * np.max(np.abs(V[f])), f
+
+
+def test_smoothing_3d_is_the_cell_average(oracle_mod):
+    """Reading R11 in 3-D: at a grid point whose cell meets the payoff kink, y^N is the cell
+    average of g (geometric-basket call).  Reference: nested scipy quad with the
+    kink plane (log G is affine in w) passed as a break point.  The oracle's GL16^3 rule of a
+    kinked integrand is accurate to ~1e-4 of the payoff scale; a wrong operator (point value,
+    shifted cell) is off by O(1) of it."""
+    import math
+    from scipy.integrate import quad
+    from paper_1909_13560_b200 import workloads as W
+    spec = dict(W.basket_3d(K=1, N=2, L=2, P=9), npts=[9, 9, 9])
+    o = oracle_mod.Oracle(spec, nthreads=2)
+    V = o.layers()
+    p = spec["terminal_params"]
+    S0, K, mu, sg, T = p[:3], p[3], p[4], p[5:8], spec["T"]
+    alpha = sum(math.log(S0[k]) + (mu - 0.5 * sg[k] ** 2) * T for k in range(3)) / 3
+    beta = [s / 3 for s in sg]
+
+    def g(a, b, c):
+        return max(math.exp(alpha + beta[0] * a + beta[1] * b + beta[2] * c) - K, 0.0)
+
+    def kink(b, c):
+        return (math.log(K) - alpha - beta[1] * b - beta[2] * c) / beta[0]
+
+    x = np.linspace(-8, 8, 9)
+    h = x[1] - x[0]
+    i, j, k = 0, 3, 7                                     # the kink plane crosses this cell
+    lo = [x[i] - h / 2, x[j] - h / 2, x[k] - h / 2]
+    hi = [x[i] + h / 2, x[j] + h / 2, x[k] + h / 2]
+    corners = [g(a, b, c) for a in (lo[0], hi[0]) for b in (lo[1], hi[1]) for c in (lo[2], hi[2])]
+    assert min(corners) == 0.0 < max(corners)
+
+    def inner(b, c):
+        kp = min(max(kink(b, c), lo[0]), hi[0])
+        return quad(lambda a: g(a, b, c), lo[0], hi[0], points=[kp], epsabs=1e-12, epsrel=1e-12)[0]
+
+    mid = lambda c: quad(lambda b: inner(b, c), lo[1], hi[1], epsabs=1e-10, epsrel=1e-10)[0]  # noqa: E731
+    avg = quad(mid, lo[2], hi[2], epsabs=1e-10, epsrel=1e-10)[0] / h ** 3
+    assert abs(V[0][i, j, k] - avg) <= 1e-3 * max(corners), (V[0][i, j, k], avg)
+    # away from the kink the terminal layer is g itself
+    assert abs(V[0][8, 8, 8] - g(x[8], x[8], x[8])) <= 1e-14 * V[0][8, 8, 8] and V[0][0, 0, 0] == 0.0
+
+
+# --------------------------------------------------------------------------- forward SDE (Eq. 1)
+# The FBSDE of Eq. 1 (PAPER.md:30-40) with the forward process approximated "by using the
+# Euler-Scheme" (PAPER.md:50): the level-j sample from x_i is x_i + a(x_i) j dt + b(x_i) dW_j.
+
+def _fsde_spec(sde, sp, terminal, tp, driver="zero", dp=(), K=1, N=2, P=257, box=(-8.0, 8.0), T=0.1, L=8):
+    return dict(d=1, t0=0.0, T=T, N=N, Ky=K, Kz=K, L=L, npts=[P], xlo=[box[0]], xhi=[box[1]], r=4,
+                driver=driver, driver_params=list(dp), terminal=terminal, terminal_params=list(tp),
+                sde=sde, sde_params=list(sp), bootstrap=1, bootstrap_substeps=2, picard_max=30, name=f"fsde_{sde}")
+
+
+def test_fsde_brownian_special_case_is_the_bsde_path(oracle_mod):
+    """OU with kappa = 0, sigma = 1 is X = W: the Euler sample x + 0 * j dt + 1 * dW is bitwise
+    x + dW, so every layer equals the X = W solve of Eq. 2 (Ex. 2 driver, K = 3, bootstrap)."""
+    from paper_1909_13560_b200 import workloads as W
+    s = dict(W.ex2(3, 16, npts=801), bootstrap=1, bootstrap_substeps=2)
+    a = oracle_mod.Oracle(s, nthreads=os.cpu_count())
+    a.solve()
+    b = oracle_mod.Oracle(dict(s, sde="ou", sde_params=[0.0] * 6 + [1.0] * 3), nthreads=os.cpu_count())
+    b.solve()
+    assert np.array_equal(a.layers(), b.layers())
+
+
+def test_fsde_gbm_linear_payoff_exact(oracle_mod):
+    """GBM dX = mu X dt + sigma X dW, f = 0, g = x, K = 1: E[X_{n+1} | x] = x (1 + mu dt) for one
+    Euler step, the spline reproduces linear data and the Gauss-Hermite rule integrates linear
+    functions exactly, so y^n = x (1 + mu dt)^(N-n) and z^n = sigma x (1 + mu dt)^(N-n)
+    (z = b grad u, Eq. 1; z^N = sigma x) at every point whose samples stay inside the box."""
+    mu, sig, N = 0.35, 0.4, 4
+    spec = _fsde_spec("gbm", [mu, 0, 0, sig, 0, 0, 0, 0, 0, 1.0], "poly", [0.0, 1.0, 0.0, 0.0], N=N, P=321,
+                      box=(0.0, 16.0), T=0.2)
+    o = oracle_mod.Oracle(spec, nthreads=2)
+    o.solve()
+    x = np.linspace(0.0, 16.0, 321)
+    m = x <= 3.0                      # the clamped samples near x = 16 leak through the spline to ~x = 8
+    fac = (1.0 + mu * spec["T"] / N) ** N
+    assert np.max(np.abs(o.layer(0)[m] - x[m] * fac)) <= 1e-13 * 8
+    assert np.max(np.abs(o.layer(1)[m] - sig * x[m] * fac)) <= 1e-13 * 8
+
+
+def _gauss_compose(coef, alpha, beta, s):
+    """Coefficients (ascending) of x -> E[p(alpha x + beta + s Z)], Z ~ N(0, 1), for the polynomial
+    p with ascending coefficients coef; E[Z^m] = (m-1)!! for even m, 0 for odd m."""
+    from numpy.polynomial import polynomial as Pn
+    out = np.zeros(1)
+    lin = np.array([beta, alpha])
+    for k, ck in enumerate(coef):
+        acc = np.zeros(1)
+        for m in range(0, k + 1, 2):
+            ez = float(np.prod(np.arange(m - 1, 0, -2))) if m else 1.0
+            acc = Pn.polyadd(acc, math.comb(k, m) * s ** m * ez * Pn.polypow(lin, k - m))
+        out = Pn.polyadd(out, ck * acc)
+    return out
+
+
+def test_fsde_ou_cubic_exact_discrete_solution(oracle_mod):
+    """OU dX = kappa (theta - X) dt + sigma dW, f = 0, g = x^3 - x, K = 1: one Euler step maps
+    x to alpha x + beta + sigma sqrt(dt) Z with alpha = 1 - kappa dt, beta = kappa theta dt, so the
+    discrete solution stays a cubic, y^n(x) = E[y^{n+1}(alpha x + beta + sigma sqrt(dt) Z)] and
+    z^n = E[z^{n+1}(...)] from z^N = sigma g'(x) (Eq. 20 with K = 1, f = 0) -- computed here by
+    polynomial algebra.  The spline reproduces cubics, L = 4 Gauss-Hermite is exact to degree 7."""
+    from numpy.polynomial import polynomial as Pn
+    kap, th, sig, N, T = 0.7, 0.3, 0.5, 3, 0.15
+    spec = _fsde_spec("ou", [kap, 0, 0, th, 0, 0, sig, 0, 0, 0.0], "poly", [0.0, -1.0, 0.0, 1.0], N=N, P=257, T=T, L=4)
+    o = oracle_mod.Oracle(spec, nthreads=2)
+    o.solve()
+    dt = T / N
+    y = np.array([0.0, -1.0, 0.0, 1.0])
+    z = sig * Pn.polyder(y)
+    for _ in range(N):
+        y = _gauss_compose(y, 1 - kap * dt, kap * th * dt, sig * math.sqrt(dt))
+        z = _gauss_compose(z, 1 - kap * dt, kap * th * dt, sig * math.sqrt(dt))
+    x = np.linspace(-8.0, 8.0, 257)
+    m = np.abs(x) <= 3.0
+    assert np.max(np.abs(o.layer(0)[m] - Pn.polyval(x[m], y))) <= 1e-12 * 27
+    assert np.max(np.abs(o.layer(1)[m] - Pn.polyval(x[m], z))) <= 1e-12 * 27
+
+
+def test_fsde_gbm_black_scholes_in_price_space(oracle_mod):
+    """Black-Scholes call (Ex. 3 parameters without dividend) solved in price space:
+    X = S is a GBM with drift mu, f = -(r y + theta z), theta = (mu - r)/sigma (Eq. 29-30).
+    Accuracy, not parity: y0 at S0 = K = 100 within 0.5 % of the closed form and z0 within 2 %
+    (the Euler forward step is weak order 1; a wrong drift would be off by ~|mu - r| T S0 ~ 0.7)."""
+    from scipy.stats import norm
+    S0, Kst, r, mu, sig, T = 100.0, 100.0, 0.03, 0.05, 0.2, 0.33
+    d1 = (math.log(S0 / Kst) + (r + 0.5 * sig ** 2) * T) / (sig * math.sqrt(T))
+    ey = S0 * norm.cdf(d1) - Kst * math.exp(-r * T) * norm.cdf(d1 - sig * math.sqrt(T))
+    ez = sig * S0 * norm.cdf(d1)
+    spec = _fsde_spec("gbm", [mu, 0, 0, sig, 0, 0, 0, 0, 0, S0], "call_x", [0.0, Kst], driver="affine",
+                      dp=[-r, -(mu - r) / sig, 0, 0, 0], K=3, N=32, P=1601, box=(0.0, 400.0), T=T, L=16)
+    o = oracle_mod.Oracle(spec, nthreads=os.cpu_count())
+    y0, z0 = o.solve()
+    assert abs(y0 - ey) <= 5e-3 * ey and abs(z0[0] - ez) <= 2e-2 * ez, (y0, ey, z0, ez)
+
+
+# --------------------------------------------------------------------------- FD-bicubic 2-D interpolation
+# PAPER.md:406: "bicubic interpolation for 2-dimensional cases ... first and mixed derivatives
+# ... approximated using finite difference schemes of the fourth order of accuracy (central,
+# forward and backward) ... a matrix vector multiplication ... for each point".
+
+def test_fd_weights_are_the_fourth_order_stencils(oracle_mod):
+    """The 5-point derivative weights (Fornberg's tables): central (1, -8, 0, 8, -1)/12, one-sided
+    (-25, 48, -36, 16, -3)/12 and (-3, -10, 18, -6, 1)/12; derivatives exact on quartics (also at
+    the ends) and 4th order on a quintic (error ratio ~16 per halving of h)."""
+    assert np.allclose(oracle_mod.fd_weights([-2, -1, 0, 1, 2]) * 12, [1, -8, 0, 8, -1], atol=1e-13)
+    assert np.allclose(oracle_mod.fd_weights([0, 1, 2, 3, 4]) * 12, [-25, 48, -36, 16, -3], atol=1e-12)
+    assert np.allclose(oracle_mod.fd_weights([-1, 0, 1, 2, 3]) * 12, [-3, -10, 18, -6, 1], atol=1e-12)
+    x = np.linspace(-1.0, 2.0, 13)
+    assert np.max(np.abs(oracle_mod.fd_deriv(x ** 4 - 2 * x ** 3 + x, x[1] - x[0]) - (4 * x ** 3 - 6 * x ** 2 + 1))) <= 1e-12
+    errs = []
+    for n in (17, 33):
+        x = np.linspace(0.0, 1.0, n)
+        errs.append(np.max(np.abs(oracle_mod.fd_deriv(x ** 5, x[1] - x[0]) - 5 * x ** 4)))
+    assert 12 < errs[0] / errs[1] < 40
+
+
+def test_bicubic_reproduces_bicubic_polynomials(oracle_mod):
+    """With f = x1^3 x2^2 + x1 x2 the 4th-order differences are exact (degree <= 4 per axis), so
+    the 16-coefficient cells reproduce f at random points (SPEC examples: xy reproduced, corner
+    value = sample), inside and outside the box (clamped)."""
+    from paper_1909_13560_b200 import workloads as W
+    spec = dict(W.heat_poly(2, 1, N=2, P=9, T=0.25, box=2.0, L=2), npts=[9, 13], xlo=[-2.0, -1.0],
+                xhi=[2.0, 3.0], interp="fd_bicubic")
+    spec["terminal_params"] = [0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 1.0, 0.0]       # x1^3 * x2^2
+    o = oracle_mod.Oracle(spec, nthreads=1)
+    rng = np.random.Generator(np.random.PCG64(1909135600))
+    for _ in range(100):
+        x = [rng.uniform(-2.5, 2.5), rng.uniform(-1.5, 3.5)]
+        xc = np.clip(x, [-2.0, -1.0], [2.0, 3.0])
+        v = o.eval_newest(x)
+        assert abs(v[0] - xc[0] ** 3 * xc[1] ** 2) <= 1e-12 * 72
+        assert abs(v[1] - 3 * xc[0] ** 2 * xc[1] ** 2) <= 1e-11 * 108      # z_1 = d/dx1 of g
+        assert abs(v[2] - 2 * xc[0] ** 3 * xc[1]) <= 1e-11 * 48
+
+
+def test_P6_heat_polynomial_exact_2d_bicubic(oracle_mod):
+    """P6 with the FD-bicubic interpolation: g = x1^3 x2 is in the bicubic space and its FD
+    derivatives are exact, so every K reproduces y = x1^3 x2 + 3 x1 x2 (T-t) away from the edge."""
+    from paper_1909_13560_b200 import workloads as W
+    spec = dict(W.heat_poly(2, 3, N=5, P=65, T=0.25, box=16.0, L=8), interp="fd_bicubic")
+    o = oracle_mod.Oracle(spec, nthreads=os.cpu_count())
+    o.solve()
+    x = np.linspace(-16, 16, 65)
+    X1, X2 = np.meshgrid(x, x, indexing="ij")
+    m = (np.abs(X1) <= 5) & (np.abs(X2) <= 5)
+    assert np.max(np.abs(o.layer(0)[m] - (X1 ** 3 * X2 + 0.75 * X1 * X2)[m])) <= 1e-12 * 625
+    assert np.max(np.abs(o.layer(1)[m] - (3 * X1 ** 2 * X2 + 0.75 * X2)[m])) <= 1e-12 * 375
+
+
+@pytest.mark.parametrize("row", [r for r in _rows("ex4", 16)], ids=lambda r: f"ex4_K{r[1]}_N{r[2]}")
+def test_P10_printed_rows_2d_bicubic(oracle_mod, row):
+    """Table 9 was computed with the FD-bicubic interpolation: the oracle's
+    bicubic path reproduces the gated printed rows within 3 % (y and Euclidean z, reading R15)."""
+    from paper_1909_13560_b200 import workloads as W
+    spec = dict(W.ex4_2d(int(row[1]), int(row[2])), interp="fd_bicubic")
+    o = oracle_mod.Oracle(spec, nthreads=os.cpu_count())
+    y0, z0 = o.solve()
+    _check_row(row, abs(y0), float(np.linalg.norm(np.asarray(z0) - 1.0)))
