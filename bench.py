@@ -29,20 +29,33 @@ sys.path.insert(0, ROOT)
 METRIC = "grid-point·time-step updates/s (fp64) + time-to-solution at fixed error vs host oracle"
 UNIT = "updates/s"
 KS = [1, 2, 3, 4, 5, 6]
-# Algorithmic FP64 flops per point-step of the fused kernel:
-#   per tap: 2 fields x 4 FMA (16) + driver diff-rates (8) + accumulations (6)   = 30
-#   per point: K*L taps, + 2 per tap at j = Ky (E[y]), Picard 30 x (8 + 2)       = 300
-#   spline of the new level: 2 fields x 21                                       = 42
-FLOP_TAP, FLOP_PICARD, FLOP_SPLINE = 30, 300, 42
+P_CFG2, N_CFG2, L_CFG2 = 65536, 256, 16
 
 
-def flops_per_point_step(K, L=16):
-    return K * L * FLOP_TAP + L * 2 + FLOP_PICARD + FLOP_SPLINE
+def survey_ops(K, L, d, F_f, p=30.0):
+    """Algorithmic FP64 work per point-step, SURVEY.md §8(d) as written (FMA = 1 op):
+    K L^d (F 4^d + F_f + 2d + 1) + p (F_f + 2) + 2 K d + 10 F,  F = 1 + d.
+    F_f: FP64 ops of one driver evaluation (differential rates 1-D: 5)."""
+    F = 1 + d
+    return K * L ** d * (F * 4 ** d + F_f + 2 * d + 1) + p * (F_f + 2) + 2 * K * d + 10 * F
 
 
-def peak_fp64_tflops(sm_mhz=1965.0, nsm=148):
-    # B200: 64 FP64 FMA per clock per SM (B200_PROFILING.md / SURVEY A.4), 2 flops per FMA
-    return nsm * 64 * 2 * sm_mhz * 1e6 / 1e12
+def fp64_pipe_peak(sm_mhz=1965.0, nsm=148):
+    """FP64 pipe ops/s (FMA = 1 op): 148 SM x 64 DFMA lanes per clock (B200_PROFILING.md: 148 SMs,
+    1965 MHz max; the 64 DFMA/clk/SM of sm_100 confirmed by ncu's
+    sm__sass_thread_inst_executed_op_dfma_pred_on.avg.peak_sustained), in units of 1e12."""
+    return nsm * 64 * sm_mhz * 1e6 / 1e12
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def _dist():
@@ -134,25 +147,27 @@ def run_ours(args):
         res = solve_batch(ss)
         t = res[0].t_sweep_s
         upd = sum(r.updates for r in res)
+        pexec = sum(r.picard_iters for r in res)
         # one batched launch is counted by every context; the rest are the y0 evaluations
         launches = 1 + sum(s.kernel_launches - a - 1 for s, a in zip(ss, n0))
         y0 = {K: (r.y0, r.z0[0]) for K, r in zip(KS, res)}
         for s in ss:
             s.close()
-        return t, upd, launches, y0
+        return t, upd, launches, y0, pexec
 
     for _ in range(args.warmup):
         one_step()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    times, upds, launches = [], 0, 0
+    times, upds, launches, pexecs = [], 0, 0, 0
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
-            t, u, nl, y0 = one_step()
+            t, u, nl, y0, pe = one_step()
             times.append(t)
             upds += u
             launches += nl
+            pexecs += pe
     torch.cuda.synchronize()
     elapsed = sum(times)
     if dist:
@@ -161,38 +176,48 @@ def run_ours(args):
         elapsed = float(tt.item())
     value = upds * world / elapsed
 
-    # ---- the dominant kernel is quad1d_fused: ONE persistent launch per bench step runs all
-    # six sweeps (round-robin over the problems).  Its average duration is the CUDA-event time
-    # of the launches of the timed region (recorded on `stream` inside bsde_solve_batch).
+    # ---- roofline of the dominant kernel, quad1d_fused: ONE persistent launch per bench step runs
+    # all six sweeps (round-robin over the problems); its average duration is the CUDA-event time of
+    # the launches of the timed region (recorded on `stream` inside bsde_solve_batch).  Algorithmic
+    # work: SURVEY §8(d)'s per-point-step FP64 op count as written (FMA = 1 op, p = 30 Picard
+    # iterations, differential-rates driver F_f = 5) x the point-steps of one launch.
     launch_s = elapsed / args.steps
-    fl = sum(flops_per_point_step(K) * 65536 * (256 - K + 1) for K in KS)
+    pts = {K: P_CFG2 * (N_CFG2 - K + 1) for K in KS}
+    ops = sum(survey_ops(K, L_CFG2, 1, 5) * pts[K] for K in KS)
+    p_exec = pexecs / max(args.steps, 1) / sum(pts.values())          # mean executed Picard iterations
+    ops_exec = sum(survey_ops(K, L_CFG2, 1, 5, p=p_exec) * pts[K] for K in KS)
     clocks = clk.summary()
-    peak = peak_fp64_tflops(1965.0)
-    achieved = fl / launch_s / 1e12
+    peak = fp64_pipe_peak(1965.0)
+    achieved = ops / launch_s / 1e12
     traffic = None
-    try:   # dram__bytes_read.sum + dram__bytes_write.sum (MB) per launch, from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "round1", "ncu_quad1d_fused_batch_summary.json")) as fh:
-            prof = json.load(fh)
-        traffic = (float(prof["dram__bytes_read.sum"]) + float(prof["dram__bytes_write.sum"])) * 1e6
-    except (OSError, KeyError, ValueError):
-        pass
-    roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
+    prof = _load_profile("ncu_quad1d_fused_batch_summary.json")
+    if prof:   # dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu --set full capture
+        traffic = _dram_bytes(prof)
+    roof = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "traffic_note": "DRAM bytes per launch (six sweeps; state is L2-resident) from ncu --set full",
+            "unit_note": "FP64-pipe ops/s, FMA = 1 op (SURVEY §8(d) convention); peak = 148 SM x 64 DFMA lanes/clk "
+                         "x 1965 MHz (B200_PROFILING.md SM count and max clock; no FP64 figure in MEASURED_PEAKS.json)",
             "kernel": "quad1d_fused<DRV_DIFF>: one launch = the 6 sweeps K=1..6 (1521 steps)",
-            "flops_per_launch": fl, "launch_us": round(launch_s * 1e6, 3),
-            "peak_note": "FP64 pipe: 148 SM x 64 DFMA/clk x 2 x 1965 MHz (derived; DESIGN.md Roofline)"}
+            "ops_per_launch": ops, "launch_us": round(launch_s * 1e6, 3),
+            "ops_formula": "K L (F 4 + F_f + 2d + 1) + p (F_f + 2) + 2 K d + 10 F, d=1, F=2, F_f=5, L=16, p=30",
+            "executed_picard": {"mean_iterations": round(p_exec, 3),
+                                "frac": round(ops_exec / launch_s / 1e12 / peak, 4),
+                                "note": "the same formula with p = the Picard iterations the kernel executed "
+                                        "(it leaves the loop at an exact fixed point; bsde_result.picard_iters)"},
+            "traffic_note": "DRAM bytes per launch (the state is L2-resident) from ncu --set full, profiles/round2"}
+    if clocks.get("sm_mhz"):
+        roof["frac_at_sampled_clock"] = round(achieved / fp64_pipe_peak(float(clocks["sm_mhz"])), 4)
     try:   # the same denominator measured: a DFMA-chain kernel of the library (bsde_measure_fp64_peak)
         from paper_1909_13560_b200 import measure_fp64_peak
         mp = measure_fp64_peak(dev)
-        roof["peak_measured"] = {"value": round(mp["tflops"], 2), "unit": "TFLOP/s",
-                                 "frac_of_measured": round(achieved / mp["tflops"], 4),
+        roof["peak_measured"] = {"value": round(mp["tflops"] / 2, 3), "unit": "T op/s (FMA = 1)",
+                                 "frac_of_measured": round(achieved / (mp["tflops"] / 2), 4),
                                  "note": "16 independent DFMA chains/thread, 8 x 256-thread CTAs per SM"}
     except Exception as exc:  # noqa: BLE001 -- reported, never fatal for the bench line
         roof["peak_measured"] = {"error": str(exc)}
 
     # ---- e2e: setup (host config -> device) + sweep + final layers device -> host, host clock
-    host = np.empty(65536, dtype=np.float64)
+    host = np.empty(P_CFG2, dtype=np.float64)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e2e_upd, h2d, d2h = 0, 0, 0
@@ -204,7 +229,7 @@ def run_ours(args):
             s.layer(1, out=host)
             e2e_upd += r.updates
             h2d += K * 16 * 72 + 2 * 16 * 8 + 1024          # tap table + GL rule + config/params
-            d2h += 2 * 65536 * 8 + 32                        # y, z of layer 0 + y0/z0
+            d2h += 2 * P_CFG2 * 8 + 32                      # y, z of layer 0 + y0/z0
             s.close()
     torch.cuda.synchronize()
     e2e_t = time.perf_counter() - t0
@@ -220,14 +245,19 @@ def run_ours(args):
            "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": "cfg2: 1-D differential-rates call, P=65536, N=256, L=16, K=1..6 (one step = the six sweeps in one bsde_solve_batch launch)",
-                      "global_batch": 65536 * world, "seq_len": 256, "parallelism": f"replicas{world}",
+                      "global_batch": P_CFG2 * world, "seq_len": N_CFG2, "parallelism": f"replicas{world}",
                       "l2": "flushed (512 MiB write) before every step; the six sweeps' state (~50 MiB) is L2-resident by design"},
            "roofline": roof, "e2e": e2e, "gpu_launches": launches // max(args.steps, 1),
            "clocks": clocks,
-           "accuracy": {str(K): {"y0": y0[K][0], "z0": y0[K][1]} for K in KS},
+           "accuracy": {str(K): {"y0": y0[K][0], "z0": y0[K][1],
+                                 "note": "K >= 3 at P = 2^16, L = 16 is linearly unstable (DESIGN.md R25); see cfg2_stable"}
+                        for K in KS},
            "reference_solution": list(W.reference_solution(specs[1])[:1]) + [W.reference_solution(specs[1])[1][0]]}
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0 and world == 1:
+        out["cfg2_stable"] = cfg2_stable(dev, stream)
+        out["cfg1_latency"] = cfg1_latency(dev, stream)
     if rank == 0 and not args.no_tts:
         out["tts"] = tts_sweep(dev)
     if rank == 0 and world == 1 and not args.no_d23:
@@ -237,6 +267,69 @@ def run_ours(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+PROFILE_DIRS = ("round2", "round1")
+
+
+def _load_profile(name):
+    for d in PROFILE_DIRS:
+        try:
+            with open(os.path.join(ROOT, "profiles", d, name)) as fh:
+                return json.load(fh)
+        except (OSError, ValueError):
+            continue
+    return None
+
+
+def _dram_bytes(prof):
+    """dram__bytes_read.sum + dram__bytes_write.sum of an ncu summary, in bytes."""
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(prof[k]) * scale.get(prof.get(k + ".unit", "byte"), 1.0)
+        return tot
+    except (KeyError, ValueError):
+        return None
+
+
+def cfg2_stable(dev, stream):
+    """The stable companion of cfg 2 (R25): the same problem at P = 16385 (stable for
+    every K with L = 16), all six sweeps in one batched launch: throughput and accuracy per K."""
+    from paper_1909_13560_b200 import Solver, solve_batch, workloads as W
+    P = 16385
+    specs = [dict(W.diff_rates(K, N=N_CFG2, P=P), name=f"cfg2_stable_K{K}") for K in KS]
+    ref = W.reference_solution(specs[0])
+    best, acc = None, None
+    for _ in range(3):
+        ss = [Solver(sp, device=dev, stream=stream) for sp in specs]
+        res = solve_batch(ss)
+        t = res[0].t_sweep_s
+        if best is None or t < best[0]:
+            best = (t, sum(r.updates for r in res))
+            acc = {str(K): {"y0_err": abs(r.y0 - ref[0]), "z0_err": abs(r.z0[0] - ref[1][0])} for K, r in zip(KS, res)}
+        for s in ss:
+            s.close()
+    return {"workload": "cfg2 shape at P=16385 (stable for all K, DESIGN.md R25), N=256, L=16, K=1..6 batched",
+            "ms": best[0] * 1e3, "updates_per_s": best[1] / best[0], "accuracy": acc}
+
+
+def cfg1_latency(dev, stream):
+    """BASELINE cfg 1 (Black-Scholes, P=256, K=2, N=32, L=8) as a latency path: device time of
+    the sweep (bsde_solve) and wall time of setup + solve, best of 5."""
+    from paper_1909_13560_b200 import Solver, workloads as W
+    spec = W.cfg1()
+    sweep, wall = 1e9, 1e9
+    for _ in range(5):
+        t0 = time.perf_counter()
+        with Solver(spec, device=dev, stream=stream) as s:
+            r = s.solve()
+            launches = s.kernel_launches
+        wall = min(wall, time.perf_counter() - t0)
+        sweep = min(sweep, r.t_sweep_s)
+    return {"workload": spec["name"], "sweep_us": sweep * 1e6, "setup_plus_solve_ms": wall * 1e3,
+            "kernel_launches": launches, "y0": r.y0}
 
 
 TTS_NS = [16, 32, 64, 128, 256, 512, 1024]
@@ -309,32 +402,69 @@ def tts_sweep(dev, oracle_budget_s=90.0):
             "oracle_cores": nthreads, "results": out}
 
 
-# algorithmic FP64 flops per point-step of the d >= 2 configs (separable evaluation, FMA = 2;
-# DESIGN.md §5): per tap F x 4 FMA (last axis) + the staged row/plane passes' share + driver +
-# accumulation, K L^d taps, + Picard + spline passes
-FLOPS_CFG4 = 4 * 64 * (24 + 3 + 6 + 10) + 2 * 64 + 30 * 8 + 3 * 2 * 21
-FLOPS_CFG5 = 3 * 512 * (32 + 4 + 18 + 14) + 2 * 512 + 30 * 22 + 4 * 3 * 21
-# cfg 4 through the affine separable path (aff2.cuh): per level and field an axis-0 operator
-# (L x (4 interpolation + 2 accumulation) FMA per output) and three axis-1 operators (L x (8 + 3)
-# FMA per point) + the combination (6 FMA); Picard 30 x 4 FMA; splines as above
-FLOPS_CFG4_AFF = 2 * (4 * 3 * (6 * 8 + 11 * 8 + 6) + 30 * 4) + 3 * 2 * 21
-# cfg 5 through the decomposed differential-rates path: per level the per-tap part on U alone
-# (L^3 x (4 interpolation FMA + 1 add for 2 max(U, 0) + 2 accumulation FMA; the pair weights
-# are applied once per (l0, l1)) + row-pass and plane-stack shares) and the separable affine
-# part (3 axis passes over 5 / 6 / 7 arrays); Picard 30 x 22; splines 4 fields x 3 axes x 21
-FLOPS_CFG5_DEC = 3 * (13 * 512 + 683 + 320 + 197 * 8 + 12) + 30 * 22 + 4 * 3 * 21
+# Per-kernel rooflines of the d >= 2 configs (committed ncu --set full summaries, profiles/round2):
+# FP64-pipe kernels report ncu's sm__pipe_fp64_cycles_active (the executed FP64 work per cycle),
+# HBM kernels their algorithmic bytes (8 B read + 8 B write per point, field and pass) / duration
+# against MEASURED_PEAKS.json's copy bandwidth.
+D23_KERNELS = {
+    "cfg4": [("aff_rows", "ncu_aff_rows_cfg4_summary.json", "alu"),
+             ("spline_pass<4>", "ncu_spline_pass4_cfg4_summary.json", "hbm"),
+             ("spline_pass<1>", "ncu_spline_pass1_cfg4_summary.json", "hbm")],
+    "cfg5": [("quad3d<DRV_DIFF,1>", "ncu_quad3d_dec_cfg5_summary.json", "alu"),
+             ("spline_pass<4>", "ncu_spline_pass4_cfg5_summary.json", "hbm")],
+}
+
+
+def _hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "B200_PROFILING.md fallback"
+
+
+def kernel_rooflines(cfg, points):
+    out = []
+    hbm, hbm_src = _hbm_peak()
+    for kname, fname, bound in D23_KERNELS.get(cfg, []):
+        prof = _load_profile(fname)
+        if not prof:
+            out.append({"kernel": kname, "profile": None, "note": f"profiles/round2/{fname} not captured"})
+            continue
+        dur = float(prof["gpu__time_duration.sum"]) * {"ms": 1e-3, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3,
+                                                         "ns": 1e-9, "nsecond": 1e-9}.get(prof.get("gpu__time_duration.sum.unit", "ms"), 1e-3)
+        ent = {"kernel": kname, "launch_us": dur * 1e6, "traffic": _dram_bytes(prof), "profile": fname}
+        if bound == "alu":
+            pct = float(prof["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"])
+            ent.update({"bound": "alu", "frac": round(pct / 100.0, 4), "unit": "TFLOP/s",
+                        "peak": round(fp64_pipe_peak(), 3),
+                        "achieved": round(pct / 100.0 * fp64_pipe_peak(), 3),
+                        "note": "executed FP64-pipe utilisation of the launch (ncu sm__pipe_fp64_cycles_active, "
+                                "FMA = 1 op)"})
+        else:
+            alg = points * 16.0                       # 8 B read + 8 B write per point of one field-pass
+            ach = alg / dur / 1e9
+            ent.update({"bound": "hbm", "unit": "GB/s", "achieved": round(ach, 1), "peak": hbm,
+                        "frac": round(ach / hbm, 4), "peak_source": hbm_src,
+                        "note": "algorithmic bytes of one field-pass (16 B per point) / ncu duration"})
+        out.append(ent)
+    return out
 
 
 def d23_configs(dev, stream):
     """cfg 4 and cfg 5 at their full sizes: device time of backward steps (after one warm-up
-    step) through bsde_step, with the FP64 fraction of the derived peak.  Setup untimed."""
+    step) through bsde_step, the survey's direct-stencil op count per point-step over that time,
+    and the per-kernel rooflines of the committed ncu captures.  Setup untimed."""
     import torch
     from paper_1909_13560_b200 import Solver, workloads as W
     out = {}
-    for name, spec, steps, fl, kv in (("cfg4", W.cfg4(), 3, FLOPS_CFG4_AFF, 0),
-                                      ("cfg4_per_tap", W.cfg4(), 3, FLOPS_CFG4, 2),
-                                      ("cfg5", W.basket_3d(3, 64, 8, P=512), 2, FLOPS_CFG5_DEC, 0),
-                                      ("cfg5_per_tap", W.basket_3d(3, 64, 8, P=512), 2, FLOPS_CFG5, 2)):
+    runs = (("cfg4", W.cfg4(), 3, 0, 3, "default: affine separable path (aff2.cuh)"),
+            ("cfg4_per_tap", W.cfg4(), 3, 2, 3, "per-tap quad2d"),
+            ("cfg4_fd_bicubic", dict(W.cfg4(), interp="fd_bicubic"), 1, 0, 3,
+             "the paper's FD-bicubic interpolation (bicubic.cuh, one thread per point)"),
+            ("cfg5", W.basket_3d(3, 64, 8, P=512), 2, 0, 9, "default: decomposed driver (quad3d on U + separable affine part)"),
+            ("cfg5_per_tap", W.basket_3d(3, 64, 8, P=512), 1, 2, 9, "per-tap quad3d"))
+    for name, spec, steps, kv, F_f, path in runs:
         with Solver(spec, device=dev, stream=stream, kernel_variant=kv) as s:
             npts = 1
             for n in s.shape:
@@ -348,47 +478,62 @@ def d23_configs(dev, stream):
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / steps
         ups = npts / (ms * 1e-3)
-        out[name] = {"workload": spec["name"], "points": npts, "ms_per_step": ms, "updates_per_s": ups,
-                     "path": {0: "default" + (" (affine separable, aff2.cuh)" if name == "cfg4"
-                                              else " (decomposed driver: quad3d on U + separable affine part)"),
-                              2: "per-tap " + ("quad2d" if name.startswith("cfg4") else "quad3d")}[kv],
-                     "flops_per_point_step": fl, "tflops": fl * ups / 1e12,
-                     "frac_fp64_peak": fl * ups / 1e12 / peak_fp64_tflops(1965.0)}
+        d = spec["d"]
+        K = max(spec["Ky"], spec["Kz"])
+        ops = survey_ops(K, spec["L"], d, F_f)
+        out[name] = {"workload": spec["name"], "points": npts, "ms_per_step": ms, "updates_per_s": ups, "path": path,
+                     "survey_ops_per_point_step": ops,
+                     "survey_ops_frac": round(ops * ups / 1e12 / fp64_pipe_peak(), 4),
+                     "survey_ops_note": "SURVEY §8(d) direct-stencil op count / step time / FP64-pipe peak; the "
+                                        "separable paths execute fewer ops than the direct form (can exceed 1)"}
+        if name in D23_KERNELS:
+            out[name]["kernels"] = kernel_rooflines(name, npts)
     return out
 
 
-def _oracle_sample(max_seconds=15.0, steps_per_K=120, nthreads=None):
-    """Time the oracle (as it stands) on a bounded sample of cfg 2: steps_per_K backward
-    steps of each K after its (untimed) setup."""
+ORACLE_STEPS_PER_K = 8      # one oracle sample: 8 backward steps of each K = 1..6 of cfg 2 (setup untimed)
+
+
+def oracle_sample(nthreads=None, steps_per_K=ORACLE_STEPS_PER_K):
+    """ONE sampling protocol for both arms: the oracle (as it stands, OpenMP over all host cores)
+    on a bounded sample of the cfg 2 workload -- steps_per_K backward steps of each K after its
+    (untimed) setup.  Returns (updates, seconds, threads)."""
     import oracle
     from paper_1909_13560_b200 import workloads as W
     nthreads = nthreads or os.cpu_count() or 1
     tot_t, tot_u = 0.0, 0
     for K in KS:
         o = oracle.Oracle(W.cfg2(K), nthreads=nthreads)
+        t0 = time.perf_counter()
         for _ in range(steps_per_K):
-            t0 = time.perf_counter()
             o.step()
-            tot_t += time.perf_counter() - t0
-            tot_u += 65536
-            if tot_t > max_seconds:
-                break
+        tot_t += time.perf_counter() - t0
+        tot_u += P_CFG2 * steps_per_K
         o.close()
-    return tot_u / tot_t, tot_u, tot_t, nthreads
+    return tot_u, tot_t, nthreads
 
 
-def cpu_baseline(args):
-    v, u, t, nt = _oracle_sample()
-    v1, u1, t1, _ = _oracle_sample(max_seconds=5.0, steps_per_K=4, nthreads=1)
-    return {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
-            "sample": f"cfg2, up to 120 backward steps per K=1..6 after untimed setup, capped at 15 s "
-                      f"({u} updates in {t:.2f} s)",
-            "one_thread": {"value": v1, "unit": UNIT, "cores": 1,
-                           "sample": f"cfg2, 4 backward steps per K=1..6 ({u1} updates in {t1:.2f} s); "
-                                     "comparable to the paper's serial CPU baseline (PAPER.md:458)"}}
+def _sample_text(n):
+    return (f"{n} sample(s) of {ORACLE_STEPS_PER_K} backward steps of each K=1..6 of cfg2 (P=65536, L=16) after "
+            f"untimed setup; host CPU: {cpu_model()}")
+
+
+def cpu_baseline(args, budget_s=10.0):
+    us, ts, n, nt = 0, 0.0, 0, 1
+    while ts < budget_s or n < 1:
+        u, t, nt = oracle_sample()
+        us, ts, n = us + u, ts + t, n + 1
+    u1, t1, _ = oracle_sample(nthreads=1, steps_per_K=1)
+    return {"value": us / ts, "unit": UNIT, "cores": nt, "kind": "oracle", "cpu_model": cpu_model(),
+            "sample": _sample_text(n) + f" ({us} updates in {ts:.2f} s)",
+            "one_thread": {"value": u1 / t1, "unit": UNIT, "cores": 1,
+                           "sample": f"1 backward step of each K, 1 thread ({u1} updates in {t1:.2f} s); comparable "
+                                     "to the paper's serial CPU baseline (PAPER.md:458)"}}
 
 
 def run_reference(args):
+    """--impl reference: the oracle, as it stands, on the host cores; each bench step is one
+    oracle sample (the protocol of cpu_baseline) of the same cfg 2 workload."""
     dist, rank, world = _dist()
     if rank != 0:
         if dist:
@@ -396,11 +541,10 @@ def run_reference(args):
             dist.destroy_process_group()
         return
     for _ in range(args.warmup):
-        _oracle_sample(max_seconds=3.0, steps_per_K=1)
-    vals, us, ts = [], 0, 0.0
+        oracle_sample(steps_per_K=1)
+    us, ts, nt = 0, 0.0, 1
     for _ in range(args.steps):
-        v, u, t, nt = _oracle_sample(max_seconds=8.0, steps_per_K=4)
-        vals.append(v)
+        u, t, nt = oracle_sample()
         us += u
         ts += t
     value = us / ts
@@ -408,9 +552,9 @@ def run_reference(args):
            "warmup": args.warmup, "ms_per_step": ts / args.steps * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": "cfg2: 1-D differential-rates call, P=65536, N=256, L=16, K=1..6",
-                      "global_batch": 65536, "seq_len": 256, "parallelism": "host cores (OpenMP)"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "kind": "oracle", "cores": os.cpu_count(),
-                            "sample": "each step: 4 backward steps of each K=1..6 of cfg2 (setup untimed)"},
+                      "global_batch": P_CFG2, "seq_len": N_CFG2, "parallelism": "host cores (OpenMP)"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "kind": "oracle", "cores": nt, "cpu_model": cpu_model(),
+                            "sample": _sample_text(args.steps)},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
     if dist:

@@ -152,6 +152,10 @@ typedef struct {
                                 the d = 1 persistent kernel)                                */
   double  t_quad_s;          /* cfg.timing = 1: quadrature + z + Picard kernels             */
   double  t_comm_s;          /* cfg.timing = 1: halo exchange (NCCL or peer copies)         */
+  int64_t picard_iters;      /* Picard iterations executed by the sweep of this call (all
+                                points; the d = 1 persistent kernel counts them, -1 otherwise).
+                                The kernel leaves the loop at an exact fixed point, where the
+                                remaining iterations of the fixed count p are identities     */
 } bsde_result;
 
 typedef struct bsde_ctx bsde_ctx;
@@ -192,6 +196,14 @@ bsde_status bsde_solve(bsde_ctx* ctx, bsde_result* res);
  * updates the context's own.  Synchronises ctxs[0]'s stream; NUMERICAL_DOMAIN as for
  * bsde_solve (first failing context).                                                 */
 bsde_status bsde_solve_batch(bsde_ctx* const* ctxs, int32_t n, bsde_result* res);
+
+/* bsde_solve_batch with an explicit CTA schedule.  mode 0: auto (= bsde_solve_batch: the
+ * problem-partitioned schedule when a plan fits, else round robin); 1: round robin (every CTA
+ * steps every problem on one tile of TP points); 2: problem-partitioned (each problem gets its
+ * own CTAs, each CTA a range of consecutive tiles whose spline is built in one pass, sized by a
+ * cost model so that all problems finish together; RESOURCE_LIMIT if no plan fits).  The
+ * arithmetic of every point is the same in every mode (bitwise identical results).        */
+bsde_status bsde_solve_batch_mode(bsde_ctx* const* ctxs, int32_t n, int32_t mode, bsde_result* res);
 
 /* index n of the newest level                                                         */
 bsde_status bsde_level(const bsde_ctx* ctx, int32_t* n_out);

@@ -29,7 +29,8 @@ INTERPS = {"spline": 0, "fd_bicubic": 1}
 EXPORTS = ["bsde_query_workspace", "bsde_setup", "bsde_step", "bsde_solve", "bsde_level", "bsde_get_layer",
            "bsde_get_picard_counts", "bsde_query_grid", "bsde_query_taps", "bsde_eval", "bsde_layer_device_ptr",
            "bsde_query_partition", "bsde_query_partition_cfg", "bsde_nccl_unique_id", "bsde_group_step",
-           "bsde_group_solve", "bsde_solve_batch", "bsde_kernel_launches", "bsde_measure_fp64_peak",
+           "bsde_group_solve", "bsde_solve_batch", "bsde_solve_batch_mode", "bsde_kernel_launches",
+           "bsde_measure_fp64_peak",
            "bsde_last_error", "bsde_destroy"]
 
 
@@ -58,7 +59,7 @@ class bsde_result(C.Structure):
     _fields_ = [("y0", C.c_double), ("z0", C.c_double * 3), ("t_setup_s", C.c_double),
                 ("t_sweep_s", C.c_double), ("t_total_s", C.c_double), ("updates", C.c_int64),
                 ("picard_max_used", C.c_int32), ("t_bootstrap_s", C.c_double), ("t_spline_s", C.c_double),
-                ("t_quad_s", C.c_double), ("t_comm_s", C.c_double)]
+                ("t_quad_s", C.c_double), ("t_comm_s", C.c_double), ("picard_iters", C.c_int64)]
 
 
 _lock = threading.Lock()
@@ -92,6 +93,7 @@ def load_library(path: str = LIB_PATH):
             lib.bsde_group_step.argtypes = [C.POINTER(C.c_void_p), I32]
             lib.bsde_group_solve.argtypes = [C.POINTER(C.c_void_p), I32, C.POINTER(bsde_result)]
             lib.bsde_solve_batch.argtypes = [C.POINTER(C.c_void_p), I32, C.POINTER(bsde_result)]
+            lib.bsde_solve_batch_mode.argtypes = [C.POINTER(C.c_void_p), I32, I32, C.POINTER(bsde_result)]
             lib.bsde_measure_fp64_peak.argtypes = [I32, I32, D, D]
             lib.bsde_last_error.argtypes = [P]
             lib.bsde_last_error.restype = C.c_char_p
@@ -299,14 +301,15 @@ class Solver:
         return int(n.value)
 
 
-def solve_batch(solvers) -> list:
-    """``bsde_solve_batch``: the remaining steps of several independent d = 1 Solvers (same
-    grid, driver and device) in one persistent launch with round-robin steps."""
+def solve_batch(solvers, mode: int = 0) -> list:
+    """``bsde_solve_batch_mode``: the remaining steps of several independent d = 1 Solvers (same
+    grid, driver and device) in one persistent launch; mode 0 auto, 1 round robin, 2
+    problem-partitioned CTAs."""
     lib = load_library()
     n = len(solvers)
     arr = (C.c_void_p * n)(*[s._h for s in solvers])
     res = (bsde_result * n)()
-    st = lib.bsde_solve_batch(arr, n, res)
+    st = lib.bsde_solve_batch_mode(arr, n, int(mode), res)
     if st != BSDE_OK:
         raise BsdeError(st, lib.bsde_last_error(None).decode() or
                         " | ".join(lib.bsde_last_error(s._h).decode() for s in solvers))

@@ -91,6 +91,7 @@ struct StepArgs {
   int32_t* picard;         // out: npts
   unsigned long long* bad; // first non-finite output: min of bad_key(n, point) (bsde_internal.h)
   int32_t n;               // index of the level this step computes (ring_mode 0 launches)
+  unsigned long long* picard_exec;   // optional: + the Picard iterations executed (fused 1-D kernel)
   unsigned long long* phase_ns;  // optional (debug): per-CTA %globaltimer stamps of the fused kernel
 };
 
@@ -138,6 +139,7 @@ struct Persist1D {
 // 0, 1, ..., then step it + 1), so a problem's neighbour waits overlap the other problems'
 // work.  A single solve is a batch of one.
 constexpr int kMaxBatch = 8;
+constexpr int kFlagCap = 8192;   // progress flags per kind and context (the workspace holds 2 x kFlagCap)
 struct FusedProb {
   StepArgs s;
   Persist1D pp;

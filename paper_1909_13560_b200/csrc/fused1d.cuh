@@ -116,6 +116,12 @@ struct FusedBatch {
   const unsigned char* arena;   // global address of the constant tap arena (bulk-copy source)
   int nprob, max_steps;
   FusedProb prob[kMaxBatch];
+  // problem-partitioned mode (part = 1): CTAs [cta0[ip], cta0[ip+1]) serve problem ip alone,
+  // each a range of ns[ip] consecutive tiles of TP points (sub-tiles, pass 1) whose spline is
+  // built in one pass 2; round-robin mode (part = 0): every CTA serves every problem on one tile
+  int part;
+  int cta0[kMaxBatch + 1];
+  int ns[kMaxBatch];
 };
 
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
@@ -169,13 +175,14 @@ __device__ __forceinline__ void wait_flags(const unsigned* flag, unsigned* mk, i
 // would cost one round trip each); one acquire fence afterwards orders every later access
 // of the CTA (after the barrier that follows) behind them.
 template <int KIND>   // 0: ring flags (short range D[1]), 1: done flags (short range D[0])
-__device__ __forceinline__ void refresh_marks(const FusedProb* prob, int nprob, int it, unsigned* marks, int b, int nb) {
+__device__ __forceinline__ void refresh_marks(const FusedProb* prob, int nprob, int it, unsigned* marks, int b, int nb,
+                                              int only) {
   const int lane = threadIdx.x & 31;
   unsigned v[kMaxBatch];
 #pragma unroll
   for (int ip = 0; ip < kMaxBatch; ++ip) {
     v[ip] = 0xffffffffu;
-    if (ip < nprob && it < prob[ip].pp.nsteps) {
+    if (ip < nprob && it < prob[ip].pp.nsteps && (only < 0 || ip == only)) {
       const Persist1D& pp = prob[ip].pp;
       const int q = b - pp.DK + lane;
       if (2 * pp.DK + 1 <= 32 && lane <= 2 * pp.DK && q >= 0 && q < nb)
@@ -184,7 +191,7 @@ __device__ __forceinline__ void refresh_marks(const FusedProb* prob, int nprob, 
   }
 #pragma unroll
   for (int ip = 0; ip < kMaxBatch; ++ip) {
-    if (ip >= nprob || it >= prob[ip].pp.nsteps || 2 * prob[ip].pp.DK + 1 > 32) continue;
+    if (ip >= nprob || it >= prob[ip].pp.nsteps || 2 * prob[ip].pp.DK + 1 > 32 || (only >= 0 && ip != only)) continue;
     const Persist1D& pp = prob[ip].pp;
     const int Dn = KIND ? pp.D[0] : pp.D[1];
     const int d = lane - pp.DK;
@@ -293,14 +300,26 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   const int chunk = warp / NWPG, pg = warp % NWPG;
   const int P = (int)g.P[0];
   const int TP = fz.TP;
-  const int bid = blockIdx.x, nb = gridDim.x;
-  const int lo = bid * TP;
-  const int hi = min(lo + TP, P);
+  // this CTA: problem ipc (part mode; -1: every problem), its index bid among the nb CTAs that
+  // serve that problem (the index of its progress flags), and its range [clo, chi) of nsub tiles
+  int ipc = -1, bid = blockIdx.x, nb = gridDim.x, nsub = 1;
+  if (bt.part) {
+    ipc = 0;
+    while (ipc + 1 < bt.nprob && (int)blockIdx.x >= bt.cta0[ipc + 1]) ++ipc;
+    bid = blockIdx.x - bt.cta0[ipc];
+    nb = bt.cta0[ipc + 1] - bt.cta0[ipc];
+    nsub = bt.ns[ipc];
+  }
+  const int clo = bid * nsub * TP;
+  const int chi = min(clo + nsub * TP, P);
+  const int nunit_sub = (chi - clo + TP - 1) / TP;   // non-empty tiles of the range
+  int lo = clo;                                      // the current tile [lo, hi) (pass 1)
+  int hi = min(lo + TP, chi);
   const int li0 = (pg * 32 + lane) * R;              // first local point of this lane
-  const bool active = lo + li0 < hi;
+  bool active = lo + li0 < hi;
   const int H = kPcrHalo;
   // coefficients this CTA owns (c indices k = storage - 1) and the PCR extent around them
-  const int k0 = lo == 0 ? -1 : lo, k1 = hi == P ? P + 1 : hi;
+  const int k0 = clo == 0 ? -1 : clo, k1 = chi == P ? P + 1 : chi;
   const int base = k0 - 4 - H;
   const int Wa = (k1 - k0) + 8 + 2 * H;
   // values window [va, vb] of both fields (clamped to the grid); the grid is long enough
@@ -313,6 +332,8 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   // progress marks of the neighbours' flags, 4 per problem: ring (short range, DK), done
   // (short range, DK); see wait_flags
   unsigned* const marks = reinterpret_cast<unsigned*>(smem_raw + 64);
+  unsigned long long* const pcnt = reinterpret_cast<unsigned long long*>(smem_raw + 192);   // per problem
+  if (tid < kMaxBatch) pcnt[tid] = 0;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -340,20 +361,31 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   grid_dep_wait();            // previous kernel in the stream has completed
   __syncthreads();
   uint32_t ph[4] = {0, 0, 0, 0};
+  unsigned pexec = 0;         // Picard iterations this thread executed in the current problem-step
   int prefetched = 0;         // windows of the current problem already in flight
   // the warp that issues the next problem's copies during the epilogue: one without points
   // (its lanes would otherwise idle through the Picard iterations), else warp 0.  It touches
   // the flag marks only between CTA barriers that separate it from warp 0's waits.
-  const int iw = (hi - lo <= NT - 32) ? NT / 32 - 1 : 0;
+  const int iw = (TP <= NT - 32) ? NT / 32 - 1 : 0;
   bool taps_in = false;       // its tap table is in flight
+  // work units of a round: round-robin mode one per problem (the CTA's tile), part mode one per
+  // tile of the CTA's range (its one problem)
+  const int nunits = bt.part ? nunit_sub : bt.nprob;
+  const int it_end = bt.part ? PB[ipc].pp.nsteps : bt.max_steps;
+  auto unit_prob = [&](int u) { return bt.part ? ipc : u; };
+  auto unit_lo = [&](int u) { return bt.part ? clo + u * TP : clo; };
 
-  for (int it = 0; it < bt.max_steps; ++it) {
-    // ================= pass 1: levels K..1, z and Picard of step it of every problem
-    if (warp == 0 && it > 0) refresh_marks<0>(PB, bt.nprob, it, marks, bid, nb);
-    for (int ip = 0; ip < bt.nprob; ++ip) {
+  for (int it = 0; it < it_end; ++it) {
+    // ================= pass 1: levels K..1, z and Picard of step it of every problem / tile
+    if (warp == 0 && it > 0) refresh_marks<0>(PB, bt.nprob, it, marks, bid, nb, ipc);
+    for (int un = 0; un < nunits; ++un) {
+      const int ip = unit_prob(un);
       const FusedProb& fp = PB[ip];
       const Persist1D& pp = fp.pp;
       if (it >= pp.nsteps) continue;
+      lo = unit_lo(un);
+      hi = min(lo + TP, chi);
+      active = lo + li0 < hi;
       const StepArgs& s = fp.s;
       const int it_stamp = it;
       PHASE_STAMP(0);
@@ -509,27 +541,32 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       __syncthreads();
       PHASE_STAMP(16);
       {
-        int iq = ip + 1;
-        while (iq < bt.nprob && it >= PB[iq].pp.nsteps) ++iq;
-        if (iq < bt.nprob) {
+        // the next unit of this round (next problem, or next tile of the range)
+        int uq = un + 1;
+        while (uq < nunits && it >= PB[unit_prob(uq)].pp.nsteps) ++uq;
+        if (uq < nunits) {
+          const int iq = unit_prob(uq);
+          const int lq = unit_lo(uq), hq = min(lq + TP, chi);
           if (warp == iw) {
             issue_taps(PB[iq], bt.arena, tsm, &bar[3]);
-            start_windows(PB[iq], spans + 2 * kMaxK * iq, marks + 4 * iq, it, 0, buf0, buf1, WM, bar, lo, hi,
+            start_windows(PB[iq], spans + 2 * kMaxK * iq, marks + 4 * iq, it, 0, buf0, buf1, WM, bar, lq, hq,
                           bid, nb);
           }
           prefetched = 2;
           taps_in = true;
         } else {
-          // last problem of the round: the first problem of the next round (its taps; with a
+          // last unit of the round: the first unit of the next round (its taps; with a
           // separate spline scratch also its windows of levels >= 2)
-          iq = 0;
-          while (iq < bt.nprob && it + 1 >= PB[iq].pp.nsteps) ++iq;
-          if (iq < bt.nprob) {
+          uq = 0;
+          while (uq < nunits && it + 1 >= PB[unit_prob(uq)].pp.nsteps) ++uq;
+          if (uq < nunits) {
+            const int iq = unit_prob(uq);
+            const int lq = unit_lo(uq), hq = min(lq + TP, chi);
             if (warp == iw) {
               issue_taps(PB[iq], bt.arena, tsm, &bar[3]);
               if (fz.sep)
-                start_windows_ahead(PB[iq], spans + 2 * kMaxK * iq, marks + 4 * iq, it + 1, buf0, buf1, WM, bar, lo,
-                                    hi, bid, nb);
+                start_windows_ahead(PB[iq], spans + 2 * kMaxK * iq, marks + 4 * iq, it + 1, buf0, buf1, WM, bar, lq,
+                                    hq, bid, nb);
             }
             prefetched = fz.sep ? min(2, max(0, PB[iq].s.K - 1)) : 0;   // what start_windows_ahead issued
             taps_in = true;
@@ -554,6 +591,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
           const double dy = fabs(yn - y);
           const bool fixed = (yn == y);     // exact fixed point: the remaining iterations are identities
           y = yn;
+          ++pexec;
           if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
           if (fixed) { itp = s.picard_max; break; }
         }
@@ -565,19 +603,25 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         if (!isfinite(y) || !isfinite(z)) atomicMin(s.bad, bad_key(pp.ring_mode ? pp.n0 - it : s.n, p));
       }
       PHASE_STAMP(18);
+      {   // executed Picard iterations of this problem (the roofline's executed-work figure)
+        const unsigned ex = __reduce_add_sync(0xffffffffu, pexec);
+        if (lane == 0 && ex) atomicAdd(pcnt + ip, (unsigned long long)ex);
+        pexec = 0;
+      }
       // generic-proxy accesses of the level buffers before later bulk copies into them
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       PHASE_STAMP(9);
-      if (tid == publisher) st_release(pp.done_flag + bid, (unsigned)it + 1);
+      // the problem's level n is complete on this CTA after its last unit
+      if (tid == publisher && (!bt.part || un == nunits - 1)) st_release(pp.done_flag + bid, (unsigned)it + 1);
     }
 
     // ================= pass 2: spline of every problem's new level n on this CTA's tile
-    if (warp == 0) refresh_marks<1>(PB, bt.nprob, it, marks, bid, nb);
+    if (warp == 0) refresh_marks<1>(PB, bt.nprob, it, marks, bid, nb, ipc);
     for (int ip = 0; ip < bt.nprob; ++ip) {
       const FusedProb& fp = PB[ip];
       const Persist1D& pp = fp.pp;
-      if (it >= pp.nsteps) continue;
+      if (it >= pp.nsteps || (ipc >= 0 && ip != ipc)) continue;
       const StepArgs& s = fp.s;
       const int it_stamp = it;
       int slot_out;
@@ -738,6 +782,8 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       if (tid == publisher) st_release(pp.ring_flag + bid, (unsigned)it + 1);
     }
   }
+  __syncthreads();
+  if (tid < bt.nprob && PB[tid].s.picard_exec != nullptr && pcnt[tid] != 0) atomicAdd(PB[tid].s.picard_exec, pcnt[tid]);
 }
 
 // instantiated (R, C, NT, MB = CTAs per SM) variants of the fused kernel; index 0 is the default
@@ -847,12 +893,14 @@ int fused1d_blocks_per_sm(int variant, size_t smem) {
 // one cooperative launch over nprob problems (round-robin steps); the progress flags of
 // every problem (pp.ring_flag, 2 x blocks) are cleared first
 cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& g, const Fused1D& fz, int driver_id,
-                                 int threads, int blocks, size_t smem, cudaStream_t st) {
+                                 int threads, int blocks, size_t smem, cudaStream_t st, const int* ncta,
+                                 const int* nsub) {
   if (nprob < 1 || nprob > kMaxBatch) return cudaErrorInvalidValue;
   thread_local static FusedBatch bt;     // ~6 KB: kept off the stack
   bt = FusedBatch{};
   bt.fz = fz;
   bt.g = g;
+  bt.part = ncta != nullptr;
   {
     void* a = nullptr;
     cudaError_t e = cudaGetSymbolAddress(&a, c_arena);
@@ -867,15 +915,27 @@ cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& 
   int order[kMaxBatch];
   for (int i = 0; i < nprob; ++i) order[i] = i;
   std::stable_sort(order, order + nprob, [&](int a, int b) { return probs[a].s.K > probs[b].s.K; });
+  int tot = 0;
   for (int i = 0; i < nprob; ++i) {
     bt.prob[i] = probs[order[i]];
+    if (bt.part) {
+      bt.cta0[i] = tot;
+      bt.ns[i] = nsub[order[i]];
+      tot += ncta[order[i]];
+    }
     if (bt.prob[i].pp.nsteps > bt.max_steps) bt.max_steps = bt.prob[i].pp.nsteps;
 #ifdef BSDE_DEBUG
     if (getenv("BSDE_DEBUG_NOWAIT")) bt.prob[i].pp.nowait = 1;   // timing experiments only: wrong results
     if (getenv("BSDE_DEBUG_NOPAD")) bt.prob[i].pp.nopad = 1;
 #endif
-    cudaError_t e = cudaMemsetAsync(probs[i].pp.ring_flag, 0, sizeof(unsigned) * 2 * (size_t)blocks, st);
+    // ring flags at [0, n), done flags behind them (round-robin: n = blocks; part: 8192)
+    const size_t nf = bt.part ? 2 * (size_t)kFlagCap : 2 * (size_t)blocks;
+    cudaError_t e = cudaMemsetAsync(probs[i].pp.ring_flag, 0, sizeof(unsigned) * nf, st);
     if (e != cudaSuccess) return e;
+  }
+  if (bt.part) {
+    bt.cta0[nprob] = tot;
+    if (tot != blocks) return cudaErrorInvalidValue;
   }
   switch (driver_id) {
     case DRV_ZERO: return launch_fused1d_v<DRV_ZERO>(bt, threads, blocks, smem, st);
@@ -908,5 +968,5 @@ cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem
   for (int j = 0; j <= kMaxK; ++j) fp.pp.D[j] = D[j];
   fp.pp.DK = DK;
   for (int i = 0; i < 12; ++i) fp.dp[i] = pb.dp[i];
-  return launch_fused1d_batch(&fp, 1, g, fz, pb.driver_id, threads, blocks, smem, st);
+  return launch_fused1d_batch(&fp, 1, g, fz, pb.driver_id, threads, blocks, smem, st, nullptr, nullptr);
 }

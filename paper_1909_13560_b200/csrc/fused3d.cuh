@@ -35,7 +35,7 @@ __global__ void axis0_pass(const double* __restrict__ C, double* __restrict__ A,
   const int64_t plane = g.cstride[0];
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= plane) return;
-  const int64_t i0 = blockIdx.y;                   // local storage plane = local value row
+  const int64_t i0 = g.own0 + blockIdx.y;          // owned local plane (quad3d reads only these)
   const int l = blockIdx.z;
   const AxisTap& ta = axis_taps(tap_off)[(size_t)(j - 1) * 3 * L + l];
   double Bt[4];
@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(128) axis0_u_lin(const double* __restrict__ C,
   const int64_t plane = g.cstride[0];
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= plane) return;
-  const int64_t i0 = (int64_t)blockIdx.y * RA;                   // first local plane
-  const int64_t P0 = g.P[0];
+  const int64_t i0 = g.own0 + (int64_t)blockIdx.y * RA;          // first (owned) local plane
+  const int64_t P0 = g.P[0], iend = g.own0 + g.nown0;
   const AxisTap* t0 = axis_taps(tap_off) + (size_t)(j - 1) * 3 * L;
   const double* Ce = C + e;
   double lp[RA], ls[RA], z0[RA], z1[RA], z2[RA], yy[RA];
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(128) axis0_u_lin(const double* __restrict__ C,
     }
 #pragma unroll
     for (int r = 0; r < RA; ++r)
-      if (i0 + r < P0) A[((int64_t)l * P0 + i0 + r) * plane + e] = u[r];
+      if (i0 + r < iend) A[((int64_t)l * P0 + i0 + r) * plane + e] = u[r];
   }
   // the affine part's axis-0 arrays for the owned planes: [Lf, Lf s0, z_0, z_1, z_2, y][owned][plane]
   const int64_t arr = g.nown0 * plane;
@@ -602,11 +602,12 @@ static cudaError_t launch_step3d_t(const StepArgs& s, const Grid& g, const Probl
   for (int j = 1; j <= s.K; ++j) {
     const double* C = s.ring + (int64_t)s.slot[j - 1] * s.slot_elems;
     if constexpr (NF == 1) {
-      dim3 gu((unsigned)((plane + 127) / 128), (unsigned)((g.P[0] + 7) / 8), 1);
+      // owned planes only (a slab rank's halo planes feed the stencil rows, never a stack)
+      dim3 gu((unsigned)((plane + 127) / 128), (unsigned)((g.nown0 + 7) / 8), 1);
       double* W0 = A + (int64_t)s.L * g.P[0] * plane + (int64_t)(j - 1) * 6 * g.nown0 * plane;
       axis0_u_lin<<<gu, 128, 0, st>>>(C, A, W0, g, s.tap_off, j, s.L, uc, lc);
     } else {
-      dim3 ga((unsigned)((plane + 255) / 256), (unsigned)g.P[0], (unsigned)s.L);
+      dim3 ga((unsigned)((plane + 255) / 256), (unsigned)g.nown0, (unsigned)s.L);
       axis0_pass<<<ga, 256, 0, st>>>(C, A, g, s.tap_off, j, s.L);
     }
     dim3 gq((unsigned)((g.P[2] + k3TX - 1) / k3TX), (unsigned)((g.P[1] + k3TY - 1) / k3TY), (unsigned)g.nown0);

@@ -42,7 +42,8 @@ int fused1d_blocks_per_sm(int variant, size_t smem);
 size_t fused1d_smem(Fused1D& fz);
 cudaError_t measure_fp64_peak(int device, int iters, double* tflops, double* ms_out);
 cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& g, const Fused1D& fz, int driver_id,
-                                 int threads, int blocks, size_t smem, cudaStream_t st);
+                                 int threads, int blocks, size_t smem, cudaStream_t st, const int* ncta,
+                                 const int* nsub);
 cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
 cudaError_t init_device_attributes();
 cudaError_t launch_quad2d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, cudaStream_t st);
@@ -54,6 +55,10 @@ int fused2d_window(const AxisTap* host_taps, int K, int L);
 size_t fused2d_smem(int WC);
 int fused3d_window(const AxisTap* host_taps, int K, int L);
 size_t fused3d_smem(int WC, int nf);
+struct Small1D;
+size_t small1d_smem(int P, int cpad, int RS);
+cudaError_t launch_small_sweep(const StepArgs& s, const Grid& g, const Problem& pb, int n0, int nsteps, int cur, double t0,
+                               double dt, double* v0, double* v1, cudaStream_t st);
 cudaError_t launch_fsde_step(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st);
 cudaError_t launch_hermite(const Grid& g, const double* values, int F, double* slot, cudaStream_t st, int64_t* launches);
 cudaError_t launch_bicubic_step(const StepArgs& s, const Grid& g, const Problem& pb, cudaStream_t st);
@@ -82,6 +87,7 @@ struct bsde_ctx {
   double* vbuf[2] = {nullptr, nullptr};   // ping-pong value buffers, F * npts each
   int cur = 0;                  // vbuf[cur] holds the newest level
   int fused_variant = 0;        // fused 1-D kernel variant (kernel_variant = 10 + v)
+  bool small_ok = false;        // d = 1 latency path: the whole sweep in one single-CTA launch
   int wc2 = 0, boot_wc2 = 0;    // 2-D / 3-D fused kernel column window (0: use the generic kernel)
   int wca = 0;                  // d = 2 affine path column window (0: not used)
   int nsm = 148;
@@ -462,9 +468,6 @@ bsde_status validate(const bsde_config* cfg, bsde_ctx* c) {
   if (cfg->sde_id < 0 || cfg->sde_id > 2) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "sde_id %d outside 0..2", cfg->sde_id);
   if (cfg->terminal_id == BSDE_TERM_CALL_X && cfg->sde_id == BSDE_SDE_BROWNIAN)
     return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "terminal CALL_X is a payoff of a forward SDE: set sde_id");
-  if (cfg->sde_id != BSDE_SDE_BROWNIAN && cfg->terminal_id != BSDE_TERM_CALL_X && cfg->terminal_id != BSDE_TERM_POLY &&
-      cfg->terminal_id != BSDE_TERM_CONST)
-    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "forward-SDE problems take the terminal CALL_X, POLY or CONST");
   if (cfg->sde_id != BSDE_SDE_BROWNIAN && cfg->driver_id == BSDE_DRV_EX2)
     return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "the Ex. 2 driver is defined for X = W only");
   if (cfg->sde_id != BSDE_SDE_BROWNIAN && cfg->nranks > 1)
@@ -601,7 +604,7 @@ Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d, bool aff2) {
             : 0;
   L.picard = off; off += al(sizeof(int32_t) * g.npts);
   L.bad = off; off += 256;
-  L.barrier = off; off += al(sizeof(unsigned) * 2 * 8192);      // fused-kernel progress flags
+  L.barrier = off; off += al(sizeof(unsigned) * 2 * kFlagCap);  // fused-kernel progress flags (ring, done)
   L.dres = off; off += 256;
   L.total = off;
   return L;
@@ -1013,6 +1016,11 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     set_distances(c, c->taps, c->K, c->geo);
   }
   if (cfg->sde_id != BSDE_SDE_BROWNIAN || cfg->interp != BSDE_INTERP_SPLINE) { c->wc2 = 0; c->wca = 0; }
+  // small 1-D grids (no fused geometry): the single-CTA whole-sweep kernel when its shared
+  // memory (every ring line + the spline scratch) fits
+  if (c->d == 1 && cfg->sde_id == BSDE_SDE_BROWNIAN && !c->geo.ok && cfg->kernel_variant == 0 && c->g.P[0] >= 16 &&
+      small1d_smem((int)c->g.P[0], (int)c->g.cpad, c->RS) <= 200 * 1024)
+    c->small_ok = true;
   c->tap_count = (int)c->taps.size();
   {
     const int bytes = (int)(sizeof(AxisTap) * c->taps.size());
@@ -1159,6 +1167,11 @@ static bsde_status check_bad(bsde_ctx* c) {
                  x[2], c->level, v[0], v[1], v[2], v[3]);
 }
 
+// device counter of the Picard iterations the fused 1-D kernel executes (in the dres area)
+static unsigned long long* pexec_counter(const bsde_ctx* c) {
+  return reinterpret_cast<unsigned long long*>(c->dres + 16);
+}
+
 // StepArgs of a persistent fused launch (ring_mode 1: the kernel derives the per-step slots,
 // times and value buffers from Persist1D)
 static StepArgs persistent_args(const bsde_ctx* c) {
@@ -1179,6 +1192,7 @@ static StepArgs persistent_args(const bsde_ctx* c) {
   s.picard = c->picard;
   s.bad = c->bad;
   s.phase_ns = c->phase_ns;
+  s.picard_exec = pexec_counter(c);
   return s;
 }
 
@@ -1192,6 +1206,7 @@ static void fill_result(bsde_ctx* c, bsde_result* res, const double out[4], doub
   res->t_total_s = c->t_setup + t_call;
   res->updates = c->g.nown0 * row_len(c) * steps;
   res->picard_max_used = c->cfg.picard_max;
+  res->picard_iters = -1;
   tcollect(c);                                   // the stream is synchronised by now
   res->t_spline_s = c->t_stage[ST_SPLINE];
   res->t_quad_s = c->t_stage[ST_QUAD];
@@ -1214,9 +1229,30 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
   // d = 1 fused path: all remaining steps in one cooperative (persistent) launch
   const bool fused = c->d == 1 && (c->cfg.kernel_variant == 0 || c->cfg.kernel_variant >= 10) && c->geo.ok &&
                      c->tap1_off >= 0;
-  if (fused && c->level >= 2) {
+  int64_t pexec = -1;
+  if (c->small_ok && c->level >= 1) {                  // latency path: one single-CTA launch
     const StepArgs s = persistent_args(c);
     const int ns = c->level;
+    cudaEvent_t tq = c->cfg.timing ? tmark(c) : nullptr;
+    cudaMemsetAsync(pexec_counter(c), 0, sizeof(unsigned long long), c->stream);
+    cudaError_t e = launch_small_sweep(s, c->g, c->pb, c->level - 1, ns, c->cur, c->cfg.t0, c->dt, c->vbuf[0],
+                                       c->vbuf[1], c->stream);
+    ++c->launches;
+    tstage(c, ST_QUAD, tq);
+    if (e != cudaSuccess) st = set_err(c, BSDE_ERR_CUDA, "small sweep kernel: %s", cudaGetErrorString(e));
+    else {
+      c->cur ^= (ns & 1);
+      c->level = 0;
+      steps = ns;
+      unsigned long long v = 0;
+      if (cudaMemcpyAsync(&v, pexec_counter(c), sizeof v, cudaMemcpyDeviceToHost, c->stream) == cudaSuccess &&
+          cudaStreamSynchronize(c->stream) == cudaSuccess)
+        pexec = (int64_t)v;
+    }
+  } else if (fused && c->level >= 2) {
+    const StepArgs s = persistent_args(c);
+    const int ns = c->level;
+    cudaMemsetAsync(pexec_counter(c), 0, sizeof(unsigned long long), c->stream);
     cudaEvent_t tq = c->cfg.timing ? tmark(c) : nullptr;
     cudaError_t e = launch_fused1d_steps(s, c->g, c->pb, c->geo.fz, c->level - 1, ns, 1, c->cur, c->cfg.t0, c->dt, c->vbuf[0],
                                c->vbuf[1], c->barrier, c->geo.D, c->geo.DK, c->geo.threads, c->geo.blocks,
@@ -1228,6 +1264,10 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
       c->cur ^= (ns & 1);
       c->level = 0;
       steps = ns;
+      unsigned long long v = 0;
+      if (cudaMemcpyAsync(&v, pexec_counter(c), sizeof v, cudaMemcpyDeviceToHost, c->stream) == cudaSuccess &&
+          cudaStreamSynchronize(c->stream) == cudaSuccess)
+        pexec = (int64_t)v;
     }
   }
   while (st == BSDE_OK && c->level > 0) {
@@ -1247,12 +1287,71 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
     if ((st = eval_point(c, out))) return st;
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
-    if (res) fill_result(c, res, out, ms * 1e-3, now_s() - t0, steps);
+    if (res) {
+      fill_result(c, res, out, ms * 1e-3, now_s() - t0, steps);
+      res->picard_iters = pexec;
+    }
   }
   return BSDE_OK;
 }
 
+// CTA distances of the fused kernel's neighbour waits for CTAs owning `tile` points (the
+// problem-partitioned batch: a range of ns tiles per CTA)
+static void distances_for(const bsde_ctx* c, int tile, int* D, int& DK) {
+  const int L = c->L;
+  for (int j = 0; j <= kMaxK; ++j) D[j] = 0;
+  D[0] = (kPcrHalo + 6 + tile - 1) / tile;
+  int dk = D[0];
+  for (int j = 1; j <= c->K; ++j) {
+    const int qa = -c->taps[(size_t)(j - 1) * L].q, qb = c->taps[(size_t)(j - 1) * L + L - 1].q;
+    D[j] = (std::max(qa, qb) + 4 + tile - 1) / tile;
+    dk = std::max(dk, D[j]);
+  }
+  DK = dk;
+}
+
+// Problem-partitioned plan of a batch (fused1d.cuh FusedBatch::part): problem i gets ncta[i]
+// CTAs, each a range of ns[i] consecutive tiles.  The fixed costs of a (CTA, step) -- the
+// spline pass, the hand-off latencies -- are then paid sum_i ncta_i steps_i times instead of
+// blocks * sum_i steps_i (round robin).  Cost model per (CTA, step) in units of one tile-level:
+// ns (K a + b) + c; the plan minimises the slowest problem's steps x cost subject to
+// sum ncta <= slots (binary search on that time).  Returns false if no plan fits.
+static bool plan_batch_partition(int n, const int* K, const int* steps, int tiles, int slots, int nsmax, int* ncta,
+                                 int* ns) {
+  const double a = 1.0, b = 1.0, c = 2.5;
+  auto cost = [&](int i, int s) { return (double)steps[i] * (s * (K[i] * a + b) + c + 0.25 * s); };
+  auto fit = [&](double T, int* nc, int* nsv) {
+    int tot = 0;
+    for (int i = 0; i < n; ++i) {
+      int s = 0;
+      for (int t = nsmax; t >= 1; --t)
+        if (cost(i, t) <= T) { s = t; break; }
+      if (s == 0) return false;
+      nc[i] = (tiles + s - 1) / s;
+      nsv[i] = (tiles + nc[i] - 1) / nc[i];           // balanced tiles per CTA
+      tot += nc[i];
+    }
+    return tot <= slots;
+  };
+  double lo = 0.0, hi = 0.0;
+  for (int i = 0; i < n; ++i) hi = std::max(hi, cost(i, nsmax));
+  hi *= 4.0;
+  int nc[kMaxBatch], nsv[kMaxBatch];
+  if (!fit(hi, nc, nsv)) return false;
+  for (int it = 0; it < 60; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (fit(mid, nc, nsv)) hi = mid; else lo = mid;
+  }
+  fit(hi, ncta, ns);
+  return true;
+}
+
 bsde_status bsde_solve_batch(bsde_ctx* const* cs, int32_t n, bsde_result* res) {
+  return bsde_solve_batch_mode(cs, n, 0, res);
+}
+
+bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, bsde_result* res) {
+  if (mode < 0 || mode > 2) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: mode %d outside 0..2", mode);
   if (!cs || n < 1 || n > kMaxBatch) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: need 1..%d contexts", kMaxBatch);
   for (int i = 0; i < n; ++i)
     if (!cs[i]) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: ctx %d is NULL", i);
@@ -1281,11 +1380,35 @@ bsde_status bsde_solve_batch(bsde_ctx* const* cs, int32_t n, bsde_result* res) {
     fz.WS = std::max(fz.WS, f.WS);
     fz.TK = std::max(fz.TK, f.TK);
   }
-  const size_t smem = fused1d_smem(fz);
+  // problem-partitioned mode for n >= 2 problems when a plan fits (else round robin)
+  int ncta[kMaxBatch], nsub[kMaxBatch], pblocks = 0;
+  bool part = false;
+  Fused1D fzp = fz;
+  size_t smem_p = 0;
+  if (mode != 1 && (n >= 2 || mode == 2)) {
+    const int TP = fz.TP, P = (int)c0->g.P[0];
+    const int mb = fused1d_blocks_per_sm(fz.variant, fused1d_smem(fzp));
+    const int nsmax = std::max(1, std::min(9, (P - 2 * kPcrHalo - 256) / (2 * TP)));
+    int Kv[kMaxBatch], st[kMaxBatch];
+    for (int i = 0; i < n; ++i) { Kv[i] = cs[i]->K; st[i] = cs[i]->level; }
+    if (mb > 0 && plan_batch_partition(n, Kv, st, c0->geo.blocks, c0->nsm * mb, nsmax, ncta, nsub)) {
+      int nsm_ = 1;
+      for (int i = 0; i < n; ++i) { nsm_ = std::max(nsm_, nsub[i]); pblocks += ncta[i]; }
+      fzp.WP = ((nsm_ * TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;   // PCR extent of a CTA's range
+      fzp.WS = 6 * fzp.WP + 16;
+      smem_p = fused1d_smem(fzp);
+      part = smem_p > 0 && pblocks <= c0->nsm * fused1d_blocks_per_sm(fzp.variant, smem_p) && pblocks <= kFlagCap;
+    }
+  }
+  if (mode == 2 && !part)
+    return set_err(c0, BSDE_ERR_RESOURCE_LIMIT, "batch: no problem-partitioned plan fits (shared memory / co-residency)");
+  if (part) fz = fzp;
+  const size_t smem = part ? smem_p : fused1d_smem(fz);
   if (smem == 0) return set_err(c0, BSDE_ERR_RESOURCE_LIMIT, "batch: the level windows do not fit in shared memory");
   const int per_sm = fused1d_blocks_per_sm(fz.variant, smem);
-  if (c0->geo.blocks > c0->nsm * per_sm)
-    return set_err(c0, BSDE_ERR_RESOURCE_LIMIT, "batch: %d CTAs with %zu B of shared memory are not co-resident", c0->geo.blocks, smem);
+  const int blocks = part ? pblocks : c0->geo.blocks;
+  if (blocks > c0->nsm * per_sm)
+    return set_err(c0, BSDE_ERR_RESOURCE_LIMIT, "batch: %d CTAs with %zu B of shared memory are not co-resident", blocks, smem);
   const double t0 = now_s();
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
@@ -1299,6 +1422,7 @@ bsde_status bsde_solve_batch(bsde_ctx* const* cs, int32_t n, bsde_result* res) {
       cudaStreamWaitEvent(c0->stream, ev, 0);
       cudaEventDestroy(ev);
     }
+  for (int i = 0; i < n; ++i) cudaMemsetAsync(pexec_counter(cs[i]), 0, sizeof(unsigned long long), c0->stream);
   cudaEventRecord(e0, c0->stream);
   FusedProb probs[kMaxBatch];
   int64_t steps[kMaxBatch];
@@ -1316,14 +1440,19 @@ bsde_status bsde_solve_batch(bsde_ctx* const* cs, int32_t n, bsde_result* res) {
     fp.pp.vbuf[0] = c->vbuf[0];
     fp.pp.vbuf[1] = c->vbuf[1];
     fp.pp.ring_flag = c->barrier;
-    fp.pp.done_flag = c->barrier + c->geo.blocks;
-    for (int j = 0; j <= kMaxK; ++j) fp.pp.D[j] = c->geo.D[j];
-    fp.pp.DK = c->geo.DK;
+    if (part) {
+      fp.pp.done_flag = c->barrier + kFlagCap;
+      distances_for(c, nsub[i] * fz.TP, fp.pp.D, fp.pp.DK);
+    } else {
+      fp.pp.done_flag = c->barrier + c->geo.blocks;
+      for (int j = 0; j <= kMaxK; ++j) fp.pp.D[j] = c->geo.D[j];
+      fp.pp.DK = c->geo.DK;
+    }
     for (int k = 0; k < 12; ++k) fp.dp[k] = c->pb.dp[k];
     steps[i] = c->level;
   }
-  cudaError_t e = launch_fused1d_batch(probs, n, c0->g, fz, c0->pb.driver_id, c0->geo.threads, c0->geo.blocks, smem,
-                                       c0->stream);
+  cudaError_t e = launch_fused1d_batch(probs, n, c0->g, fz, c0->pb.driver_id, c0->geo.threads, blocks, smem,
+                                       c0->stream, part ? ncta : nullptr, part ? nsub : nullptr);
   cudaEventRecord(e1, c0->stream);
   if (e != cudaSuccess) {
     cudaEventDestroy(e0);
@@ -1352,6 +1481,9 @@ bsde_status bsde_solve_batch(bsde_ctx* const* cs, int32_t n, bsde_result* res) {
       e = cudaStreamSynchronize(cs[i]->stream);
       if (e != cudaSuccess) return set_err(cs[i], BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
       fill_result(cs[i], &res[i], out, ms * 1e-3, now_s() - t0, steps[i]);
+      unsigned long long v = 0;
+      if (cudaMemcpy(&v, pexec_counter(cs[i]), sizeof v, cudaMemcpyDeviceToHost) == cudaSuccess)
+        res[i].picard_iters = (int64_t)v;
     }
   }
   return BSDE_OK;

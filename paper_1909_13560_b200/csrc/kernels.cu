@@ -550,6 +550,7 @@ __global__ void __launch_bounds__(256) quad_generic(StepArgs s, Grid g, Problem 
 
 // ------------------------------------------------------------------ 1-D fused step kernel
 #include "fused1d.cuh"
+#include "fused1d_small.cuh"
 
 // ------------------------------------------------------------------ 2-D fused quadrature kernel
 #include "fused2d.cuh"
