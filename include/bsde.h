@@ -156,6 +156,8 @@ typedef struct {
                                 points; the d = 1 persistent kernel counts them, -1 otherwise).
                                 The kernel leaves the loop at an exact fixed point, where the
                                 remaining iterations of the fixed count p are identities     */
+  int32_t batch_ctas;        /* bsde_solve_batch*: CTAs that stepped this problem            */
+  int32_t batch_tiles;       /* ... and tiles (of TP points) per CTA (1: round robin)         */
 } bsde_result;
 
 typedef struct bsde_ctx bsde_ctx;
@@ -202,7 +204,8 @@ bsde_status bsde_solve_batch(bsde_ctx* const* ctxs, int32_t n, bsde_result* res)
  * steps every problem on one tile of TP points); 2: problem-partitioned (each problem gets its
  * own CTAs, each CTA a range of consecutive tiles whose spline is built in one pass, sized by a
  * cost model so that all problems finish together; RESOURCE_LIMIT if no plan fits).  The
- * arithmetic of every point is the same in every mode (bitwise identical results).        */
+ * arithmetic of every point is the same in every mode (bitwise identical results).
+ * mode 11..19 (ablation): problem-partitioned with mode - 10 tiles per CTA for every problem. */
 bsde_status bsde_solve_batch_mode(bsde_ctx* const* ctxs, int32_t n, int32_t mode, bsde_result* res);
 
 /* index n of the newest level                                                         */

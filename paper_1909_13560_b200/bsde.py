@@ -59,7 +59,8 @@ class bsde_result(C.Structure):
     _fields_ = [("y0", C.c_double), ("z0", C.c_double * 3), ("t_setup_s", C.c_double),
                 ("t_sweep_s", C.c_double), ("t_total_s", C.c_double), ("updates", C.c_int64),
                 ("picard_max_used", C.c_int32), ("t_bootstrap_s", C.c_double), ("t_spline_s", C.c_double),
-                ("t_quad_s", C.c_double), ("t_comm_s", C.c_double), ("picard_iters", C.c_int64)]
+                ("t_quad_s", C.c_double), ("t_comm_s", C.c_double), ("picard_iters", C.c_int64),
+                ("batch_ctas", C.c_int32), ("batch_tiles", C.c_int32)]
 
 
 _lock = threading.Lock()

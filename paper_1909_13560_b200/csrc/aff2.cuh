@@ -218,17 +218,10 @@ __global__ void __launch_bounds__(kA1Thr) aff_rows(StepArgs s, Grid g, Problem p
     if (i1 + p >= P1) break;
     const double z[2] = {az0[p] * inv_gz0, az1[p] * inv_gz0};
     const double rhs = fma(s.ky_dt, af[p], ay[p]);
-    double y = ay[p];
     int it;
-    for (it = 1; it <= s.picard_max; ++it) {
-      const double yn = fma(s.ky_dt_gy0, dn(y, z), rhs);
-      const double dy = fabs(yn - y);
-      const bool fixed = (yn == y);
-      y = yn;
-      if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
-      if (fixed) { it = s.picard_max; break; }
-    }
-    if (it > s.picard_max) it = s.picard_max;
+    unsigned ex = 0;
+    const double y = picard_solve([&](double v) { return dn(v, z); }, ay[p], rhs, s.ky_dt_gy0, s.picard_max,
+                                  s.picard_tol, it, ex);
     const int64_t pidx = (g.own0 + i) * P1 + i1 + p;               // local value index
     s.values[pidx] = y;
     s.values[g.npts + pidx] = z[0];

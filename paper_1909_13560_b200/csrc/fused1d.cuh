@@ -377,7 +377,10 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
 
   for (int it = 0; it < it_end; ++it) {
     // ================= pass 1: levels K..1, z and Picard of step it of every problem / tile
-    if (warp == 0 && it > 0) refresh_marks<0>(PB, bt.nprob, it, marks, bid, nb, ipc);
+    // one relaxed read of every problem's flags + one acquire fence serve all problems' waits of
+    // the pass; a CTA with a single problem waits with per-flag acquire loads instead (no fence)
+    const bool multi = ipc < 0 && bt.nprob > 1;
+    if (warp == 0 && it > 0 && multi) refresh_marks<0>(PB, bt.nprob, it, marks, bid, nb, ipc);
     for (int un = 0; un < nunits; ++un) {
       const int ip = unit_prob(un);
       const FusedProb& fp = PB[ip];
@@ -452,19 +455,20 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
           const int q = t.q;
           double yh[R], zh[R];
           {
+            // the R 4-term stencils of consecutive points, coefficient-major: every loaded
+            // coefficient feeds up to 4 independent FMA chains at once (y and z interleaved), so
+            // few registers stay live and the chains overlap
             const double* py = wy + (rel0 + q);
             const double* pz = wz + (rel0 + q);
-            double c[R + 3];
+            const double B0 = t.B[0], B1 = t.B[1], B2 = t.B[2], B3 = t.B[3];
 #pragma unroll
-            for (int k = 0; k < R + 3; ++k) c[k] = py[k];
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-              yh[r] = fma(t.B[0], c[r], fma(t.B[1], c[r + 1], fma(t.B[2], c[r + 2], t.B[3] * c[r + 3])));
-#pragma unroll
-            for (int k = 0; k < R + 3; ++k) c[k] = pz[k];
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-              zh[r] = fma(t.B[0], c[r], fma(t.B[1], c[r + 1], fma(t.B[2], c[r + 2], t.B[3] * c[r + 3])));
+            for (int k = 0; k < R + 3; ++k) {
+              const double cy = py[k], cz = pz[k];
+              if (k < R) { yh[k] = B0 * cy; zh[k] = B0 * cz; }
+              if (k - 1 >= 0 && k - 1 < R) { yh[k - 1] = fma(B1, cy, yh[k - 1]); zh[k - 1] = fma(B1, cz, zh[k - 1]); }
+              if (k - 2 >= 0 && k - 2 < R) { yh[k - 2] = fma(B2, cy, yh[k - 2]); zh[k - 2] = fma(B2, cz, zh[k - 2]); }
+              if (k - 3 >= 0 && k - 3 < R) { yh[k - 3] = fma(B3, cy, yh[k - 3]); zh[k - 3] = fma(B3, cz, zh[k - 3]); }
+            }
           }
           const int cb = cl0 + q, ce = cb + R - 1;     // lane's cells
           if ((left && cb <= -1 && ce >= -3) || (right && cb <= P + 2 && ce >= P - 1)) {
@@ -555,20 +559,15 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
           prefetched = 2;
           taps_in = true;
         } else {
-          // last unit of the round: the first unit of the next round (its taps; with a
-          // separate spline scratch also its windows of levels >= 2)
+          // last unit of the round: the tap table of the first unit of the next round (with a
+          // separate spline scratch its windows of levels >= 2 follow at the start of pass 2,
+          // off the critical path of this epilogue)
           uq = 0;
           while (uq < nunits && it + 1 >= PB[unit_prob(uq)].pp.nsteps) ++uq;
           if (uq < nunits) {
             const int iq = unit_prob(uq);
-            const int lq = unit_lo(uq), hq = min(lq + TP, chi);
-            if (warp == iw) {
-              issue_taps(PB[iq], bt.arena, tsm, &bar[3]);
-              if (fz.sep)
-                start_windows_ahead(PB[iq], spans + 2 * kMaxK * iq, marks + 4 * iq, it + 1, buf0, buf1, WM, bar, lq,
-                                    hq, bid, nb);
-            }
-            prefetched = fz.sep ? min(2, max(0, PB[iq].s.K - 1)) : 0;   // what start_windows_ahead issued
+            if (warp == iw) issue_taps(PB[iq], bt.arena, tsm, &bar[3]);
+            prefetched = fz.sep ? min(2, max(0, PB[iq].s.K - 1)) : 0;   // what pass 2 issues
             taps_in = true;
           }
         }
@@ -584,18 +583,9 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         dn.at(tn);
         const double z = az[u] * inv_gz0;
         const double rhs = fma(s.ky_dt, af[u], ay[u]);
-        double y = ay[u];
         int itp;
-        for (itp = 1; itp <= s.picard_max; ++itp) {
-          const double yn = fma(s.ky_dt_gy0, dn(y, &z), rhs);
-          const double dy = fabs(yn - y);
-          const bool fixed = (yn == y);     // exact fixed point: the remaining iterations are identities
-          y = yn;
-          ++pexec;
-          if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
-          if (fixed) { itp = s.picard_max; break; }
-        }
-        if (itp > s.picard_max) itp = s.picard_max;
+        const double y = picard_solve([&](double v) { return dn(v, &z); }, ay[u], rhs, s.ky_dt_gy0, s.picard_max,
+                                      s.picard_tol, itp, pexec);
         const int p = lo + t;
         vout[p] = y;
         vout[P + p] = z;
@@ -617,7 +607,32 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
     }
 
     // ================= pass 2: spline of every problem's new level n on this CTA's tile
-    if (warp == 0) refresh_marks<1>(PB, bt.nprob, it, marks, bid, nb, ipc);
+    if (fz.sep && warp == iw && iw != 0) {
+      // the next round's first unit: its windows of levels >= 2 (ring data of round it-1 or
+      // older) stream into the level buffers during this pass (ring marks only: warp 0 touches
+      // the done marks)
+      int uq = 0;
+      while (uq < nunits && it + 1 >= PB[unit_prob(uq)].pp.nsteps) ++uq;
+      if (uq < nunits) {
+        const int iq = unit_prob(uq);
+        const int lq = unit_lo(uq), hq = min(lq + TP, chi);
+        start_windows_ahead(PB[iq], spans + 2 * kMaxK * iq, marks + 4 * iq, it + 1, buf0, buf1, WM, bar, lq, hq, bid,
+                            nb);
+      }
+    }
+    if (warp == 0) {
+      if (multi) refresh_marks<1>(PB, bt.nprob, it, marks, bid, nb, ipc);
+      if (fz.sep && iw == 0) {      // no point-free warp: warp 0 issues the windows itself
+        int uq = 0;
+        while (uq < nunits && it + 1 >= PB[unit_prob(uq)].pp.nsteps) ++uq;
+        if (uq < nunits) {
+          const int iq = unit_prob(uq);
+          const int lq = unit_lo(uq), hq = min(lq + TP, chi);
+          start_windows_ahead(PB[iq], spans + 2 * kMaxK * iq, marks + 4 * iq, it + 1, buf0, buf1, WM, bar, lq, hq,
+                              bid, nb);
+        }
+      }
+    }
     for (int ip = 0; ip < bt.nprob; ++ip) {
       const FusedProb& fp = PB[ip];
       const Persist1D& pp = fp.pp;

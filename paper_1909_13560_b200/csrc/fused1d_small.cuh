@@ -118,18 +118,9 @@ __global__ void __launch_bounds__(256, 1) quad1d_small(const __grid_constant__ S
       // z (Eq. 20 line 2, explicit) then y by Picard from E[y^{n+Ky}] (Eq. 20 line 1)
       const double z = Az / a.gz0;
       const double rhs = fma(a.ky_dt, Af, Ay);
-      double y = Ay;
       int itp;
-      for (itp = 1; itp <= a.picard_max; ++itp) {
-        const double yn = fma(a.ky_dt_gy0, dn(y, &z), rhs);
-        const double dy = fabs(yn - y);
-        const bool fixed = (yn == y);      // exact fixed point: the remaining iterations are identities
-        y = yn;
-        ++pexec;
-        if (a.picard_tol > 0.0 && dy <= a.picard_tol) break;
-        if (fixed) { itp = a.picard_max; break; }
-      }
-      if (itp > a.picard_max) itp = a.picard_max;
+      const double y = picard_solve([&](double v) { return dn(v, &z); }, Ay, rhs, a.ky_dt_gy0, a.picard_max,
+                                    a.picard_tol, itp, pexec);
       V[p] = y;
       V[P + p] = z;
       a.picard[p] = itp;

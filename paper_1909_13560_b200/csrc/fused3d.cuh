@@ -379,17 +379,10 @@ __global__ void epilogue_zy3(StepArgs s, Grid g, Problem pb, const double* __res
   const double z[3] = {acc[o] * inv_gz0, acc[nown + o] * inv_gz0, acc[2 * nown + o] * inv_gz0};
   const double af = acc[3 * nown + o], ay = acc[4 * nown + o];
   const double rhs = fma(s.ky_dt, af, ay);
-  double y = ay;
   int it;
-  for (it = 1; it <= s.picard_max; ++it) {
-    const double yn = fma(s.ky_dt_gy0, dn(y, z), rhs);
-    const double dy = fabs(yn - y);
-    const bool fixed = (yn == y);
-    y = yn;
-    if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
-    if (fixed) { it = s.picard_max; break; }
-  }
-  if (it > s.picard_max) it = s.picard_max;
+  unsigned ex = 0;
+  const double y = picard_solve([&](double v) { return dn(v, z); }, ay, rhs, s.ky_dt_gy0, s.picard_max,
+                                s.picard_tol, it, ex);
   const int64_t pidx = g.own0 * g.P[1] * g.P[2] + o;       // local value index
   s.values[pidx] = y;
   s.values[g.npts + pidx] = z[0];

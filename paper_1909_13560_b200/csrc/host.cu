@@ -1351,7 +1351,8 @@ bsde_status bsde_solve_batch(bsde_ctx* const* cs, int32_t n, bsde_result* res) {
 }
 
 bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, bsde_result* res) {
-  if (mode < 0 || mode > 2) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: mode %d outside 0..2", mode);
+  if (mode < 0 || (mode > 2 && (mode < 11 || mode > 19)))
+    return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: mode %d outside 0..2, 11..19", mode);
   if (!cs || n < 1 || n > kMaxBatch) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: need 1..%d contexts", kMaxBatch);
   for (int i = 0; i < n; ++i)
     if (!cs[i]) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: ctx %d is NULL", i);
@@ -1385,13 +1386,24 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
   bool part = false;
   Fused1D fzp = fz;
   size_t smem_p = 0;
-  if (mode != 1 && (n >= 2 || mode == 2)) {
+  if (mode != 1 && (n >= 2 || mode >= 2)) {
     const int TP = fz.TP, P = (int)c0->g.P[0];
     const int mb = fused1d_blocks_per_sm(fz.variant, fused1d_smem(fzp));
     const int nsmax = std::max(1, std::min(9, (P - 2 * kPcrHalo - 256) / (2 * TP)));
     int Kv[kMaxBatch], st[kMaxBatch];
     for (int i = 0; i < n; ++i) { Kv[i] = cs[i]->K; st[i] = cs[i]->level; }
-    if (mb > 0 && plan_batch_partition(n, Kv, st, c0->geo.blocks, c0->nsm * mb, nsmax, ncta, nsub)) {
+    bool planned = false;
+    if (mode >= 11) {                                  // ablation: every problem ns = mode - 10 tiles per CTA
+      planned = true;
+      for (int i = 0; i < n; ++i) {
+        nsub[i] = std::min(mode - 10, nsmax);
+        ncta[i] = (c0->geo.blocks + nsub[i] - 1) / nsub[i];
+        nsub[i] = (c0->geo.blocks + ncta[i] - 1) / ncta[i];
+      }
+    } else {
+      planned = mb > 0 && plan_batch_partition(n, Kv, st, c0->geo.blocks, c0->nsm * mb, nsmax, ncta, nsub);
+    }
+    if (planned) {
       int nsm_ = 1;
       for (int i = 0; i < n; ++i) { nsm_ = std::max(nsm_, nsub[i]); pblocks += ncta[i]; }
       fzp.WP = ((nsm_ * TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;   // PCR extent of a CTA's range
@@ -1400,7 +1412,7 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
       part = smem_p > 0 && pblocks <= c0->nsm * fused1d_blocks_per_sm(fzp.variant, smem_p) && pblocks <= kFlagCap;
     }
   }
-  if (mode == 2 && !part)
+  if (mode >= 2 && !part)
     return set_err(c0, BSDE_ERR_RESOURCE_LIMIT, "batch: no problem-partitioned plan fits (shared memory / co-residency)");
   if (part) fz = fzp;
   const size_t smem = part ? smem_p : fused1d_smem(fz);
@@ -1481,6 +1493,8 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
       e = cudaStreamSynchronize(cs[i]->stream);
       if (e != cudaSuccess) return set_err(cs[i], BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
       fill_result(cs[i], &res[i], out, ms * 1e-3, now_s() - t0, steps[i]);
+      res[i].batch_ctas = part ? ncta[i] : blocks;
+      res[i].batch_tiles = part ? nsub[i] : 1;
       unsigned long long v = 0;
       if (cudaMemcpy(&v, pexec_counter(cs[i]), sizeof v, cudaMemcpyDeviceToHost) == cudaSuccess)
         res[i].picard_iters = (int64_t)v;

@@ -459,17 +459,10 @@ __device__ inline void epilogue(const StepArgs& s, int64_t p, int64_t npts, doub
 #pragma unroll
   for (int a = 0; a < D; ++a) z[a] = Az[a] / s.gz0;
   const double rhs = fma(s.ky_dt, Af, Ay);
-  double y = Ay;
   int it;
-  for (it = 1; it <= s.picard_max; ++it) {
-    const double yn = fma(s.ky_dt_gy0, drv(y, z), rhs);
-    const double dy = fabs(yn - y);
-    const bool fixed = (yn == y);    // exact fixed point: the remaining iterations are identities
-    y = yn;
-    if (s.picard_tol > 0.0 && dy <= s.picard_tol) break;
-    if (fixed) { it = s.picard_max; break; }
-  }
-  if (it > s.picard_max) it = s.picard_max;
+  unsigned ex = 0;
+  const double y = picard_solve([&](double v) { return drv(v, z); }, Ay, rhs, s.ky_dt_gy0, s.picard_max,
+                                s.picard_tol, it, ex);
   s.values[p] = y;
   bool bad = !isfinite(y);
 #pragma unroll

@@ -85,6 +85,39 @@ template <int D> struct Driver<DRV_DIFF, D> {
   }
 };
 
+// ---------------------------------------------------------------- Picard solve of Eq. 20
+// y = rhs + c f(t_n, y, z^n) by Picard iteration from y0 = E[y^{n+Ky}] (Eq. 20 line 1,
+// PAPER.md:343-345, 377-378): exactly pmax iterations (p = 30; R8), or
+// until |y^(k) - y^(k-1)| <= tol when tol > 0.  Two exact shortcuts leave the loop early without
+// changing the result bit for bit: at a fixed point (y^(k) == y^(k-1)) every later iterate is
+// y^(k); on a period-2 cycle (y^(k) == y^(k-2), rounding oscillation between two doubles) the
+// iterate pmax is y^(k) or y^(k-1) by parity (and |dy| stays the same, so tol cannot be met
+// later).  count: the iteration count the scheme defines (pmax, or the tolerance exit);
+// executed: += the iterations actually evaluated.
+template <class Fn>
+__device__ __forceinline__ double picard_solve(const Fn& f, double y0, double rhs, double c, int pmax, double tol,
+                                               int& count, unsigned& executed) {
+  double y = y0, yprev = nan("");
+  int it;
+  for (it = 1; it <= pmax; ++it) {
+    const double yn = fma(c, f(y), rhs);
+    const double dy = fabs(yn - y);
+    const bool fixed = (yn == y), cycle2 = (yn == yprev);
+    yprev = y;
+    y = yn;
+    ++executed;
+    if (tol > 0.0 && dy <= tol) break;
+    if (fixed) { it = pmax; break; }
+    if (cycle2) {
+      if ((pmax - it) & 1) y = yprev;
+      it = pmax;
+      break;
+    }
+  }
+  count = it > pmax ? pmax : it;
+  return y;
+}
+
 // ---------------------------------------------------------------- terminal g, grad g
 __device__ inline double logistic_d(double s) { return 1.0 / (1.0 + exp(-s)); }
 
