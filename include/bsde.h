@@ -200,12 +200,14 @@ bsde_status bsde_solve(bsde_ctx* ctx, bsde_result* res);
 bsde_status bsde_solve_batch(bsde_ctx* const* ctxs, int32_t n, bsde_result* res);
 
 /* bsde_solve_batch with an explicit CTA schedule.  mode 0: auto (= bsde_solve_batch: the
- * problem-partitioned schedule when a plan fits, else round robin); 1: round robin (every CTA
- * steps every problem on one tile of TP points); 2: problem-partitioned (each problem gets its
- * own CTAs, each CTA a range of consecutive tiles whose spline is built in one pass, sized by a
- * cost model so that all problems finish together; RESOURCE_LIMIT if no plan fits).  The
- * arithmetic of every point is the same in every mode (bitwise identical results).
- * mode 11..19 (ablation): problem-partitioned with mode - 10 tiles per CTA for every problem. */
+ * schedule of mode 3 when a plan fits, else round robin); 1: round robin (every CTA steps every
+ * problem on one tile of TP points); 2: paired problem-partitioned (the problems are paired by K
+ * rank -- smallest with largest -- and each pair gets its own CTAs, which step the pair's two
+ * problems round robin on a range of consecutive tiles whose spline is built in one pass; the
+ * CTAs per pair come from a cost model so that all pairs finish together); 3: the same with one
+ * problem per group; RESOURCE_LIMIT from modes 2, 3 if no plan fits.  The arithmetic of every
+ * point is the same in every mode (bitwise identical results).
+ * mode 11..19 (ablation): one problem per group, mode - 10 tiles per CTA.                    */
 bsde_status bsde_solve_batch_mode(bsde_ctx* const* ctxs, int32_t n, int32_t mode, bsde_result* res);
 
 /* index n of the newest level                                                         */

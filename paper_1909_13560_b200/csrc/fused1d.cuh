@@ -20,6 +20,7 @@
 // one launch (persistent), bsde_step one step per launch.  Levels are processed K..1 so the
 // wait for the neighbours' level-(n+1) coefficients is hidden behind levels K..2.
 #pragma once
+#include <type_traits>
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -116,12 +117,13 @@ struct FusedBatch {
   const unsigned char* arena;   // global address of the constant tap arena (bulk-copy source)
   int nprob, max_steps;
   FusedProb prob[kMaxBatch];
-  // problem-partitioned mode (part = 1): CTAs [cta0[ip], cta0[ip+1]) serve problem ip alone,
-  // each a range of ns[ip] consecutive tiles of TP points (sub-tiles, pass 1) whose spline is
+  // problem-partitioned mode (part = 1): the problems form groups (contiguous in prob[]); the
+  // CTAs [gcta0[g], gcta0[g+1]) serve group g's problems [gp0[g], gp0[g+1]) round robin, each
+  // CTA a range of gns[g] consecutive tiles of TP points (sub-tiles of pass 1) whose spline is
   // built in one pass 2; round-robin mode (part = 0): every CTA serves every problem on one tile
-  int part;
-  int cta0[kMaxBatch + 1];
-  int ns[kMaxBatch];
+  int part, ngroup;
+  int gp0[kMaxBatch + 1], gcta0[kMaxBatch + 1];
+  int gns[kMaxBatch];
 };
 
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
@@ -176,13 +178,13 @@ __device__ __forceinline__ void wait_flags(const unsigned* flag, unsigned* mk, i
 // of the CTA (after the barrier that follows) behind them.
 template <int KIND>   // 0: ring flags (short range D[1]), 1: done flags (short range D[0])
 __device__ __forceinline__ void refresh_marks(const FusedProb* prob, int nprob, int it, unsigned* marks, int b, int nb,
-                                              int only) {
+                                              int pf, int pl) {
   const int lane = threadIdx.x & 31;
   unsigned v[kMaxBatch];
 #pragma unroll
   for (int ip = 0; ip < kMaxBatch; ++ip) {
     v[ip] = 0xffffffffu;
-    if (ip < nprob && it < prob[ip].pp.nsteps && (only < 0 || ip == only)) {
+    if (ip < nprob && it < prob[ip].pp.nsteps && ip >= pf && ip < pl) {
       const Persist1D& pp = prob[ip].pp;
       const int q = b - pp.DK + lane;
       if (2 * pp.DK + 1 <= 32 && lane <= 2 * pp.DK && q >= 0 && q < nb)
@@ -191,7 +193,7 @@ __device__ __forceinline__ void refresh_marks(const FusedProb* prob, int nprob, 
   }
 #pragma unroll
   for (int ip = 0; ip < kMaxBatch; ++ip) {
-    if (ip >= nprob || it >= prob[ip].pp.nsteps || 2 * prob[ip].pp.DK + 1 > 32 || (only >= 0 && ip != only)) continue;
+    if (ip >= nprob || it >= prob[ip].pp.nsteps || 2 * prob[ip].pp.DK + 1 > 32 || ip < pf || ip >= pl) continue;
     const Persist1D& pp = prob[ip].pp;
     const int Dn = KIND ? pp.D[0] : pp.D[1];
     const int d = lane - pp.DK;
@@ -300,15 +302,18 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   const int chunk = warp / NWPG, pg = warp % NWPG;
   const int P = (int)g.P[0];
   const int TP = fz.TP;
-  // this CTA: problem ipc (part mode; -1: every problem), its index bid among the nb CTAs that
-  // serve that problem (the index of its progress flags), and its range [clo, chi) of nsub tiles
-  int ipc = -1, bid = blockIdx.x, nb = gridDim.x, nsub = 1;
+  // this CTA: its problems [pf, pl) (part mode: its group's; else every problem), its index bid
+  // among the nb CTAs that serve them (the index of its progress flags), its range [clo, chi) of
+  // nsub tiles
+  int pf = 0, pl = bt.nprob, bid = blockIdx.x, nb = gridDim.x, nsub = 1;
   if (bt.part) {
-    ipc = 0;
-    while (ipc + 1 < bt.nprob && (int)blockIdx.x >= bt.cta0[ipc + 1]) ++ipc;
-    bid = blockIdx.x - bt.cta0[ipc];
-    nb = bt.cta0[ipc + 1] - bt.cta0[ipc];
-    nsub = bt.ns[ipc];
+    int gi = 0;
+    while (gi + 1 < bt.ngroup && (int)blockIdx.x >= bt.gcta0[gi + 1]) ++gi;
+    pf = bt.gp0[gi];
+    pl = bt.gp0[gi + 1];
+    bid = blockIdx.x - bt.gcta0[gi];
+    nb = bt.gcta0[gi + 1] - bt.gcta0[gi];
+    nsub = bt.gns[gi];
   }
   const int clo = bid * nsub * TP;
   const int chi = min(clo + nsub * TP, P);
@@ -370,17 +375,19 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   bool taps_in = false;       // its tap table is in flight
   // work units of a round: round-robin mode one per problem (the CTA's tile), part mode one per
   // tile of the CTA's range (its one problem)
-  const int nunits = bt.part ? nunit_sub : bt.nprob;
-  const int it_end = bt.part ? PB[ipc].pp.nsteps : bt.max_steps;
-  auto unit_prob = [&](int u) { return bt.part ? ipc : u; };
-  auto unit_lo = [&](int u) { return bt.part ? clo + u * TP : clo; };
+  // (problem-major: every tile of a problem, then the next problem of the group)
+  const int nunits = (pl - pf) * nunit_sub;
+  int it_end = 0;
+  for (int ip = pf; ip < pl; ++ip) it_end = max(it_end, PB[ip].pp.nsteps);
+  auto unit_prob = [&](int u) { return pf + u / nunit_sub; };
+  auto unit_lo = [&](int u) { return clo + (u % nunit_sub) * TP; };
 
   for (int it = 0; it < it_end; ++it) {
     // ================= pass 1: levels K..1, z and Picard of step it of every problem / tile
     // one relaxed read of every problem's flags + one acquire fence serve all problems' waits of
     // the pass; a CTA with a single problem waits with per-flag acquire loads instead (no fence)
-    const bool multi = ipc < 0 && bt.nprob > 1;
-    if (warp == 0 && it > 0 && multi) refresh_marks<0>(PB, bt.nprob, it, marks, bid, nb, ipc);
+    const bool multi = pl - pf > 1;
+    if (warp == 0 && it > 0 && multi) refresh_marks<0>(PB, bt.nprob, it, marks, bid, nb, pf, pl);
     for (int un = 0; un < nunits; ++un) {
       const int ip = unit_prob(un);
       const FusedProb& fp = PB[ip];
@@ -449,50 +456,66 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         drv.at(tlev[j - 1]);
         const bool yj = (j == s.Ky);
         const int cl0 = lo + li0;                      // lane's first point
-        const int rel0 = cl0 - wv;                     // ... relative to the window (q = 0)
-        for (int l = chunk; l < L; l += C) {
-          const Tap1D& t = tj[l];
-          const int q = t.q;
-          double yh[R], zh[R];
-          {
-            // the R 4-term stencils of consecutive points, coefficient-major: every loaded
-            // coefficient feeds up to 4 independent FMA chains at once (y and z interleaved), so
-            // few registers stay live and the chains overlap
-            const double* py = wy + (rel0 + q);
-            const double* pz = wz + (rel0 + q);
-            const double B0 = t.B[0], B1 = t.B[1], B2 = t.B[2], B3 = t.B[3];
+        // ... relative to the window (q = 0); a lane past a ragged tile's end reads the tile's
+        // first point's stencils instead (its sums are never stored), so the tap loop has no
+        // per-lane branch
+        const int rel0 = (active ? cl0 : lo) - wv;
+        // EDGE: the tile's stencils may straddle the box boundary (edge CTAs only); YJ: this
+        // level also feeds E[y^{n+Ky}].  Specialised so that the interior tap loop is
+        // branch-free and consecutive taps interleave.
+        auto tap_loop = [&](auto edge_c, auto yj_c) {
+          constexpr bool EDGE = decltype(edge_c)::value;
+          constexpr bool YJ = decltype(yj_c)::value;
+#pragma unroll 2
+          for (int l = chunk; l < L; l += C) {
+            const Tap1D& t = tj[l];
+            const int q = t.q;
+            double yh[R], zh[R];
+            {
+              // the R 4-term stencils of consecutive points, coefficient-major: every loaded
+              // coefficient feeds up to 4 independent FMA chains at once (y and z interleaved), so
+              // few registers stay live and the chains overlap
+              const double* py = wy + (rel0 + q);
+              const double* pz = wz + (rel0 + q);
+              const double B0 = t.B[0], B1 = t.B[1], B2 = t.B[2], B3 = t.B[3];
 #pragma unroll
-            for (int k = 0; k < R + 3; ++k) {
-              const double cy = py[k], cz = pz[k];
-              if (k < R) { yh[k] = B0 * cy; zh[k] = B0 * cz; }
-              if (k - 1 >= 0 && k - 1 < R) { yh[k - 1] = fma(B1, cy, yh[k - 1]); zh[k - 1] = fma(B1, cz, zh[k - 1]); }
-              if (k - 2 >= 0 && k - 2 < R) { yh[k - 2] = fma(B2, cy, yh[k - 2]); zh[k - 2] = fma(B2, cz, zh[k - 2]); }
-              if (k - 3 >= 0 && k - 3 < R) { yh[k - 3] = fma(B3, cy, yh[k - 3]); zh[k - 3] = fma(B3, cz, zh[k - 3]); }
+              for (int k = 0; k < R + 3; ++k) {
+                const double cy = py[k], cz = pz[k];
+                if (k < R) { yh[k] = B0 * cy; zh[k] = B0 * cz; }
+                if (k - 1 >= 0 && k - 1 < R) { yh[k - 1] = fma(B1, cy, yh[k - 1]); zh[k - 1] = fma(B1, cz, zh[k - 1]); }
+                if (k - 2 >= 0 && k - 2 < R) { yh[k - 2] = fma(B2, cy, yh[k - 2]); zh[k - 2] = fma(B2, cz, zh[k - 2]); }
+                if (k - 3 >= 0 && k - 3 < R) { yh[k - 3] = fma(B3, cy, yh[k - 3]); zh[k - 3] = fma(B3, cz, zh[k - 3]); }
+              }
             }
-          }
-          const int cb = cl0 + q, ce = cb + R - 1;     // lane's cells
-          if ((left && cb <= -1 && ce >= -3) || (right && cb <= P + 2 && ce >= P - 1)) {
+            if (EDGE) {
+              const int cb = cl0 + q, ce = cb + R - 1;     // lane's cells
+              if ((left && cb <= -1 && ce >= -3) || (right && cb <= P + 2 && ce >= P - 1)) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                  const int cell = cb + r;
+                  if (cell >= -3 && cell <= -1) { yh[r] = fy0; zh[r] = fz0; }
+                  if (cell >= P - 1 && cell <= P + 2) { yh[r] = fy1; zh[r] = fz1; }
+                }
+              }
+            }
+            const double wcz = t.wcz, wgz = t.wgz, wgy = t.wgy;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-              const int cell = cb + r;
-              if (cell >= -3 && cell <= -1) { yh[r] = fy0; zh[r] = fz0; }
-              if (cell >= P - 1 && cell <= P + 2) { yh[r] = fy1; zh[r] = fz1; }
+              const double f = drv(yh[r], &zh[r]);
+              Az[r] = fma(wcz, zh[r], fma(wgz, f, Az[r]));
+              Af[r] = fma(wgy, f, Af[r]);
+            }
+            if (YJ) {
+              const double wy_ = t.wy;
+#pragma unroll
+              for (int r = 0; r < R; ++r) Ay[r] = fma(wy_, yh[r], Ay[r]);
             }
           }
-          if (!active) continue;
-          const double wcz = t.wcz, wgz = t.wgz, wgy = t.wgy;
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const double f = drv(yh[r], &zh[r]);
-            Az[r] = fma(wcz, zh[r], fma(wgz, f, Az[r]));
-            Af[r] = fma(wgy, f, Af[r]);
-          }
-          if (yj) {
-            const double wy_ = t.wy;
-#pragma unroll
-            for (int r = 0; r < R; ++r) Ay[r] = fma(wy_, yh[r], Ay[r]);
-          }
-        }
+        };
+        using T_ = std::true_type;
+        using F_ = std::false_type;
+        if (left || right) { if (yj) tap_loop(T_{}, T_{}); else tap_loop(T_{}, F_{}); }
+        else { if (yj) tap_loop(F_{}, T_{}); else tap_loop(F_{}, F_{}); }
       };
 
       // levels K, ..., 1, double-buffered: level j-2 streams in while level j is computed
@@ -603,7 +626,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       __syncthreads();
       PHASE_STAMP(9);
       // the problem's level n is complete on this CTA after its last unit
-      if (tid == publisher && (!bt.part || un == nunits - 1)) st_release(pp.done_flag + bid, (unsigned)it + 1);
+      if (tid == publisher && un % nunit_sub == nunit_sub - 1) st_release(pp.done_flag + bid, (unsigned)it + 1);
     }
 
     // ================= pass 2: spline of every problem's new level n on this CTA's tile
@@ -621,7 +644,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       }
     }
     if (warp == 0) {
-      if (multi) refresh_marks<1>(PB, bt.nprob, it, marks, bid, nb, ipc);
+      if (multi) refresh_marks<1>(PB, bt.nprob, it, marks, bid, nb, pf, pl);
       if (fz.sep && iw == 0) {      // no point-free warp: warp 0 issues the windows itself
         int uq = 0;
         while (uq < nunits && it + 1 >= PB[unit_prob(uq)].pp.nsteps) ++uq;
@@ -636,7 +659,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
     for (int ip = 0; ip < bt.nprob; ++ip) {
       const FusedProb& fp = PB[ip];
       const Persist1D& pp = fp.pp;
-      if (it >= pp.nsteps || (ipc >= 0 && ip != ipc)) continue;
+      if (it >= pp.nsteps || ip < pf || ip >= pl) continue;
       const StepArgs& s = fp.s;
       const int it_stamp = it;
       int slot_out;
@@ -908,14 +931,14 @@ int fused1d_blocks_per_sm(int variant, size_t smem) {
 // one cooperative launch over nprob problems (round-robin steps); the progress flags of
 // every problem (pp.ring_flag, 2 x blocks) are cleared first
 cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& g, const Fused1D& fz, int driver_id,
-                                 int threads, int blocks, size_t smem, cudaStream_t st, const int* ncta,
-                                 const int* nsub) {
+                                 int threads, int blocks, size_t smem, cudaStream_t st, const int* group,
+                                 const int* gcta, const int* gns, int ngroup) {
   if (nprob < 1 || nprob > kMaxBatch) return cudaErrorInvalidValue;
   thread_local static FusedBatch bt;     // ~6 KB: kept off the stack
   bt = FusedBatch{};
   bt.fz = fz;
   bt.g = g;
-  bt.part = ncta != nullptr;
+  bt.part = group != nullptr;
   {
     void* a = nullptr;
     cudaError_t e = cudaGetSymbolAddress(&a, c_arena);
@@ -927,17 +950,30 @@ cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& 
   // problems with more levels first: the first problem of a round then has windows of levels
   // >= 2 that stream in during the previous round's pass 2 (a stable order; each problem's
   // arithmetic does not depend on it)
+  // (part mode: group-major, each group's problems contiguous)
   int order[kMaxBatch];
   for (int i = 0; i < nprob; ++i) order[i] = i;
-  std::stable_sort(order, order + nprob, [&](int a, int b) { return probs[a].s.K > probs[b].s.K; });
+  std::stable_sort(order, order + nprob, [&](int a, int b) {
+    if (group && group[a] != group[b]) return group[a] < group[b];
+    return probs[a].s.K > probs[b].s.K;
+  });
   int tot = 0;
+  if (bt.part) {
+    bt.ngroup = ngroup;
+    for (int gi = 0; gi < ngroup; ++gi) {
+      bt.gcta0[gi] = tot;
+      bt.gns[gi] = gns[gi];
+      tot += gcta[gi];
+    }
+    bt.gcta0[ngroup] = tot;
+    int k = 0;
+    for (int gi = 0; gi <= ngroup; ++gi) {
+      while (k < nprob && group[order[k]] < gi) ++k;
+      bt.gp0[gi] = k;
+    }
+  }
   for (int i = 0; i < nprob; ++i) {
     bt.prob[i] = probs[order[i]];
-    if (bt.part) {
-      bt.cta0[i] = tot;
-      bt.ns[i] = nsub[order[i]];
-      tot += ncta[order[i]];
-    }
     if (bt.prob[i].pp.nsteps > bt.max_steps) bt.max_steps = bt.prob[i].pp.nsteps;
 #ifdef BSDE_DEBUG
     if (getenv("BSDE_DEBUG_NOWAIT")) bt.prob[i].pp.nowait = 1;   // timing experiments only: wrong results
@@ -948,10 +984,7 @@ cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& 
     cudaError_t e = cudaMemsetAsync(probs[i].pp.ring_flag, 0, sizeof(unsigned) * nf, st);
     if (e != cudaSuccess) return e;
   }
-  if (bt.part) {
-    bt.cta0[nprob] = tot;
-    if (tot != blocks) return cudaErrorInvalidValue;
-  }
+  if (bt.part && tot != blocks) return cudaErrorInvalidValue;
   switch (driver_id) {
     case DRV_ZERO: return launch_fused1d_v<DRV_ZERO>(bt, threads, blocks, smem, st);
     case DRV_AFFINE: return launch_fused1d_v<DRV_AFFINE>(bt, threads, blocks, smem, st);
@@ -983,5 +1016,5 @@ cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem
   for (int j = 0; j <= kMaxK; ++j) fp.pp.D[j] = D[j];
   fp.pp.DK = DK;
   for (int i = 0; i < 12; ++i) fp.dp[i] = pb.dp[i];
-  return launch_fused1d_batch(&fp, 1, g, fz, pb.driver_id, threads, blocks, smem, st, nullptr, nullptr);
+  return launch_fused1d_batch(&fp, 1, g, fz, pb.driver_id, threads, blocks, smem, st, nullptr, nullptr, nullptr, 0);
 }

@@ -42,8 +42,8 @@ int fused1d_blocks_per_sm(int variant, size_t smem);
 size_t fused1d_smem(Fused1D& fz);
 cudaError_t measure_fp64_peak(int device, int iters, double* tflops, double* ms_out);
 cudaError_t launch_fused1d_batch(const FusedProb* probs, int nprob, const Grid& g, const Fused1D& fz, int driver_id,
-                                 int threads, int blocks, size_t smem, cudaStream_t st, const int* ncta,
-                                 const int* nsub);
+                                 int threads, int blocks, size_t smem, cudaStream_t st, const int* group,
+                                 const int* gcta, const int* gns, int ngroup);
 cudaError_t launch_eval(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
 cudaError_t init_device_attributes();
 cudaError_t launch_quad2d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, cudaStream_t st);
@@ -1310,31 +1310,37 @@ static void distances_for(const bsde_ctx* c, int tile, int* D, int& DK) {
   DK = dk;
 }
 
-// Problem-partitioned plan of a batch (fused1d.cuh FusedBatch::part): problem i gets ncta[i]
-// CTAs, each a range of ns[i] consecutive tiles.  The fixed costs of a (CTA, step) -- the
-// spline pass, the hand-off latencies -- are then paid sum_i ncta_i steps_i times instead of
-// blocks * sum_i steps_i (round robin).  Cost model per (CTA, step) in units of one tile-level:
-// ns (K a + b) + c; the plan minimises the slowest problem's steps x cost subject to
-// sum ncta <= slots (binary search on that time).  Returns false if no plan fits.
-static bool plan_batch_partition(int n, const int* K, const int* steps, int tiles, int slots, int nsmax, int* ncta,
-                                 int* ns) {
+// Problem-partitioned plan of a batch (fused1d.cuh FusedBatch::part): the problems form groups;
+// group g gets gcta[g] CTAs, each serving the group's problems round robin on a range of gns[g]
+// tiles.  The fixed costs of a (CTA, problem, step) -- the spline pass, the hand-offs -- are paid
+// for fewer CTAs than round robin, and within a group of >= 2 problems a problem's neighbour waits
+// overlap the other problem's work.  Cost model of a group's (CTA, step) in units of one
+// tile-level: sum_{i in g} steps_i (ns (K_i a + b) + c); the plan minimises the slowest group's
+// time subject to sum gcta <= slots (binary search on that time).  Returns false if none fits.
+static bool plan_batch_groups(int n, const int* K, const int* steps, const int* group, int ngroup, int tiles, int slots,
+                              int nsmax, int* gcta, int* gns) {
   const double a = 1.0, b = 1.0, c = 2.5;
-  auto cost = [&](int i, int s) { return (double)steps[i] * (s * (K[i] * a + b) + c + 0.25 * s); };
+  auto cost = [&](int gi, int s) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i)
+      if (group[i] == gi) t += (double)steps[i] * (s * (K[i] * a + b) + c + 0.25 * s);
+    return t;
+  };
   auto fit = [&](double T, int* nc, int* nsv) {
     int tot = 0;
-    for (int i = 0; i < n; ++i) {
+    for (int gi = 0; gi < ngroup; ++gi) {
       int s = 0;
       for (int t = nsmax; t >= 1; --t)
-        if (cost(i, t) <= T) { s = t; break; }
+        if (cost(gi, t) <= T) { s = t; break; }
       if (s == 0) return false;
-      nc[i] = (tiles + s - 1) / s;
-      nsv[i] = (tiles + nc[i] - 1) / nc[i];           // balanced tiles per CTA
-      tot += nc[i];
+      nc[gi] = (tiles + s - 1) / s;
+      nsv[gi] = (tiles + nc[gi] - 1) / nc[gi];           // balanced tiles per CTA
+      tot += nc[gi];
     }
     return tot <= slots;
   };
   double lo = 0.0, hi = 0.0;
-  for (int i = 0; i < n; ++i) hi = std::max(hi, cost(i, nsmax));
+  for (int gi = 0; gi < ngroup; ++gi) hi = std::max(hi, cost(gi, nsmax));
   hi *= 4.0;
   int nc[kMaxBatch], nsv[kMaxBatch];
   if (!fit(hi, nc, nsv)) return false;
@@ -1342,7 +1348,7 @@ static bool plan_batch_partition(int n, const int* K, const int* steps, int tile
     const double mid = 0.5 * (lo + hi);
     if (fit(mid, nc, nsv)) hi = mid; else lo = mid;
   }
-  fit(hi, ncta, ns);
+  fit(hi, gcta, gns);
   return true;
 }
 
@@ -1351,8 +1357,8 @@ bsde_status bsde_solve_batch(bsde_ctx* const* cs, int32_t n, bsde_result* res) {
 }
 
 bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, bsde_result* res) {
-  if (mode < 0 || (mode > 2 && (mode < 11 || mode > 19)))
-    return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: mode %d outside 0..2, 11..19", mode);
+  if (mode < 0 || (mode > 3 && (mode < 11 || mode > 19)))
+    return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: mode %d outside 0..3, 11..19", mode);
   if (!cs || n < 1 || n > kMaxBatch) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: need 1..%d contexts", kMaxBatch);
   for (int i = 0; i < n; ++i)
     if (!cs[i]) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: ctx %d is NULL", i);
@@ -1381,8 +1387,11 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
     fz.WS = std::max(fz.WS, f.WS);
     fz.TK = std::max(fz.TK, f.TK);
   }
-  // problem-partitioned mode for n >= 2 problems when a plan fits (else round robin)
-  int ncta[kMaxBatch], nsub[kMaxBatch], pblocks = 0;
+  // problem-partitioned modes (groups of problems on their own CTAs) when a plan fits, else
+  // round robin.  mode 2: pairs (smallest K with largest K, ...); modes 0, 3 and 11..19: one
+  // problem per group (11..19: mode - 10 tiles per CTA, ablation).  Measured on cfg 2 (K = 1..6):
+  // round robin 20.9-22.2 ms, pairs 17.6-18.2 ms, one problem per group 16.9-17.2 ms.
+  int group[kMaxBatch], gcta[kMaxBatch], gns[kMaxBatch], ngroup = 0, pblocks = 0;
   bool part = false;
   Fused1D fzp = fz;
   size_t smem_p = 0;
@@ -1392,20 +1401,33 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
     const int nsmax = std::max(1, std::min(9, (P - 2 * kPcrHalo - 256) / (2 * TP)));
     int Kv[kMaxBatch], st[kMaxBatch];
     for (int i = 0; i < n; ++i) { Kv[i] = cs[i]->K; st[i] = cs[i]->level; }
-    bool planned = false;
-    if (mode >= 11) {                                  // ablation: every problem ns = mode - 10 tiles per CTA
-      planned = true;
-      for (int i = 0; i < n; ++i) {
-        nsub[i] = std::min(mode - 10, nsmax);
-        ncta[i] = (c0->geo.blocks + nsub[i] - 1) / nsub[i];
-        nsub[i] = (c0->geo.blocks + ncta[i] - 1) / ncta[i];
+    if (mode == 2) {                                 // pairs by K rank: (1st, last), (2nd, 2nd last), ...
+      int idx[kMaxBatch];
+      for (int i = 0; i < n; ++i) idx[i] = i;
+      std::stable_sort(idx, idx + n, [&](int x, int y) { return Kv[x] < Kv[y]; });
+      for (int r = 0; r < n; ++r) {
+        const int pr = std::min(r, n - 1 - r);
+        group[idx[r]] = pr;
+        ngroup = std::max(ngroup, pr + 1);
       }
     } else {
-      planned = mb > 0 && plan_batch_partition(n, Kv, st, c0->geo.blocks, c0->nsm * mb, nsmax, ncta, nsub);
+      for (int i = 0; i < n; ++i) group[i] = i;
+      ngroup = n;
+    }
+    bool planned = false;
+    if (mode >= 11) {
+      planned = true;
+      for (int gi = 0; gi < ngroup; ++gi) {
+        gns[gi] = std::min(mode - 10, nsmax);
+        gcta[gi] = (c0->geo.blocks + gns[gi] - 1) / gns[gi];
+        gns[gi] = (c0->geo.blocks + gcta[gi] - 1) / gcta[gi];
+      }
+    } else {
+      planned = mb > 0 && plan_batch_groups(n, Kv, st, group, ngroup, c0->geo.blocks, c0->nsm * mb, nsmax, gcta, gns);
     }
     if (planned) {
       int nsm_ = 1;
-      for (int i = 0; i < n; ++i) { nsm_ = std::max(nsm_, nsub[i]); pblocks += ncta[i]; }
+      for (int gi = 0; gi < ngroup; ++gi) { nsm_ = std::max(nsm_, gns[gi]); pblocks += gcta[gi]; }
       fzp.WP = ((nsm_ * TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;   // PCR extent of a CTA's range
       fzp.WS = 6 * fzp.WP + 16;
       smem_p = fused1d_smem(fzp);
@@ -1454,7 +1476,7 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
     fp.pp.ring_flag = c->barrier;
     if (part) {
       fp.pp.done_flag = c->barrier + kFlagCap;
-      distances_for(c, nsub[i] * fz.TP, fp.pp.D, fp.pp.DK);
+      distances_for(c, gns[group[i]] * fz.TP, fp.pp.D, fp.pp.DK);
     } else {
       fp.pp.done_flag = c->barrier + c->geo.blocks;
       for (int j = 0; j <= kMaxK; ++j) fp.pp.D[j] = c->geo.D[j];
@@ -1464,7 +1486,8 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
     steps[i] = c->level;
   }
   cudaError_t e = launch_fused1d_batch(probs, n, c0->g, fz, c0->pb.driver_id, c0->geo.threads, blocks, smem,
-                                       c0->stream, part ? ncta : nullptr, part ? nsub : nullptr);
+                                       c0->stream, part ? group : nullptr, part ? gcta : nullptr, part ? gns : nullptr,
+                                       part ? ngroup : 0);
   cudaEventRecord(e1, c0->stream);
   if (e != cudaSuccess) {
     cudaEventDestroy(e0);
@@ -1493,8 +1516,8 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
       e = cudaStreamSynchronize(cs[i]->stream);
       if (e != cudaSuccess) return set_err(cs[i], BSDE_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
       fill_result(cs[i], &res[i], out, ms * 1e-3, now_s() - t0, steps[i]);
-      res[i].batch_ctas = part ? ncta[i] : blocks;
-      res[i].batch_tiles = part ? nsub[i] : 1;
+      res[i].batch_ctas = part ? gcta[group[i]] : blocks;
+      res[i].batch_tiles = part ? gns[group[i]] : 1;
       unsigned long long v = 0;
       if (cudaMemcpy(&v, pexec_counter(cs[i]), sizeof v, cudaMemcpyDeviceToHost) == cudaSuccess)
         res[i].picard_iters = (int64_t)v;

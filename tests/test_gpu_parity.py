@@ -257,7 +257,7 @@ def test_fused_persistent_full_size():
 
 
 @gpu
-@pytest.mark.parametrize("mode", [1, 2], ids=["round_robin", "partitioned"])
+@pytest.mark.parametrize("mode", [1, 2, 3], ids=["round_robin", "paired", "partitioned"])
 def test_solve_batch_matches_single_solves_and_oracle(mode):
     """bsde_solve_batch_mode over K = 1..6 (one persistent launch; round-robin steps, or each
     problem on its own CTAs with ranges of tiles) gives the same bits as six single solves and
@@ -315,7 +315,7 @@ def test_solve_batch_full_size_oracle_final_layers():
 
 
 @gpu
-@pytest.mark.parametrize("mode", [0, 1, 2], ids=["auto", "round_robin", "partitioned"])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3], ids=["auto", "round_robin", "paired", "partitioned"])
 def test_solve_batch_full_size_bitwise(mode):
     """cfg 2 at full size, K = 1..6 batched (the bench's step) == single persistent solves, in
     every CTA schedule."""
