@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   grid_dep_wait();            // previous kernel in the stream has completed
   __syncthreads();
   uint32_t ph[4] = {0, 0, 0, 0};
-  unsigned pexec = 0;         // Picard iterations this thread executed in the current problem-step
+  unsigned pexec = 0;         // Picard iterations this thread executed (current problem-step, or the launch)
   int prefetched = 0;         // windows of the current problem already in flight
   // the warp that issues the next problem's copies during the epilogue: one without points
   // (its lanes would otherwise idle through the Picard iterations), else warp 0.  It touches
@@ -382,11 +382,11 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   auto unit_prob = [&](int u) { return pf + u / nunit_sub; };
   auto unit_lo = [&](int u) { return clo + (u % nunit_sub) * TP; };
 
+  const bool multi = pl - pf > 1;
   for (int it = 0; it < it_end; ++it) {
     // ================= pass 1: levels K..1, z and Picard of step it of every problem / tile
     // one relaxed read of every problem's flags + one acquire fence serve all problems' waits of
     // the pass; a CTA with a single problem waits with per-flag acquire loads instead (no fence)
-    const bool multi = pl - pf > 1;
     if (warp == 0 && it > 0 && multi) refresh_marks<0>(PB, bt.nprob, it, marks, bid, nb, pf, pl);
     for (int un = 0; un < nunits; ++un) {
       const int ip = unit_prob(un);
@@ -616,7 +616,8 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         if (!isfinite(y) || !isfinite(z)) atomicMin(s.bad, bad_key(pp.ring_mode ? pp.n0 - it : s.n, p));
       }
       PHASE_STAMP(18);
-      {   // executed Picard iterations of this problem (the roofline's executed-work figure)
+      if (multi) {   // executed Picard iterations of this problem (the roofline's executed work);
+                     // a one-problem CTA keeps counting in pexec and flushes once at the end
         const unsigned ex = __reduce_add_sync(0xffffffffu, pexec);
         if (lane == 0 && ex) atomicAdd(pcnt + ip, (unsigned long long)ex);
         pexec = 0;
@@ -819,6 +820,10 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       // barrier (cumulative over the CTA's stores)
       if (tid == publisher) st_release(pp.ring_flag + bid, (unsigned)it + 1);
     }
+  }
+  if (!multi && pl > pf) {
+    const unsigned ex = __reduce_add_sync(0xffffffffu, pexec);
+    if (lane == 0 && ex) atomicAdd(pcnt + pf, (unsigned long long)ex);
   }
   __syncthreads();
   if (tid < bt.nprob && PB[tid].s.picard_exec != nullptr && pcnt[tid] != 0) atomicAdd(PB[tid].s.picard_exec, pcnt[tid]);

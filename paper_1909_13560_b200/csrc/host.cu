@@ -764,7 +764,7 @@ void release(bsde_ctx* c) {
   if (c->tap1_off >= 0) arena_free(dev, c->tap1_off);
   if (c->boot_tap_off >= 0) arena_free(dev, c->boot_tap_off);
   if (c->boot_tap1_off >= 0) arena_free(dev, c->boot_tap1_off);
-  if (c->own_ws && c->ws) cudaFree(c->ws);
+  if (c->own_ws && c->ws) cudaFreeAsync(c->ws, c->stream);
   if (c->phase_ns) cudaFree(c->phase_ns);
   tfree(c);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -934,7 +934,14 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   }
   cudaError_t ce = cudaSetDevice(cfg->device);
   if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "cudaSetDevice(%d): %s", cfg->device, cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
-  ce = init_device_attributes();
+  {   // kernel attributes: once per device and process (they are per-function device state)
+    static std::mutex mu;
+    static bool done[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    const int dv = cfg->device >= 0 && cfg->device < 64 ? cfg->device : 0;
+    ce = done[dv] ? cudaSuccess : init_device_attributes();
+    if (ce == cudaSuccess) done[dv] = true;
+  }
   if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "kernel attributes: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
   if (cfg->stream) c->stream = (cudaStream_t)cfg->stream;
   else {
@@ -961,7 +968,9 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     c->ws = (char*)d_workspace;
     c->ws_bytes = bytes;
   } else {
-    ce = cudaMalloc((void**)&c->ws, lay.total);
+    // stream-ordered allocation from the device's default pool: a setup after a destroy reuses
+    // the freed block without a device synchronisation (small problems are setup-bound)
+    ce = cudaMallocAsync((void**)&c->ws, lay.total, c->stream);
     if (ce != cudaSuccess) {
       set_err(c, BSDE_ERR_RESOURCE_LIMIT, "cudaMalloc(%zu) failed: %s (grid %lld points)", lay.total,
               cudaGetErrorString(ce), (long long)c->g.npts);

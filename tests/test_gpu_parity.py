@@ -954,3 +954,54 @@ def test_fd_bicubic_reproduces_table9(row):
         assert s.shape[0] == int(row[3]) + 1
         r = s.solve()
     _check_row(row, abs(r.y0), float(np.hypot(r.z0[0] - 1, r.z0[1] - 1)))
+
+
+# ------------------------------------------------------------------ ABI: validation (host only), timers, diagnostics
+def test_validation_of_round2_config_fields_cpu():
+    """Setup-time validation of the r2 fields (host only, bsde_query_workspace / _partition_cfg):
+    Eq. 1 problems exclude the Ex. 2 driver, smoothing and slabs; CALL_X needs a forward SDE;
+    the FD-bicubic is 2-D with >= 6 points per axis; an in-process slab group cannot bootstrap."""
+    from paper_1909_13560_b200 import query_workspace, query_partition, BsdeError
+    ou = dict(W.ex1(3, 8, npts=101), sde="ou", sde_params=[0.1, 0, 0, 0, 0, 0, 1, 0, 0], bootstrap=1)
+    assert query_workspace(ou) > 0
+    for bad in (dict(W.ex2(3, 8, npts=101), sde="ou", sde_params=[0.1] + [0] * 5 + [1], bootstrap=1),
+                dict(W.black_scholes(3, 8, npts=101), sde="gbm", sde_params=[0.05, 0, 0, 0.2], bootstrap=1),   # smoothing
+                dict(W.ex1(3, 8, npts=101), terminal="call_x", terminal_params=[0, 1.0]),
+                dict(W.basket_3d(2, 4, 4, P=12), interp="fd_bicubic"),
+                dict(W.ex4_2d(3, 8, npts=5), interp="fd_bicubic")):
+        with pytest.raises(BsdeError) as ei:
+            query_workspace(bad)
+        assert ei.value.code == 1, bad
+    grp = dict(W.ex4_2d(3, 8, npts=257), bootstrap=1, bootstrap_substeps=2)
+    with pytest.raises(BsdeError) as ei:
+        query_partition(grp, 2, 0)
+    assert ei.value.code == 1
+
+
+@gpu
+def test_stage_timers_and_setup_time():
+    """bsde_result timers (r2): t_setup_s (host clock of bsde_setup), t_bootstrap_s (device time of
+    the K-1 initial layers), and with cfg.timing = 1 the spline / quadrature stages of the sweep."""
+    from paper_1909_13560_b200 import Solver
+    with Solver(dict(W.ex4_2d(3, 8, npts=65), bootstrap=1, bootstrap_substeps=2), timing=1) as s:
+        r = s.solve()
+    assert r.t_setup_s > 0 and r.t_bootstrap_s > 0 and r.t_spline_s > 0 and r.t_quad_s > 0
+    assert r.t_spline_s + r.t_quad_s <= r.t_sweep_s * 1.5 + 1e-3
+    assert r.t_total_s >= r.t_setup_s
+    with Solver(W.ex4_2d(3, 8, npts=65)) as s:           # timing off: only setup / bootstrap / sweep
+        r = s.solve()
+    assert r.t_spline_s == 0.0 and r.t_quad_s == 0.0 and r.t_setup_s > 0
+
+
+@gpu
+def test_non_finite_diagnostic_names_level_point_and_values():
+    """A solve that overflows (Ex. 1 driver -y^3 on a large polynomial terminal) fails with
+    NUMERICAL_DOMAIN and last_error naming the level n, t, the point i, x and y, z."""
+    from paper_1909_13560_b200 import Solver, BsdeError
+    spec = dict(W.ex1(1, 40, L=8, npts=201), terminal="poly", terminal_params=[0.0, 0.0, 0.0, 50.0])
+    with Solver(spec) as s:
+        with pytest.raises(BsdeError) as ei:
+            s.solve()
+    msg = str(ei.value)
+    assert ei.value.code == 4
+    assert "level n =" in msg and "point i =" in msg and "x =" in msg and "y =" in msg
