@@ -118,8 +118,10 @@ typedef struct {
                                 (R11)                          */
   int32_t  nranks, rank;     /* slab partition along axis 0 (d >= 2); 1/0 for one GPU.  Rank r
                                 owns rows [r P0/R, (r+1) P0/R) and keeps `halo` extra rows on
-                                each side (quadrature reach + cubic support + PCR decay),
-                                exchanged after every step                    */
+                                each side: reach + 3 rows of coefficients (SPIKE, slab_spline
+                                = 0) or reach + 3 + 37 rows of values (slab_spline = 1),
+                                exchanged every step.  With SPIKE and NCCL,
+                                bsde_eval / bsde_solve are collectives (every rank calls)     */
   const void* nccl_unique_id;/* nranks > 1: 128-byte ncclUniqueId from bsde_nccl_unique_id()
                                 (multi-process, one rank per GPU, halos by NCCL send/recv), or
                                 NULL for an in-process group driven by bsde_group_step/solve */
@@ -135,6 +137,14 @@ typedef struct {
   double   sde_params[12];
   int32_t  timing;           /* 1: per-stage CUDA-event timers (t_spline_s, t_quad_s, t_comm_s
                                 of bsde_result); 0: only setup / bootstrap / sweep times   */
+  int32_t  slab_spline;      /* nranks > 1: the axis-0 spline across slab interfaces.
+                                0 (default): SPIKE -- each rank solves its own rows with zero
+                                coupling, the 2 edge moments per line and rank are all-gathered,
+                                the 2 (R-1) interface system is solved (same inverse for every
+                                line) and the spike-vector correction applied; the halo is
+                                reach + 3 rows of final coefficients.
+                                1 (ablation): the axis-0 spline is re-solved redundantly over a
+                                values halo of reach + 3 + 37 rows (PCR decay, 5e-19)        */
 } bsde_config;
 
 typedef struct {

@@ -52,7 +52,7 @@ class bsde_config(C.Structure):
                 ("nranks", C.c_int32), ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("stream", C.c_void_p), ("device", C.c_int32), ("kernel_variant", C.c_int32),
                 ("interp", C.c_int32), ("sde_id", C.c_int32), ("sde_params", C.c_double * 12),
-                ("timing", C.c_int32)]
+                ("timing", C.c_int32), ("slab_spline", C.c_int32)]
 
 
 class bsde_result(C.Structure):
@@ -149,6 +149,7 @@ def make_config(spec: dict, device: int = 0, stream: int | None = None, kernel_v
     for k in range(12):
         c.sde_params[k] = float(sp[k])
     c.timing = int(timing)
+    c.slab_spline = int(spec.get("slab_spline", 0))
     return c
 
 

@@ -138,6 +138,17 @@ struct Persist1D {
 // buffers and progress flags.  CTAs run the problems' steps round-robin (step it of problem
 // 0, 1, ..., then step it + 1), so a problem's neighbour waits overlap the other problems'
 // work.  A single solve is a batch of one.
+constexpr int kMaxRanks = 16;
+struct SpikeArgs {
+  const double* gath;        // [R][F][2][plane] edges of every rank (side 0: first row, 1: last)
+  double* X;                 // [F][2][plane] this rank's m(r0 - 1), m(r1) (0 at global ends)
+  int64_t plane;             // values per axis-0 row (value layout)
+  int F, R;
+  // xL = sum_j wL[j] rhs_j, xR = sum_j wR[j] rhs_j; rhs_{2i} = last-row edge of rank i,
+  // rhs_{2i+1} = first-row edge of rank i + 1 (i = 0 .. R-2)
+  double wL[2 * kMaxRanks], wR[2 * kMaxRanks];
+};
+
 constexpr int kMaxBatch = 8;
 constexpr int kFlagCap = 8192;   // progress flags per kind and context (the workspace holds 2 x kFlagCap)
 struct FusedProb {

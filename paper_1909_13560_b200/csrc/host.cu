@@ -65,6 +65,12 @@ cudaError_t launch_bicubic_step(const StepArgs& s, const Grid& g, const Problem&
 cudaError_t launch_eval_bicubic(const Grid& g, const double* slot, int F, const double* x, double* out, cudaStream_t st);
 cudaError_t launch_step3d(const StepArgs& s, const Grid& g, const Problem& pb, int WC, double* A, double* acc,
                           int decompose, cudaStream_t st, int64_t* launches);
+cudaError_t launch_spike_reduce(const SpikeArgs& a, cudaStream_t st);
+cudaError_t launch_spike_correct(double* slot, int64_t cfield, int64_t cs0, const double* XC, int64_t plane_c,
+                                 const double* sLR, int64_t row_lo, int64_t n, int nak_a, int nak_b, int F,
+                                 cudaStream_t st);
+cudaError_t launch_spline_slab(const Grid& g, const double* values, int F, double* slot, double* tmp0, double* tmp1,
+                               bool first, bool last, double* edge, cudaStream_t st, int64_t* launches);
 }  // namespace bsde
 
 using namespace bsde;
@@ -123,6 +129,19 @@ struct bsde_ctx {
   int64_t P0g = 0, r0 = 0, r1 = 0, lo_e = 0, hi_e = 0, halo = 0;
   ncclComm_t comm = nullptr;        // multi-process mode (nccl_unique_id given)
   bool grouped = false;             // in-process group mode (bsde_group_*)
+  // SPIKE slab spline (cfg.slab_spline = 0, nranks > 1): per ring slot the edge
+  // moments [F][2][plane] of the local axis-0 solve; the all-gathered edges [R][F][2][plane]; the
+  // interface moments X [F][2][plane] and their tensor splines XC [F][2][plane_c]; the spike
+  // vectors S^L, S^R of the own unknown rows [row_lo, row_lo + spk_n) (local)
+  bool spike = false;
+  double *edge = nullptr, *gath = nullptr, *xs = nullptr, *xc = nullptr, *xtmp = nullptr, *slr = nullptr;
+  int64_t plane_v = 0, plane_c = 0, spk_n = 0, spk_row_lo = 0;
+  SpikeArgs spk{};
+  Grid gplane{};                    // the axes 1 .. d-1 grid of the interface planes
+  std::vector<double> h_slr;
+  unsigned pending = 0;             // in-process group: ring slots whose interface correction is due
+  bool prebuilt = false;            // in-process group: the newest level's spline is built (group step)
+  bool rs_ready = false;            // in-process group: the scratch slot holds the corrected newest level
   std::string err;
   bool closed_form = true;
   // timing: host-clock setup time; CUDA-event stage timers (bootstrap always, the others with
@@ -418,7 +437,9 @@ bsde_status plan_partition(bsde_ctx* c) {
       const int q = c->taps[((size_t)(j - 1) * c->d + 0) * c->L + l].q;
       reach = std::max(reach, q < 0 ? -q : q);
     }
-  c->halo = reach + 3 + kPcrHalo + 6;
+  // SPIKE: the final coefficients are exchanged, reach + 3 rows (the 4-row stencil of the farthest
+  // tap); the redundant-halo ablation re-solves the axis-0 spline over the halo: + PCR decay
+  c->halo = c->cfg.slab_spline == 0 ? reach + 3 : reach + 3 + kPcrHalo + 6;
   for (int r = 0; r < c->nranks; ++r) {
     int64_t a, b;
     rank_rows(c->P0g, c->nranks, r, a, b);
@@ -475,6 +496,9 @@ bsde_status validate(const bsde_config* cfg, bsde_ctx* c) {
   if (cfg->sde_id != BSDE_SDE_BROWNIAN && cfg->smoothing)
     return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "terminal smoothing is defined for X = W payoffs only (R11)");
   if (cfg->interp < 0 || cfg->interp > 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "interp %d outside 0..1", cfg->interp);
+  if (cfg->slab_spline < 0 || cfg->slab_spline > 1)
+    return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "slab_spline %d outside 0..1", cfg->slab_spline);
+  if (cfg->nranks > kMaxRanks) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "nranks %d > %d", cfg->nranks, kMaxRanks);
   if (cfg->interp == BSDE_INTERP_FD_BICUBIC && (cfg->d != 2 || cfg->sde_id != BSDE_SDE_BROWNIAN || cfg->nranks > 1))
     return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "FD-bicubic interpolation is the paper's 2-D scheme: d = 2, X = W, one rank");
   if (cfg->driver_id == BSDE_DRV_EX2 && cfg->d != 1) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "EX2 driver is 1-D");
@@ -577,7 +601,7 @@ bool use_fused3d(const bsde_config* cfg) {
 }
 
 struct Layout {
-  size_t values, ring, tmp0, tmp1, a3, acc3, picard, bad, barrier, dres, total;
+  size_t values, ring, tmp0, tmp1, a3, acc3, picard, bad, barrier, dres, spike, total;
 };
 // values: 2 ping-pong buffers of F * npts (the fused 1-D step reads level n+1 while
 // other CTAs write level n)
@@ -585,7 +609,7 @@ struct Layout {
 // fused3d: the d = 3 fused path's per-level plane stacks (L x F x local planes) and the
 // 5 partial sums per owned point; aff2: the d = 2 affine path's axis-0 operators of every
 // level (K x 2 x F x owned rows, in the a3 region)
-Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d, bool aff2) {
+Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d, bool aff2, int R = 1, bool spike = false) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   Layout L{};
   size_t off = 0;
@@ -606,6 +630,13 @@ Layout layout(const Grid& g, int F, int K, int nodes, bool fused3d, bool aff2) {
   L.bad = off; off += 256;
   L.barrier = off; off += al(sizeof(unsigned) * 2 * kFlagCap);  // fused-kernel progress flags (ring, done)
   L.dres = off; off += 256;
+  L.spike = off;
+  if (spike && g.d >= 2) {            // edges per slot, gathered edges, X, XC, scratch, spike vectors
+    const size_t pv = (size_t)(g.npts / g.P[0]), pc = (size_t)g.cstride[0];
+    off += al(sizeof(double) * (size_t)(K + 3) * F * 2 * pv) + al(sizeof(double) * (size_t)R * F * 2 * pv) +
+           al(sizeof(double) * F * 2 * pv) + al(sizeof(double) * F * 2 * pc) + al(sizeof(double) * pc) +
+           al(sizeof(double) * 2 * (size_t)(g.P[0] + 4));
+  }
   L.total = off;
   return L;
 }
@@ -615,6 +646,10 @@ double now_s() {
 }
 
 bsde_status exchange_nccl(bsde_ctx* c);
+bsde_status finish_level(bsde_ctx* c, int slot);
+
+// SPIKE edge moments of ring slot `slot`
+static double* edge_slot(const bsde_ctx* c, int slot) { return c->edge + (int64_t)slot * c->F * 2 * c->plane_v; }
 
 // interpolant of the newest values into ring slot `slot`: tensor not-a-knot spline (B-spline
 // coefficients), or the Hermite data of the FD-bicubic surfaces (interp = 1)
@@ -622,6 +657,9 @@ cudaError_t build_level(bsde_ctx* c, int slot) {
   double* dst = c->ring + (int64_t)slot * c->F * c->g.cfield;
   if (c->cfg.interp == BSDE_INTERP_FD_BICUBIC)
     return launch_hermite(c->g, c->vbuf[c->cur], c->F, dst, c->stream, &c->launches);
+  if (c->spike)          // the local part of the SPIKE solve; finish_level applies the correction
+    return launch_spline_slab(c->g, c->vbuf[c->cur], c->F, dst, c->tmp0, c->tmp1, c->rank == 0,
+                              c->rank == c->nranks - 1, edge_slot(c, slot), c->stream, &c->launches);
   return launch_spline(c->g, c->vbuf[c->cur], c->F, dst, c->tmp0, c->tmp1, c->stream, &c->launches);
 }
 
@@ -672,8 +710,12 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
     if (timing) tstage(c, ST_QUAD, t0);
   } else {
     cudaEvent_t t0 = timing ? tmark(c) : nullptr;
-    e = build_level(c, slots[0]);
+    e = c->prebuilt ? cudaSuccess : build_level(c, slots[0]);
     if (timing) tstage(c, ST_SPLINE, t0);
+    if (e == cudaSuccess && !c->prebuilt) {
+      const bsde_status fs = finish_level(c, slots[0]);        // SPIKE interface correction (NCCL)
+      if (fs) return fs;
+    }
     cudaEvent_t t1 = timing ? tmark(c) : nullptr;
     if (e == cudaSuccess) {
       if (c->pb.sde_id != 0)                                   // forward SDE: per-point Euler samples
@@ -705,22 +747,26 @@ struct HaloPlan {
   int64_t send_hi_off, send_hi_rows;   // to rank+1
   int64_t recv_hi_off, recv_hi_rows;   // from rank+1
 };
-HaloPlan halo_plan(const bsde_ctx* c) {
+// rows of a halo of h rows (clipped to the grid); SPIKE exchanges 1 row of values (the
+// second difference of the interface rows) and h = halo rows of final coefficients
+HaloPlan halo_plan(const bsde_ctx* c, int64_t h) {
   HaloPlan p{};
   if (c->rank > 0) {
-    p.recv_lo_off = 0;
-    p.recv_lo_rows = c->r0 - c->lo_e;                          // my rows [lo_e, r0)
+    p.recv_lo_rows = std::min<int64_t>(h, c->r0);                // my rows [r0 - rows, r0)
+    p.recv_lo_off = c->r0 - p.recv_lo_rows - c->lo_e;
     p.send_lo_off = c->r0 - c->lo_e;
-    p.send_lo_rows = std::min<int64_t>(c->P0g - c->r0, c->halo);  // rank-1's rows [r0, r0 + halo)
+    p.send_lo_rows = std::min<int64_t>(c->P0g - c->r0, h);      // rank-1's rows [r0, r0 + rows)
   }
   if (c->rank < c->nranks - 1) {
     p.recv_hi_off = c->r1 - c->lo_e;
-    p.recv_hi_rows = c->hi_e - c->r1;                          // my rows [r1, hi_e)
-    p.send_hi_rows = std::min<int64_t>(c->r1, c->halo);        // rank+1's rows [r1 - halo, r1)
+    p.recv_hi_rows = std::min<int64_t>(h, c->P0g - c->r1);      // my rows [r1, r1 + rows)
+    p.send_hi_rows = std::min<int64_t>(c->r1, h);               // rank+1's rows [r1 - rows, r1)
     p.send_hi_off = c->r1 - p.send_hi_rows - c->lo_e;
   }
   return p;
 }
+// the values halo exchanged after every step
+HaloPlan halo_plan(const bsde_ctx* c) { return halo_plan(c, c->spike ? 1 : c->halo); }
 
 int64_t row_len(const bsde_ctx* c) { return c->g.npts / c->g.P[0]; }
 
@@ -751,10 +797,185 @@ bsde_status exchange_nccl(bsde_ctx* c) {
   return BSDE_OK;
 }
 
+// ------------------------------------------------------------------ SPIKE slab spline (§7)
+// unknown-row range of rank p's axis-0 moment system (global rows): Dirichlet fold nodes fa, fb
+static void spike_folds(int64_t P0g, int R, int p, int64_t& fa, int64_t& fb) {
+  int64_t r0, r1;
+  rank_rows(P0g, R, p, r0, r1);
+  fa = p == 0 ? 1 : r0 - 1;
+  fb = p == R - 1 ? P0g - 2 : r1;
+}
+// S^L_k of a system of n unknown rows: the response at row k to a unit moment at the left fold
+static long double spike_sl(int64_t n, int64_t k) {
+  const long double rho = sqrtl(3.0L) - 2.0L;
+  return (powl(rho, (long double)(k + 1)) - powl(rho, (long double)(2 * n + 1 - k))) /
+         (1.0L - powl(rho, (long double)(2 * n + 2)));
+}
+bsde_status spike_setup(bsde_ctx* c, char* base) {
+  const Grid& g = c->g;
+  const int R = c->nranks, F = c->F, p = c->rank;
+  if (R > kMaxRanks) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "SPIKE: nranks %d > %d", R, kMaxRanks);
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  c->plane_v = g.npts / g.P[0];
+  c->plane_c = g.cstride[0];
+  const size_t pv = (size_t)c->plane_v, pc = (size_t)c->plane_c;
+  char* q = base;
+  c->edge = (double*)q; q += al(sizeof(double) * (size_t)(c->K + 3) * F * 2 * pv);
+  c->gath = (double*)q; q += al(sizeof(double) * (size_t)R * F * 2 * pv);
+  c->xs = (double*)q; q += al(sizeof(double) * F * 2 * pv);
+  c->xc = (double*)q; q += al(sizeof(double) * F * 2 * pc);
+  c->xtmp = (double*)q; q += al(sizeof(double) * pc);
+  c->slr = (double*)q;
+  // the reduced system of the 2 (R - 1) interface moments u_i = m(r1_i - 1), v_i = m(r1_i):
+  //   u_i - sA_i v_i - sB_i u_{i-1} = (last-row edge of rank i)
+  //   v_i - sA_{i+1} u_i - sB_{i+1} v_{i+1} = (first-row edge of rank i + 1)
+  // sA = S^L[0] = S^R[n-1], sB = S^L[n-1] = S^R[0]; the same matrix for every line: invert it once
+  const int M = 2 * (R - 1);
+  std::vector<long double> sA(R), sB(R), A((size_t)M * M, 0.0L), Inv((size_t)M * M, 0.0L);
+  for (int r = 0; r < R; ++r) {
+    int64_t fa, fb;
+    spike_folds(c->P0g, R, r, fa, fb);
+    const int64_t n = fb - fa - 1;
+    if (n < 2) return set_err(c, BSDE_ERR_INVALID_ARGUMENT, "SPIKE: rank %d has %lld unknown rows", r, (long long)n);
+    sA[r] = spike_sl(n, 0);
+    sB[r] = spike_sl(n, n - 1);
+  }
+  for (int i = 0; i < R - 1; ++i) {
+    A[(size_t)(2 * i) * M + 2 * i] = 1.0L;
+    A[(size_t)(2 * i) * M + 2 * i + 1] = -sA[i];
+    if (i > 0) A[(size_t)(2 * i) * M + 2 * (i - 1)] = -sB[i];
+    A[(size_t)(2 * i + 1) * M + 2 * i + 1] = 1.0L;
+    A[(size_t)(2 * i + 1) * M + 2 * i] = -sA[i + 1];
+    if (i + 1 < R - 1) A[(size_t)(2 * i + 1) * M + 2 * (i + 1) + 1] = -sB[i + 1];
+  }
+  for (int i = 0; i < M; ++i) Inv[(size_t)i * M + i] = 1.0L;
+  for (int k = 0; k < M; ++k) {                   // Gauss-Jordan with partial pivoting
+    int piv = k;
+    for (int i = k + 1; i < M; ++i)
+      if (fabsl(A[(size_t)i * M + k]) > fabsl(A[(size_t)piv * M + k])) piv = i;
+    for (int j = 0; j < M; ++j) {
+      std::swap(A[(size_t)k * M + j], A[(size_t)piv * M + j]);
+      std::swap(Inv[(size_t)k * M + j], Inv[(size_t)piv * M + j]);
+    }
+    const long double dk = A[(size_t)k * M + k];
+    for (int j = 0; j < M; ++j) { A[(size_t)k * M + j] /= dk; Inv[(size_t)k * M + j] /= dk; }
+    for (int i = 0; i < M; ++i) {
+      if (i == k) continue;
+      const long double m = A[(size_t)i * M + k];
+      if (m == 0.0L) continue;
+      for (int j = 0; j < M; ++j) { A[(size_t)i * M + j] -= m * A[(size_t)k * M + j]; Inv[(size_t)i * M + j] -= m * Inv[(size_t)k * M + j]; }
+    }
+  }
+  c->spk = SpikeArgs{};
+  c->spk.gath = c->gath;
+  c->spk.X = c->xs;
+  c->spk.plane = c->plane_v;
+  c->spk.F = F;
+  c->spk.R = R;
+  for (int j = 0; j < M; ++j) {
+    c->spk.wL[j] = p > 0 ? (double)Inv[(size_t)(2 * (p - 1)) * M + j] : 0.0;      // m(r0 - 1) = u_{p-1}
+    c->spk.wR[j] = p < R - 1 ? (double)Inv[(size_t)(2 * p + 1) * M + j] : 0.0;    // m(r1) = v_p
+  }
+  // own spike vectors, local rows [row_lo, row_lo + n)
+  int64_t fa, fb;
+  spike_folds(c->P0g, R, p, fa, fb);
+  c->spk_n = fb - fa - 1;
+  c->spk_row_lo = fa + 1 - c->lo_e;
+  c->h_slr.assign((size_t)2 * c->spk_n, 0.0);
+  for (int64_t k = 0; k < c->spk_n; ++k) {
+    c->h_slr[(size_t)k] = (double)spike_sl(c->spk_n, k);
+    c->h_slr[(size_t)(c->spk_n + k)] = (double)spike_sl(c->spk_n, c->spk_n - 1 - k);
+  }
+  cudaError_t e = cudaMemcpyAsync(c->slr, c->h_slr.data(), sizeof(double) * c->h_slr.size(), cudaMemcpyHostToDevice,
+                                  c->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->xc, 0, sizeof(double) * F * 2 * pc, c->stream);   // pads stay 0
+  if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "SPIKE setup: %s", cudaGetErrorString(e));
+  // the interface planes: a (d-1)-dimensional grid of axes 1 .. d-1 (same coefficient layout as a
+  // slot's axis-0 row)
+  Grid& gp = c->gplane;
+  gp = Grid{};
+  gp.d = g.d - 1;
+  gp.npts = 1;
+  for (int a = 0; a < 3; ++a) { gp.P[a] = 1; gp.vstride[a] = 0; gp.cstride[a] = 0; }
+  for (int a = 0; a < gp.d; ++a) {
+    gp.P[a] = g.P[a + 1];
+    gp.xlo[a] = g.xlo[a + 1]; gp.xhi[a] = g.xhi[a + 1]; gp.dx[a] = g.dx[a + 1];
+    gp.npts *= gp.P[a];
+  }
+  gp.vstride[gp.d - 1] = 1;
+  for (int a = gp.d - 2; a >= 0; --a) gp.vstride[a] = gp.vstride[a + 1] * gp.P[a + 1];
+  for (int a = 0; a < gp.d; ++a) gp.cstride[a] = g.cstride[a + 1];
+  gp.cfield = c->plane_c;
+  gp.cpad = 0;
+  gp.off0 = 0; gp.Pg0 = gp.P[0]; gp.own0 = 0; gp.nown0 = gp.P[0];
+  return BSDE_OK;
+}
+
+// X = the interface moments of this rank from the gathered edges, their splines XC, the
+// correction of the slot's coefficients (one rank; the gather is done)
+static cudaError_t spike_apply(bsde_ctx* c, int slot) {
+  cudaError_t e = launch_spike_reduce(c->spk, c->stream);
+  ++c->launches;
+  if (e == cudaSuccess) e = launch_spline(c->gplane, c->xs, 2 * c->F, c->xc, c->xtmp, nullptr, c->stream, &c->launches);
+  if (e != cudaSuccess) return e;
+  double* dst = c->ring + (int64_t)slot * c->F * c->g.cfield;
+  e = launch_spike_correct(dst, c->g.cfield, c->g.cstride[0], c->xc, c->plane_c, c->slr, c->spk_row_lo, c->spk_n,
+                           c->rank == 0, c->rank == c->nranks - 1, c->F, c->stream);
+  ++c->launches;
+  return e;
+}
+
+// halo rows of ring slot `slot`'s final coefficients (SPIKE): local rows [r0 - h, r0) from
+// rank - 1 and [r1, r1 + h) from rank + 1 (coefficient storage row = local row + 1)
+bsde_status exchange_coef_nccl(bsde_ctx* c, int slot) {
+  const HaloPlan hp = halo_plan(c, c->halo);
+  const int64_t rl = c->g.cstride[0];
+  double* v = c->ring + (int64_t)slot * c->F * c->g.cfield + rl;      // storage row 1 = local row 0
+  ncclResult_t nr = ncclGroupStart();
+  for (int f = 0; f < c->F && nr == ncclSuccess; ++f) {
+    double* b = v + (int64_t)f * c->g.cfield;
+    if (c->rank > 0) {
+      nr = ncclSend(b + hp.send_lo_off * rl, (size_t)(hp.send_lo_rows * rl), ncclDouble, c->rank - 1, c->comm, c->stream);
+      if (nr == ncclSuccess)
+        nr = ncclRecv(b + hp.recv_lo_off * rl, (size_t)(hp.recv_lo_rows * rl), ncclDouble, c->rank - 1, c->comm, c->stream);
+    }
+    if (c->rank < c->nranks - 1 && nr == ncclSuccess) {
+      nr = ncclSend(b + hp.send_hi_off * rl, (size_t)(hp.send_hi_rows * rl), ncclDouble, c->rank + 1, c->comm, c->stream);
+      if (nr == ncclSuccess)
+        nr = ncclRecv(b + hp.recv_hi_off * rl, (size_t)(hp.recv_hi_rows * rl), ncclDouble, c->rank + 1, c->comm, c->stream);
+    }
+  }
+  ncclResult_t ne = ncclGroupEnd();
+  if (nr != ncclSuccess || ne != ncclSuccess)
+    return set_err(c, BSDE_ERR_COMM, "coefficient halo exchange: %s", ncclGetErrorString(nr != ncclSuccess ? nr : ne));
+  return BSDE_OK;
+}
+
+// the interface correction of a freshly built slot: NCCL ranks all-gather the edges and finish
+// now; an in-process group member defers it to the group (bsde_group_step)
+bsde_status finish_level(bsde_ctx* c, int slot) {
+  if (!c->spike) return BSDE_OK;
+  if (c->grouped) {
+    c->pending |= 1u << slot;
+    return BSDE_OK;
+  }
+  cudaEvent_t t0 = c->cfg.timing && !c->in_setup ? tmark(c) : nullptr;
+  const size_t cnt = (size_t)c->F * 2 * c->plane_v;
+  ncclResult_t nr = ncclAllGather(edge_slot(c, slot), c->gath, cnt, ncclDouble, c->comm, c->stream);
+  if (nr != ncclSuccess) return set_err(c, BSDE_ERR_COMM, "edge all-gather: %s", ncclGetErrorString(nr));
+  tstage(c, ST_COMM, t0);
+  cudaError_t e = spike_apply(c, slot);
+  if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "SPIKE correction: %s", cudaGetErrorString(e));
+  cudaEvent_t t1 = c->cfg.timing && !c->in_setup ? tmark(c) : nullptr;
+  bsde_status st = exchange_coef_nccl(c, slot);
+  tstage(c, ST_COMM, t1);
+  return st;
+}
+
 bsde_status spline_into(bsde_ctx* c, int slot) {
   cudaError_t e = build_level(c, slot);
   if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "spline kernel: %s", cudaGetErrorString(e));
-  return BSDE_OK;
+  return finish_level(c, slot);
 }
 
 void release(bsde_ctx* c) {
@@ -793,6 +1014,14 @@ bsde_status eval_point(bsde_ctx* c, double* out) {
   const double u0 = (0.0 - c->g.xlo[0]) / c->g.dx[0];
   int64_t row = on_grid ? (c->P0g - 1) / 2 : std::min<int64_t>(std::max<int64_t>((int64_t)floor(u0), 0), c->P0g - 2);
   const bool owner = row >= c->r0 && row < c->r1;
+  // SPIKE: the newest level's spline is a collective of every rank (NCCL), or built by the group
+  const bool spike_rs = c->spike && !on_grid;
+  if (spike_rs && !c->grouped) {
+    bsde_status st = spline_into(c, c->RS);
+    if (st) return st;
+  }
+  if (spike_rs && c->grouped && !c->rs_ready)
+    return set_err(c, BSDE_ERR_STATE, "slab group member: the evaluation spline is built by bsde_group_solve");
   if (owner) {
     if (on_grid) {
       int64_t idx = (row - c->lo_e) * c->g.vstride[0];
@@ -804,8 +1033,10 @@ bsde_status eval_point(bsde_ctx* c, double* out) {
       }
     } else {
       const double x[3] = {0, 0, 0};
-      bsde_status st = spline_into(c, c->RS);                 // newest level -> scratch slot
-      if (st) return st;
+      if (!spike_rs) {
+        bsde_status st = spline_into(c, c->RS);               // newest level -> scratch slot
+        if (st) return st;
+      }
       cudaError_t e = c->cfg.interp == BSDE_INTERP_FD_BICUBIC
                           ? launch_eval_bicubic(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, x, c->dres, c->stream)
                           : launch_eval(c->g, c->ring + (int64_t)c->RS * c->F * c->g.cfield, c->F, x, c->dres, c->stream);
@@ -869,6 +1100,63 @@ bsde_status group_exchange(bsde_ctx** cs, int n) {
   return BSDE_OK;
 }
 
+static bsde_status group_sync(bsde_ctx** cs, int n) {
+  for (int r = 0; r < n; ++r) {
+    cudaSetDevice(cs[r]->cfg.device);
+    cudaError_t e = cudaStreamSynchronize(cs[r]->stream);
+    if (e != cudaSuccess) return set_err(cs[r], BSDE_ERR_CUDA, "group sync: %s", cudaGetErrorString(e));
+  }
+  return BSDE_OK;
+}
+
+// SPIKE interface correction of ring slot `slot` across an in-process group: gather every
+// member's edge moments (peer copies), correct each member's slot, then copy the coefficient
+// halo rows from the neighbours
+bsde_status group_finish(bsde_ctx** cs, int n, int slot) {
+  bsde_status st = group_sync(cs, n);
+  if (st) return st;
+  for (int r = 0; r < n; ++r) {
+    bsde_ctx* c = cs[r];
+    cudaSetDevice(c->cfg.device);
+    const size_t cnt = (size_t)c->F * 2 * c->plane_v;
+    for (int q = 0; q < n; ++q) {
+      cudaError_t e = cudaMemcpyPeerAsync(c->gath + (int64_t)q * cnt, c->cfg.device, edge_slot(cs[q], slot),
+                                          cs[q]->cfg.device, sizeof(double) * cnt, c->stream);
+      if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "edge gather: %s", cudaGetErrorString(e));
+    }
+    cudaError_t e = spike_apply(c, slot);
+    if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "SPIKE correction: %s", cudaGetErrorString(e));
+  }
+  if ((st = group_sync(cs, n))) return st;
+  for (int r = 0; r < n; ++r) {
+    bsde_ctx* c = cs[r];
+    const HaloPlan hp = halo_plan(c, c->halo);
+    const int64_t rl = c->g.cstride[0];
+    cudaSetDevice(c->cfg.device);
+    for (int side = 0; side < 2; ++side) {
+      const int nbr = side == 0 ? r - 1 : r + 1;
+      if (nbr < 0 || nbr >= n) continue;
+      bsde_ctx* o = cs[nbr];
+      const HaloPlan ho = halo_plan(o, o->halo);
+      const int64_t rows = side == 0 ? hp.recv_lo_rows : hp.recv_hi_rows;
+      const int64_t dst_off = side == 0 ? hp.recv_lo_off : hp.recv_hi_off;
+      const int64_t src_off = side == 0 ? ho.send_hi_off : ho.send_lo_off;
+      const int64_t src_rows = side == 0 ? ho.send_hi_rows : ho.send_lo_rows;
+      if (rows != src_rows)
+        return set_err(c, BSDE_ERR_COMM, "coefficient halo plan mismatch (%lld vs %lld rows)", (long long)rows,
+                       (long long)src_rows);
+      for (int f = 0; f < c->F; ++f) {
+        double* dst = c->ring + (int64_t)slot * c->F * c->g.cfield + (int64_t)f * c->g.cfield + (1 + dst_off) * rl;
+        const double* src = o->ring + (int64_t)slot * o->F * o->g.cfield + (int64_t)f * o->g.cfield + (1 + src_off) * rl;
+        cudaError_t e = cudaMemcpyPeerAsync(dst, c->cfg.device, src, o->cfg.device, sizeof(double) * rows * rl, c->stream);
+        if (e != cudaSuccess) return set_err(c, BSDE_ERR_CUDA, "coefficient halo copy: %s", cudaGetErrorString(e));
+      }
+    }
+  }
+  for (int r = 0; r < n; ++r) cs[r]->pending &= ~(1u << slot);
+  return group_sync(cs, n);
+}
+
 // ------------------------------------------------------------------ ABI
 extern "C" {
 
@@ -879,7 +1167,8 @@ bsde_status bsde_query_workspace(const bsde_config* cfg, size_t* bytes) {
   const int K = std::max(cfg->Ky, cfg->Kz);
   Grid g{};
   fill_grid(cfg, g, (cfg->T - cfg->t0) / cfg->N);
-  *bytes = layout(g, 1 + cfg->d, K, cfg->L, use_fused3d(cfg), use_aff2(cfg)).total;
+  *bytes = layout(g, 1 + cfg->d, K, cfg->L, use_fused3d(cfg), use_aff2(cfg), cfg->nranks,
+                  cfg->nranks > 1 && cfg->slab_spline == 0).total;
   return BSDE_OK;
 }
 
@@ -959,7 +1248,8 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     }
   }
   // memory
-  Layout lay = layout(c->g, c->F, c->K, c->L, use_fused3d(cfg), use_aff2(cfg));
+  c->spike = c->nranks > 1 && cfg->slab_spline == 0 && c->d >= 2;
+  Layout lay = layout(c->g, c->F, c->K, c->L, use_fused3d(cfg), use_aff2(cfg), c->nranks, c->spike);
   if (d_workspace) {
     if (bytes < lay.total) {
       set_err(c, BSDE_ERR_RESOURCE_LIMIT, "workspace of %zu bytes < required %zu", bytes, lay.total);
@@ -991,6 +1281,9 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
   c->bad = (unsigned long long*)(c->ws + lay.bad);
   c->barrier = (unsigned*)(c->ws + lay.barrier);
   c->dres = (double*)(c->ws + lay.dres);
+  if (c->spike) {
+    if ((st = spike_setup(c, c->ws + lay.spike))) return fail(st);
+  }
 #ifdef BSDE_DEBUG
   if (getenv("BSDE_PHASE_TIMING")) {      // debug build only: per-CTA phase stamps of the fused 1-D kernel
     if (cudaMalloc((void**)&c->phase_ns, (size_t)8 * 32 * 600 * 1100) != cudaSuccess) c->phase_ns = nullptr;
@@ -1616,6 +1909,30 @@ bsde_status bsde_group_step(bsde_ctx** cs, int32_t n) {
   for (int r = 0; r < n; ++r)
     if (!cs[r] || cs[r]->rank != r || cs[r]->nranks != n || (n > 1 && !cs[r]->grouped))
       return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "group member %d is not rank %d of %d (in-process mode)", r, r, n);
+  if (n > 1 && cs[0]->spike) {
+    if (cs[0]->level <= 0) return set_err(cs[0], BSDE_ERR_STATE, "already at n = 0");
+    // initial levels built in bsde_setup, then the newest level: SPIKE correction across the group
+    for (int slot = 0; slot <= cs[0]->RS; ++slot)
+      if (cs[0]->pending & (1u << slot)) {
+        bsde_status st = group_finish(cs, n, slot);
+        if (st) return st;
+      }
+    const int slot = cs[0]->level % cs[0]->RS;
+    for (int r = 0; r < n; ++r) {
+      cudaSetDevice(cs[r]->cfg.device);
+      cudaError_t e = build_level(cs[r], slot);
+      if (e != cudaSuccess) return set_err(cs[r], BSDE_ERR_CUDA, "spline kernel: %s", cudaGetErrorString(e));
+    }
+    bsde_status st = group_finish(cs, n, slot);
+    if (st) return st;
+    for (int r = 0; r < n; ++r) {
+      cs[r]->prebuilt = true;
+      st = step_internal(cs[r]);
+      cs[r]->prebuilt = false;
+      if (st) return st;
+    }
+    return group_exchange(cs, n);
+  }
   for (int r = 0; r < n; ++r) {
     bsde_status st = step_internal(cs[r]);
     if (st) return st;
@@ -1633,15 +1950,30 @@ bsde_status bsde_group_solve(bsde_ctx** cs, int32_t n, bsde_result* res) {
     ++steps;
   }
   double out[4] = {0, 0, 0, 0};
+  if (n > 1 && cs[0]->spike) {                 // the newest level's corrected spline in the scratch slot
+    for (int r = 0; r < n; ++r) {
+      cudaSetDevice(cs[r]->cfg.device);
+      cudaError_t e = build_level(cs[r], cs[r]->RS);
+      if (e != cudaSuccess) return set_err(cs[r], BSDE_ERR_CUDA, "spline kernel: %s", cudaGetErrorString(e));
+    }
+    bsde_status st = group_finish(cs, n, cs[0]->RS);
+    if (st) return st;
+    for (int r = 0; r < n; ++r) cs[r]->rs_ready = true;
+  }
   for (int r = 0; r < n; ++r) {
     cudaSetDevice(cs[r]->cfg.device);
     bsde_status st = check_bad(cs[r]);
-    if (st) return st;
-    double o[4];
-    st = eval_point(cs[r], o);
-    if (st) return st;
-    for (int f = 0; f < 4; ++f) out[f] += o[f];
+    if (st == BSDE_OK) {
+      double o[4];
+      st = eval_point(cs[r], o);
+      for (int f = 0; f < 4 && st == BSDE_OK; ++f) out[f] += o[f];
+    }
+    if (st) {
+      for (int q = 0; q < n; ++q) cs[q]->rs_ready = false;
+      return st;
+    }
   }
+  for (int r = 0; r < n; ++r) cs[r]->rs_ready = false;
   if (res) {
     fill_result(cs[0], res, out, 0.0, 0.0, steps);
     for (int r = 1; r < n; ++r) {                    // stage times: the slowest rank
@@ -1689,6 +2021,8 @@ bsde_status bsde_eval(bsde_ctx* c, const double* x, double* out) {
 
 static bsde_status bsde_eval_internal(bsde_ctx* c, const double* x, double* out) {
   cudaSetDevice(c->cfg.device);
+  if (c->spike && c->grouped)
+    return set_err(c, BSDE_ERR_STATE, "bsde_eval on a SPIKE slab-group member (the spline spans the group)");
   double xx[3] = {0, 0, 0};
   for (int a = 0; a < c->d; ++a) xx[a] = x[a];
   bsde_status st = spline_into(c, c->RS);                        // newest level -> scratch slot

@@ -150,29 +150,21 @@ struct PassArgs {
   int32_t TS;          // outputs per tile
   double alpha[kPcrLevels];
   double inv_b;
+  // Dirichlet fold nodes of the moment system: the unknown rows are fa+1 .. fb-1 and the
+  // moments at fa, fb are known -- from the not-a-knot end rows at a global line end (nak = 1:
+  // fa = 1 / fb = P - 2, outputs extend to the ghosts), or 0 at a slab interface (nak = 0,
+  // SPIKE local solve).  Outputs k in [out_lo, out_hi].
+  int64_t fa, fb, out_lo, out_hi;
+  int32_t nak_a, nak_b;
+  // slab interface: the local moments of the first / last unknown row of every line
+  // (edge[side * e_side + b0 * e_b0 + b1]), null otherwise
+  double* edge;
+  int64_t e_side, e_b0;
 };
-
-// odd periodic extension of the reduced right-hand side about nodes 1 and P-2
-// (Dirichlet nodes after m_1 and m_{P-2} are known): exact by the method of images.
-__device__ inline double rhs_tilde(const double* F, int64_t sl, int64_t P, int64_t k, double m1, double mP2) {
-  if (k >= 2 && k <= P - 3) {                       // interior row: no fold (no 64-bit modulo)
-    double r = 6.0 * (F[(k - 1) * sl] - 2.0 * F[k * sl] + F[(k + 1) * sl]);
-    if (k == 2) r -= m1;
-    if (k == P - 3) r -= mP2;
-    return r;
-  }
-  const int64_t period = 2 * (P - 3);
-  int64_t u = (k - 1) % period;
-  if (u < 0) u += period;
-  if (u == 0 || u == P - 3) return 0.0;
-  int64_t i;
-  double sgn;
-  if (u < P - 3) { i = 1 + u; sgn = 1.0; }
-  else { i = 1 + period - u; sgn = -1.0; }
-  double r = 6.0 * (F[(i - 1) * sl] - 2.0 * F[i * sl] + F[(i + 1) * sl]);
-  if (i == 2) r -= m1;
-  if (i == P - 3) r -= mP2;
-  return sgn * r;
+// the default not-a-knot line of P values (outputs c_{-1} .. c_P)
+inline void pass_defaults(PassArgs& pa) {
+  pa.fa = 1; pa.fb = pa.P - 2; pa.out_lo = -1; pa.out_hi = pa.P;
+  pa.nak_a = 1; pa.nak_b = 1; pa.edge = nullptr;
 }
 
 // One spline pass: LANES lines per CTA (1: lines along the contiguous axis; > 1: adjacent
@@ -195,8 +187,8 @@ __global__ void spline_pass(PassArgs a) {
   const double* F = a.src + b0 * a.s_b0 + (valid ? b1 : 0) * a.s_b1;
   double* out = a.dst + b0 * a.d_b0 + (valid ? b1 : 0) * a.d_b1;
   const int64_t sl = a.s_line;
-  const int64_t k0 = -1 + (int64_t)blockIdx.x * a.TS;
-  const int64_t k1 = min(k0 + (int64_t)a.TS, P + 1);
+  const int64_t k0 = a.out_lo + (int64_t)blockIdx.x * a.TS;
+  const int64_t k1 = min(k0 + (int64_t)a.TS, a.out_hi + 1);
   const int64_t base = k0 - 3 - H;
   const int W = a.TS + 6 + 2 * H;
   const int WZ = W + 2 * kSplZP;
@@ -217,29 +209,32 @@ __global__ void spline_pass(PassArgs a) {
   }
   __syncthreads();
   auto Fv = [&](int64_t k) { return Fs[(k - lo_v) * LANES + lane]; };
-  const double m1 = lo_v == 0 ? Fv(0) - 2.0 * Fv(1) + Fv(2) : 0.0;   // not-a-knot end rows, where used
-  const double mP2 = hi_v == P - 1 ? Fv(P - 3) - 2.0 * Fv(P - 2) + Fv(P - 1) : 0.0;
+  // known moments at the fold nodes: the not-a-knot end rows (where this tile reaches them), or
+  // 0 at a slab interface
+  const int64_t fa = a.fa, fb = a.fb;
+  const double ma = a.nak_a && lo_v == 0 ? Fv(0) - 2.0 * Fv(1) + Fv(2) : 0.0;
+  const double mb = a.nak_b && hi_v == P - 1 ? Fv(P - 3) - 2.0 * Fv(P - 2) + Fv(P - 1) : 0.0;
   for (int p = worker; p < W; p += nworkers) {
     const int64_t k = base + p;
     double r;
-    if (k >= 2 && k <= P - 3) {
+    if (k > fa && k < fb) {
       r = 6.0 * (Fv(k - 1) - 2.0 * Fv(k) + Fv(k + 1));
-      if (k == 2) r -= m1;
-      if (k == P - 3) r -= mP2;
+      if (k == fa + 1) r -= ma;
+      if (k == fb - 1) r -= mb;
     } else {                                                // odd periodic extension (images)
-      const int64_t period = 2 * (P - 3);
-      int64_t u = (k - 1) % period;
+      const int64_t period = 2 * (fb - fa);
+      int64_t u = (k - fa) % period;
       if (u < 0) u += period;
-      if (u == 0 || u == P - 3) {
+      if (u == 0 || u == fb - fa) {
         r = 0.0;
       } else {
         int64_t i;
         double sgn;
-        if (u < P - 3) { i = 1 + u; sgn = 1.0; }
-        else { i = 1 + period - u; sgn = -1.0; }
+        if (u < fb - fa) { i = fa + u; sgn = 1.0; }
+        else { i = fa + period - u; sgn = -1.0; }
         r = 6.0 * (Fv(i - 1) - 2.0 * Fv(i) + Fv(i + 1));
-        if (i == 2) r -= m1;
-        if (i == P - 3) r -= mP2;
+        if (i == fa + 1) r -= ma;
+        if (i == fb - 1) r -= mb;
         r *= sgn;
       }
     }
@@ -273,25 +268,32 @@ __global__ void spline_pass(PassArgs a) {
   if (!valid) return;
   const double ib = a.inv_b;
   auto mt = [&](int64_t k) { return A[(k - base) * LANES + lane] * ib; };
+  // moments of the not-a-knot end rows: m_fa, m_fb known, m_0 = 2 m_1 - m_2, m_{P-1} likewise
   auto mk = [&](int64_t k) -> double {
-    if (k == 1) return m1;
-    if (k == P - 2) return mP2;
-    if (k == 0) return 2.0 * m1 - (P - 2 == 2 ? mP2 : mt(2));
-    if (k == P - 1) return 2.0 * mP2 - (P - 3 == 1 ? m1 : mt(P - 3));
+    if (k == fa) return ma;
+    if (k == fb) return mb;
+    if (k == fa - 1) return 2.0 * ma - (fa + 1 == fb ? mb : mt(fa + 1));
+    if (k == fb + 1) return 2.0 * mb - (fb - 1 == fa ? ma : mt(fb - 1));
     return mt(k);
   };
   for (int64_t k = k0 + worker; k < k1; k += nworkers) {
     double c;
-    if (k >= 2 && k <= P - 3) c = Fv(k) - mt(k) * (1.0 / 6.0);
+    if (k > fa && k < fb) c = Fv(k) - mt(k) * (1.0 / 6.0);
     else if (k >= 0 && k < P) c = Fv(k) - mk(k) * (1.0 / 6.0);
     else if (k < 0) {
-      const double c0 = Fv(0) - mk(0) * (1.0 / 6.0), c1 = Fv(1) - m1 * (1.0 / 6.0);
+      const double c0 = Fv(0) - mk(0) * (1.0 / 6.0), c1 = Fv(1) - ma * (1.0 / 6.0);
       c = 6.0 * Fv(0) - 4.0 * c0 - c1;
     } else {
-      const double cl = Fv(P - 1) - mk(P - 1) * (1.0 / 6.0), cm = Fv(P - 2) - mP2 * (1.0 / 6.0);
+      const double cl = Fv(P - 1) - mk(P - 1) * (1.0 / 6.0), cm = Fv(P - 2) - mb * (1.0 / 6.0);
       c = 6.0 * Fv(P - 1) - 4.0 * cl - cm;
     }
     out[(k + 1) * a.d_line] = c;
+  }
+  // SPIKE: the local moments next to the slab interfaces (the reduced system's right-hand side)
+  if (a.edge != nullptr && worker == 0) {
+    double* e = a.edge + b0 * a.e_b0 + b1;
+    if (!a.nak_a && fa + 1 >= k0 && fa + 1 < k1) e[0] = mt(fa + 1);
+    if (!a.nak_b && fb - 1 >= k0 && fb - 1 < k1) e[a.e_side] = mt(fb - 1);
   }
 }
 
@@ -319,7 +321,7 @@ void set_wide_strided(bool on) { g_wide_strided = on; }
 
 static cudaError_t run_pass(PassArgs pa, bool strided, cudaStream_t st, int64_t* launches) {
   pcr_constants(pa.alpha, &pa.inv_b);
-  const int64_t n = pa.P + 2;                              // outputs per line (c_{-1} .. c_P)
+  const int64_t n = pa.out_hi - pa.out_lo + 1;             // outputs per line (default c_{-1} .. c_P)
   // short contiguous lines (d = 3: 514 outputs) also go 4 lines per CTA, one tile per line:
   // one 256-thread CTA per short line spends its time in barriers and launch overhead
   const bool short_lines = !strided && n <= 1024 && pa.nb1 >= 4;
@@ -377,6 +379,7 @@ cudaError_t launch_spline(const Grid& g, const double* values, int F, double* sl
       double* dst = (ax == d - 1) ? cdst : (ax % 2 == 0 ? tmp0 : tmp1);
       PassArgs pa{};
       pa.P = g.P[ax];
+      pass_defaults(pa);
       // batch axes: all axes except ax, at most two; the last remaining one is "inner"
       int bax[2], nbx = 0;
       for (int b = 0; b < d; ++b) if (b != ax) bax[nbx++] = b;
@@ -413,6 +416,144 @@ cudaError_t launch_spline(const Grid& g, const double* values, int F, double* sl
     pad_fill_1d<<<F, 256, 0, st>>>(slot, g.cfield, g.P[0], g.cpad);
     if (launches) ++*launches;
     return cudaGetLastError();
+  }
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ SPIKE (slab partition)
+// North_star's "spline solves along the partitioned axis are ... all-gathered" (SURVEY §8(e)
+// option 1): rank p solves the axis-0 moment system on its own rows with zero
+// coupling to its neighbours (Dirichlet m = 0 at rows r0 - 1 and r1, method of images), emits
+// the local moments of its first / last row, the edges of every rank are all-gathered, and the
+// true moments are m = m_loc + m(r0 - 1) S^L + m(r1) S^R with the closed-form spike vectors of
+// the constant (1, 4, 1) matrix, S^L_k = (rho^{k+1} - rho^{2n+1-k}) / (1 - rho^{2n+2}),
+// rho = sqrt(3) - 2.  The interface moments solve a 2 (R - 1) system whose inverse is the same
+// for every line (host, long double); the correction is linear, so it is applied to the final
+// tensor coefficients: Delta c(k, .) = -(S^L_k XL + S^R_k XR) / 6 with XL, XR the tensor splines
+// of the interface moments along axes 1 .. d-1.
+__global__ void spike_reduce(SpikeArgs a) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = blockIdx.y;
+  if (e >= a.plane) return;
+  const int64_t rs = (int64_t)a.F * 2 * a.plane;        // rank stride of gath
+  const double* G = a.gath + (int64_t)f * 2 * a.plane + e;
+  double xl = 0.0, xr = 0.0;
+  for (int i = 0; i + 1 < a.R; ++i) {
+    const double b = G[(int64_t)i * rs + a.plane];      // last row of rank i
+    const double c = G[(int64_t)(i + 1) * rs];          // first row of rank i + 1
+    xl = fma(a.wL[2 * i], b, fma(a.wL[2 * i + 1], c, xl));
+    xr = fma(a.wR[2 * i], b, fma(a.wR[2 * i + 1], c, xr));
+  }
+  a.X[((int64_t)f * 2) * a.plane + e] = xl;
+  a.X[((int64_t)f * 2 + 1) * a.plane + e] = xr;
+}
+cudaError_t launch_spike_reduce(const SpikeArgs& a, cudaStream_t st) {
+  dim3 grid((unsigned)((a.plane + 255) / 256), (unsigned)a.F);
+  spike_reduce<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Delta c of the corrected rows: unknown rows [row_lo, row_lo + n) (local), and where a side is a
+// global not-a-knot end its two outer rows: m_0 = 2 m_1 - m_2 with m_1 fixed by the data, so
+// Delta c_0 = Delta m_2 / 6 and the ghost c_{-1} = 6 F_0 - 4 c_0 - c_1 moves by -4 Delta c_0
+// (mirrored at the right end)
+__global__ void spike_correct(double* slot, int64_t cfield, int64_t cs0, const double* XC, int64_t plane_c,
+                              const double* sLR, int64_t row_lo, int64_t n, int nak_a, int nak_b, int F) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= plane_c) return;
+  const int64_t t = blockIdx.y;              // 0 .. n-1 unknown rows, n .. n+3 the not-a-knot extras
+  int64_t row, srow;                         // corrected row; row whose Delta m it takes
+  double scale;                              // Delta c = scale * Delta m(srow)
+  if (t < n) { row = row_lo + t; srow = t; scale = -1.0 / 6.0; }
+  else {
+    const int x = (int)(t - n);
+    if (x < 2) {
+      if (!nak_a) return;
+      row = row_lo - 2 - x; srow = 0; scale = x == 0 ? 1.0 / 6.0 : -4.0 / 6.0;     // rows 0, -1
+    } else {
+      if (!nak_b) return;
+      row = row_lo + n + 1 + (x - 2); srow = n - 1; scale = x == 2 ? 1.0 / 6.0 : -4.0 / 6.0;   // P-1, P
+    }
+  }
+  const double sl = sLR[srow], sr = sLR[n + srow];
+  for (int f = 0; f < F; ++f) {
+    const double xl = XC[((int64_t)f * 2) * plane_c + e], xr = XC[((int64_t)f * 2 + 1) * plane_c + e];
+    double* c = slot + (int64_t)f * cfield + (row + 1) * cs0 + e;
+    *c = fma(scale, fma(sl, xl, sr * xr), *c);
+  }
+}
+cudaError_t launch_spike_correct(double* slot, int64_t cfield, int64_t cs0, const double* XC, int64_t plane_c,
+                                 const double* sLR, int64_t row_lo, int64_t n, int nak_a, int nak_b, int F,
+                                 cudaStream_t st) {
+  dim3 grid((unsigned)((plane_c + 255) / 256), (unsigned)(n + 4));
+  spike_correct<<<grid, 256, 0, st>>>(slot, cfield, cs0, XC, plane_c, sLR, row_lo, n, nak_a, nak_b, F);
+  return cudaGetLastError();
+}
+
+// The local part of a slab rank's tensor spline (SPIKE): the axis-0 pass over the owned rows
+// with Dirichlet folds at the interfaces (edges -> edge[F][2][plane]), then the passes along the
+// other axes over the owned rows (+ the ghost rows at a global end) only.
+cudaError_t launch_spline_slab(const Grid& g, const double* values, int F, double* slot, double* tmp0, double* tmp1,
+                               bool first, bool last, double* edge, cudaStream_t st, int64_t* launches) {
+  const int d = g.d;
+  const int64_t own0 = g.own0, nown = g.nown0, P0 = g.P[0];
+  const int64_t plane = g.npts / P0;
+  // axis-0 rows the later passes cover (local, -1 = ghost)
+  const int64_t rlo = first ? -1 : own0, rhi = last ? P0 : own0 + nown - 1;
+  for (int f = 0; f < F; ++f) {
+    const double* vsrc = values + (int64_t)f * g.npts;
+    double* cdst = slot + (int64_t)f * g.cfield;
+    const double* src = vsrc;
+    bool src_is_values = true;
+    for (int ax = 0; ax < d; ++ax) {
+      double* dst = (ax == d - 1) ? cdst : (ax % 2 == 0 ? tmp0 : tmp1);
+      PassArgs pa{};
+      pa.P = g.P[ax];
+      pass_defaults(pa);
+      int bax[2], nbx = 0;
+      for (int b = 0; b < d; ++b) if (b != ax) bax[nbx++] = b;
+      int64_t n[2] = {1, 1}, ss[2] = {0, 0}, ds[2] = {0, 0};
+      int64_t soff = 0, doff = 0;
+      for (int t = 0; t < nbx; ++t) {
+        const int b = bax[t];
+        const bool done = b < ax;
+        n[t] = done ? g.P[b] + 2 : g.P[b];
+        ss[t] = src_is_values ? g.vstride[b] : g.cstride[b];
+        ds[t] = g.cstride[b];
+        if (!done) {
+          if (!src_is_values) soff += g.cstride[b];
+          doff += g.cstride[b];
+        }
+        if (b == 0 && done) {                   // axis 0 transformed: only rows [rlo, rhi]
+          n[t] = rhi - rlo + 1;
+          soff += (rlo + 1) * ss[t];
+          doff += (rlo + 1) * ds[t];
+        }
+      }
+      if (!src_is_values) soff += g.cstride[ax];
+      pa.src = src + soff;
+      pa.dst = dst + doff;
+      pa.s_line = src_is_values ? g.vstride[ax] : g.cstride[ax];
+      pa.d_line = g.cstride[ax];
+      if (nbx == 0) { pa.nb0 = 1; pa.nb1 = 1; }
+      else if (nbx == 1) { pa.nb0 = 1; pa.nb1 = n[0]; pa.s_b1 = ss[0]; pa.d_b1 = ds[0]; }
+      else { pa.nb0 = n[0]; pa.s_b0 = ss[0]; pa.d_b0 = ds[0]; pa.nb1 = n[1]; pa.s_b1 = ss[1]; pa.d_b1 = ds[1]; }
+      if (ax == 0) {
+        pa.nak_a = first ? 1 : 0;
+        pa.nak_b = last ? 1 : 0;
+        pa.fa = first ? 1 : own0 - 1;
+        pa.fb = last ? P0 - 2 : own0 + nown;
+        pa.out_lo = first ? -1 : own0;
+        pa.out_hi = last ? P0 : own0 + nown - 1;
+        pa.edge = edge + (int64_t)f * 2 * plane;
+        pa.e_side = plane;
+        pa.e_b0 = nbx == 2 ? n[1] : 0;
+      }
+      cudaError_t e = run_pass(pa, ax != d - 1, st, launches);
+      if (e != cudaSuccess) return e;
+      src = dst;
+      src_is_values = false;
+    }
   }
   return cudaSuccess;
 }

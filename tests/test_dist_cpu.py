@@ -74,13 +74,28 @@ def test_partition_and_id_broadcast_gloo(world):
             assert b2["own_lo"] - b2["slab_lo"] == min(b2["own_lo"], b2["halo"])
             assert a["slab_hi"] - a["own_hi"] == min(P0 - a["own_hi"], a["halo"])
         for p in parts:
-            assert p["halo"] >= 31 + 4                              # PCR decay + cubic support
+            assert p["halo"] >= 4                                   # cubic support (SPIKE: coefficient halo)
+
+
+def test_spike_halo_is_reach_plus_stencil():
+    """SPIKE (default) exchanges reach + 3 rows of final coefficients; the redundant-halo
+    ablation adds the PCR decay rows (31) and the not-a-knot / ghost rows (6) of values."""
+    from paper_1909_13560_b200 import query_partition, workloads as W
+    for spec, Rs in ((W.cfg4(), (2, 4, 8)), (W.basket_3d(), (2, 4, 8)), (W.ex4_2d(3, 8, npts=257), (2,))):
+        for R in Rs:
+            a = query_partition(spec, R, 1)
+            b = query_partition(dict(spec, slab_spline=1), R, 1)
+            assert b["halo"] - a["halo"] == 37
+            assert a["own_lo"] == b["own_lo"] and a["own_hi"] == b["own_hi"]
 
 
 def test_partition_rejects_thin_slabs():
     from paper_1909_13560_b200 import query_partition, BsdeError, workloads as W
     with pytest.raises(BsdeError) as ei:
-        query_partition(W.basket_3d(P=128), 8, 0)                  # 16 planes < halo
+        query_partition(dict(W.basket_3d(P=128), slab_spline=1), 8, 0)   # 16 planes < values halo
+    assert ei.value.code == 1
+    with pytest.raises(BsdeError) as ei:
+        query_partition(W.basket_3d(P=32), 8, 0)                   # 4 planes < coefficient halo
     assert ei.value.code == 1
     with pytest.raises(BsdeError):
         query_partition(W.cfg2(6), 2, 0)                           # 1-D runs as replicas

@@ -574,16 +574,24 @@ def test_accuracy_against_closed_forms():
 
 # ------------------------------------------------------------------ slab partition (d >= 2)
 @gpu
+@pytest.mark.parametrize("slab", [0, 1], ids=["spike", "redundant_halo"])
 @pytest.mark.parametrize("R,spec", [(2, W.ex4_2d(3, 8, npts=257)), (3, W.ex4_2d(3, 8, npts=257)),
-                                    (4, W.ex4_2d(3, 16, npts=513)), (2, W.exchange_2d(2, 6, npts=201))],
+                                    (4, W.ex4_2d(3, 16, npts=513)), (2, W.exchange_2d(2, 6, npts=201)),
+                                    (5, W.ex4_2d(2, 6, npts=301))],
                          ids=lambda v: str(v) if isinstance(v, int) else v["name"])
-def test_slab_group_matches_single_context(R, spec):
-    """In-process slab group (R contexts on one GPU, halo rows copied per step) vs one context:
-    the redundant halo spline differs only by the PCR truncation (coupling 5e-19)."""
+def test_slab_group_matches_single_context(R, spec, slab):
+    """In-process slab group (R contexts on one GPU) vs one context.  SPIKE (slab = 0, the
+    default): the axis-0 spline of each slab solved with zero coupling, the edge
+    moments gathered, the interface system solved and the spike correction applied, coefficient
+    halos of reach + 3 rows -- exact up to rounding.  Redundant halo (slab = 1, ablation): the
+    axis-0 spline re-solved over a values halo, differing by the PCR truncation (5e-19)."""
     from paper_1909_13560_b200 import Solver, GroupSolver
+    if slab == 1 and R == 5:
+        pytest.skip("60-row slabs are thinner than the redundant values halo (SPIKE only)")
     with Solver(spec) as one:
         r1 = one.solve()
         ref = one.layers()
+    spec = dict(spec, slab_spline=slab)
     with GroupSolver(spec, R) as grp:
         assert [s.own for s in grp.ranks][0][0] == 0
         rg = grp.solve()
@@ -599,16 +607,18 @@ def test_slab_group_matches_single_context(R, spec):
                                     (3, dict(W.basket_3d(3, 6, 4, P=160), npts=[160, 13, 11])),
                                     (2, dict(W.ex1_3d(2, 6, 4, P=120), npts=[120, 11, 9]))],
                          ids=lambda v: str(v) if isinstance(v, int) else v["name"] + "_" + "x".join(map(str, v["npts"])))
-def test_slab_group_3d_matches_single_context_and_oracle(R, spec):
-    """d = 3 slab partition (R contexts on one GPU, axis-0 halo planes copied per step, the
-    decomposed differential-rates path and the per-tap path's plane stacks built on owned planes
-    only) vs one context (1e-13: the redundant halo spline differs by the PCR truncation 5e-19)
-    and vs the oracle (1e-11)."""
+@pytest.mark.parametrize("slab", [0, 1], ids=["spike", "redundant_halo"])
+def test_slab_group_3d_matches_single_context_and_oracle(R, spec, slab):
+    """d = 3 slab partition (R contexts on one GPU, the decomposed differential-rates path and the
+    per-tap path's plane stacks built on owned planes only) vs one context (1e-13; SPIKE exact up
+    to rounding, the redundant-halo ablation differs by the PCR truncation 5e-19) and vs the
+    oracle (1e-11)."""
     import oracle
     from paper_1909_13560_b200 import Solver, GroupSolver
     with Solver(spec) as one:
         r1 = one.solve()
         ref = one.layers()
+    spec = dict(spec, slab_spline=slab)
     with GroupSolver(spec, R) as grp:
         rg = grp.solve()
         got = grp.layers()
