@@ -12,7 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbsde_b200.so")
 SOURCES = ["kernels.cu", "host.cu"]
-HEADERS = ["bsde_internal.h", "problems.cuh", "fused1d.cuh", "fused2d.cuh", "fused3d.cuh", "aff2.cuh"]
+HEADERS = ["bsde_internal.h", "problems.cuh", "fused1d.cuh", "fused1d_small.cuh", "fused2d.cuh", "fused3d.cuh",
+           "aff2.cuh", "bicubic.cuh", "fsde.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]

@@ -113,6 +113,7 @@ struct bsde_ctx {
   int qspan = 0, qspan1 = 0, boot_qspan = 0, boot_qspan1 = 0;
   struct Geo {
     bool ok = false;
+    bool single = false;          // the one-tile-per-CTA launch is co-resident
     Fused1D fz{};
     int threads = 0, blocks = 0;
     int D[kMaxK + 1] = {};        // D[j]: CTA distance of level j's window; D[0]: values halo
@@ -415,7 +416,10 @@ void set_distances(bsde_ctx* c, const std::vector<AxisTap>& t, int K, bsde_ctx::
   }
   geo.DK = dk;
   const int per_sm = fused1d_blocks_per_sm(geo.fz.variant, geo.smem);
-  if (geo.blocks > c->nsm * per_sm || geo.blocks > 8192) geo.ok = false;
+  if (geo.blocks > 8192) geo.ok = false;
+  // one tile per CTA (bsde_step, bsde_solve) needs every CTA co-resident; a batch partitions the
+  // tiles over fewer CTAs (bsde_solve_batch checks its own co-residency)
+  geo.single = geo.blocks <= c->nsm * per_sm;
 }
 
 // balanced rows of rank r out of R
@@ -702,7 +706,7 @@ bsde_status run_step(bsde_ctx* c, int Kl, int Kyl, int Kzl, const double* gyl, c
   s.n = (int)std::floor((tn - c->cfg.t0) / c->dt + 0.5);      // level index (bootstrap: nearest level)
   const bool timing = c->cfg.timing != 0 && !c->in_setup;
   cudaError_t e;
-  if (c->d == 1 && (variant == 0 || variant >= 10) && geo.ok && tap1_off >= 0 && c->pb.sde_id == 0) {
+  if (c->d == 1 && (variant == 0 || variant >= 10) && geo.ok && geo.single && tap1_off >= 0 && c->pb.sde_id == 0) {
     cudaEvent_t t0 = timing ? tmark(c) : nullptr;            // spline fused into the kernel
     e = launch_fused1d_steps(s, c->g, c->pb, geo.fz, 0, 1, 0, c->cur, 0.0, 0.0, c->vbuf[0], c->vbuf[1], c->barrier,
                              geo.D, geo.DK, geo.threads, geo.blocks, geo.smem, c->stream);
@@ -1398,7 +1402,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
         const double tn = cfg->t0 + m * c->dt + s * db;
         const int slots[1] = {c->RS};                        // scratch slot
         // the fused 1-D kernel reads the spline of its input level from the ring: build it
-        if (c->d == 1 && c->boot_geo.ok && (st = spline_into(c, c->RS))) return fail(st);
+        if (c->d == 1 && c->boot_geo.ok && c->boot_geo.single && (st = spline_into(c, c->RS))) return fail(st);
         if ((st = run_step(c, 1, 1, 1, g1, g1, db, tn, slots, -1, c->boot_tap_off, c->boot_tap1_off, c->boot_geo,
                            cfg->kernel_variant, c->boot_wc2)))
           return fail(st);
@@ -1530,7 +1534,7 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
   bsde_status st = BSDE_OK;
   // d = 1 fused path: all remaining steps in one cooperative (persistent) launch
   const bool fused = c->d == 1 && (c->cfg.kernel_variant == 0 || c->cfg.kernel_variant >= 10) && c->geo.ok &&
-                     c->tap1_off >= 0;
+                     c->geo.single && c->tap1_off >= 0;
   int64_t pexec = -1;
   if (c->small_ok && c->level >= 1) {                  // latency path: one single-CTA launch
     const StepArgs s = persistent_args(c);
@@ -1659,8 +1663,8 @@ bsde_status bsde_solve_batch(bsde_ctx* const* cs, int32_t n, bsde_result* res) {
 }
 
 bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, bsde_result* res) {
-  if (mode < 0 || (mode > 3 && (mode < 11 || mode > 19)))
-    return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: mode %d outside 0..3, 11..19", mode);
+  if (mode < 0 || (mode > 5 && (mode < 11 || mode > 19)))
+    return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: mode %d outside 0..5, 11..19", mode);
   if (!cs || n < 1 || n > kMaxBatch) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: need 1..%d contexts", kMaxBatch);
   for (int i = 0; i < n; ++i)
     if (!cs[i]) return set_err(nullptr, BSDE_ERR_INVALID_ARGUMENT, "batch: ctx %d is NULL", i);
@@ -1700,7 +1704,15 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
   if (mode != 1 && (n >= 2 || mode >= 2)) {
     const int TP = fz.TP, P = (int)c0->g.P[0];
     const int mb = fused1d_blocks_per_sm(fz.variant, fused1d_smem(fzp));
-    const int nsmax = std::max(1, std::min(9, (P - 2 * kPcrHalo - 256) / (2 * TP)));
+    // tiles per CTA: bounded by the pass-2 window (its folded end rows) and by shared memory
+    int nsmax = std::max(1, std::min(9, (P - 2 * kPcrHalo - 256) / (2 * TP)));
+    while (nsmax > 1) {
+      Fused1D t = fz;
+      t.WP = ((nsmax * TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;
+      t.WS = 6 * t.WP + 16;
+      if (fused1d_smem(t) > 0) break;
+      --nsmax;
+    }
     int Kv[kMaxBatch], st[kMaxBatch];
     for (int i = 0; i < n; ++i) { Kv[i] = cs[i]->K; st[i] = cs[i]->level; }
     if (mode == 2) {                                 // pairs by K rank: (1st, last), (2nd, 2nd last), ...
@@ -1712,6 +1724,13 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
         group[idx[r]] = pr;
         ngroup = std::max(ngroup, pr + 1);
       }
+    } else if ((mode == 4 || mode == 5) && n > mode - 2) {   // the m = mode - 2 smallest K share a group
+      const int m = mode - 2;
+      int idx[kMaxBatch];
+      for (int i = 0; i < n; ++i) idx[i] = i;
+      std::stable_sort(idx, idx + n, [&](int x, int y) { return Kv[x] < Kv[y]; });
+      for (int r = 0; r < n; ++r) group[idx[r]] = r < m ? 0 : r - m + 1;
+      ngroup = n - m + 1;
     } else {
       for (int i = 0; i < n; ++i) group[i] = i;
       ngroup = n;

@@ -68,10 +68,10 @@ template <int D> struct Driver<DRV_EX2, D> {
 
 // f = -(r y + sum th_k z_k) + (R - r) max(sum pi_k z_k - y, 0)  (R21)
 template <int D> struct Driver<DRV_DIFF, D> {
-  double r, Rmr, th[D], pi[D];
+  double r, hRmr, th[D], pi[D];
   __device__ explicit Driver(const double* p) {
     r = p[0];
-    Rmr = p[1] - p[0];
+    hRmr = 0.5 * (p[1] - p[0]);                    // (R - r) / 2: exact scaling
 #pragma unroll
     for (int k = 0; k < D; ++k) { th[k] = p[2 + k]; pi[k] = p[5 + k]; }
   }
@@ -80,8 +80,10 @@ template <int D> struct Driver<DRV_DIFF, D> {
     double lin = r * y, hold = -y;
 #pragma unroll
     for (int k = 0; k < D; ++k) { lin = fma(th[k], z[k], lin); hold = fma(pi[k], z[k], hold); }
-    // max(hold, 0) = (hold + |hold|) / 2 exactly (one DADD with an |.| operand modifier)
-    return fma(Rmr, 0.5 * (hold + fabs(hold)), -lin);
+    // (R - r) max(hold, 0) = ((R - r) / 2) (hold + |hold|): hold + |hold| = 2 max(hold, 0) and the
+    // halving are exact, so the product is the same rounding of (R - r) max(hold, 0) as before
+    // (one DADD with an |.| operand modifier, no DMUL)
+    return fma(hRmr, hold + fabs(hold), -lin);
   }
 };
 
