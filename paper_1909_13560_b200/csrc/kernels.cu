@@ -10,6 +10,7 @@
 //   quad1d_fused      d = 1: level-1 spline (PCR) + quadrature on shared-memory windows
 //                     streamed by cp.async.bulk + z + Picard, one kernel per step (cfg 2)
 //   eval_kernel       spline of the newest level at one point (the evaluation point)
+#include <climits>
 #include <cstdlib>
 #include <algorithm>
 #include <cstdio>
@@ -297,6 +298,197 @@ __global__ void spline_pass(PassArgs a) {
   }
 }
 
+// Recursive-filter spline pass (r2): the same moment system as spline_pass, solved
+// with the factorisation (1, 4, 1) = (-1/rho)(1 - rho z^-1)(1 - rho z), rho = sqrt(3) - 2:
+//   u_k = r_k + rho u_{k-1} (causal),  v_k = u_k + rho v_{k+1} (anti-causal),  m = -rho v.
+// A CTA owns 32 adjacent lines (lane = line) and a tile of NR = 16 S rows (warp = segment of S
+// rows); each segment filters its rows in registers from a zero start, the segment carries are
+// chained through shared memory (C_w = e_{w-1} + rho^S C_{w-1}), and the local results are
+// corrected by rho^(j+1) C_w (exact: the filters are linear).  The tile starts and ends kRfH = 32
+// rows beyond its outputs (the zero start there is the truncation |rho|^32 = 5e-19, the PCR
+// pass's coupling bound).  Per element: 3 FMA-class ops for the right-hand side, 2 for the
+// filters, 2 for the fix-ups, 1 for c = F - m/6 -- against ~25 for five PCR levels.  STRIDED:
+// the lines are adjacent in memory (32 lines = one 256-byte row); else each line is contiguous and
+// the tile is transposed through shared memory on the way in and out.
+constexpr int kRfH = 32;
+constexpr int kRfSeg = 16;             // segments (warps) per CTA
+constexpr int kRfT = 32 * kRfSeg;      // threads per CTA
+template <int S, bool STRIDED>
+__global__ void __launch_bounds__(kRfT, 2) spline_rf(PassArgs a) {
+  constexpr int NR = kRfSeg * S;       // tile rows
+  constexpr int LD = 33;               // shared-memory pitch (lines + 1: conflict-free transposes)
+  extern __shared__ double sm[];
+  double* const Fs = sm;                                   // [NR + 2][LD]: rows kb - 1 .. kb + NR
+  double* const E = Fs + (size_t)(NR + 2) * LD;            // [kRfSeg][32] segment carries
+  double* const Me = E + kRfSeg * 32;                      // [2][32] m at rows fa + 1, fb - 1
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int P = (int)a.P;
+  const int k0 = (int)a.out_lo + (int)blockIdx.x * a.TS;
+  const int k1 = min(k0 + a.TS, (int)a.out_hi + 1);
+  const int kb = k0 - kRfH;                                // first tile row
+  const int64_t lb = (int64_t)blockIdx.y * 32;             // first line (b1)
+  const int nl = (int)min((int64_t)32, a.nb1 - lb);        // lines of this CTA
+  const int lo_v = max(kb - 1, 0), hi_v = min(kb + NR, P - 1);   // staged rows
+  const int nv = hi_v - lo_v + 1;
+  const double* src = a.src + (int64_t)blockIdx.z * a.s_b0;
+  double* dst = a.dst + (int64_t)blockIdx.z * a.d_b0;
+  // ---- stage F[lo_v .. hi_v] of the 32 lines (row k of the line at Fs[(k - kb + 1) * LD + line])
+  {
+    double* const F0 = Fs + (lo_v - kb + 1) * LD;
+    if (STRIDED) {
+      const double* sp = src + (int64_t)lo_v * a.s_line + lb;
+      for (int i = threadIdx.x; i < nv * 32; i += kRfT) {
+        const int r = i >> 5, l = i & 31;
+        F0[r * LD + l] = l < nl ? __ldg(sp + (int64_t)r * a.s_line + l) : 0.0;
+      }
+    } else {
+      const double* sp = src + lb * a.s_b1 + (int64_t)lo_v * a.s_line;
+      for (int l = w; l < 32; l += kRfSeg) {               // warp per line, lanes along it
+        const double* q = sp + (int64_t)l * a.s_b1;
+        for (int r = lane; r < nv; r += 32) F0[r * LD + l] = l < nl ? __ldg(q + (int64_t)r * a.s_line) : 0.0;
+      }
+    }
+  }
+  __syncthreads();
+  const double* const Fl = Fs + (1 - kb) * LD + lane;      // Fl[k * LD] = F_k of this lane's line
+  auto Fv = [&](int k) { return Fl[k * LD]; };
+  const int fa = (int)a.fa, fb = (int)a.fb;
+  const double ma = a.nak_a && lo_v == 0 ? Fv(0) - 2.0 * Fv(1) + Fv(2) : 0.0;
+  const double mb = a.nak_b && hi_v == P - 1 ? Fv(P - 3) - 2.0 * Fv(P - 2) + Fv(P - 1) : 0.0;
+  auto rhs = [&](int k) -> double {                        // odd periodic extension (images)
+    const int period = 2 * (fb - fa);
+    int u = (k - fa) % period;
+    if (u < 0) u += period;
+    if (u == 0 || u == fb - fa) return 0.0;
+    const int i = u < fb - fa ? fa + u : fa + period - u;
+    double r = 6.0 * (Fv(i - 1) - 2.0 * Fv(i) + Fv(i + 1));
+    if (i == fa + 1) r -= ma;
+    if (i == fb - 1) r -= mb;
+    return u < fb - fa ? r : -r;
+  };
+  const double rho = -0.26794919243112270;                // sqrt(3) - 2
+  const int s0 = kb + w * S;                               // this segment's first row
+  const bool interior = s0 - 1 > fa && s0 + S < fb;        // every row direct (no fold, no end row)
+  // ---- causal filter of the segment from a zero start
+  double x[S];
+  {
+    double u = 0.0;
+    if (interior) {
+      double fm = Fv(s0 - 1), f0 = Fv(s0);
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        const double fp = Fv(s0 + j + 1);
+        u = fma(rho, u, 6.0 * (fm - 2.0 * f0 + fp));
+        x[j] = u;
+        fm = f0;
+        f0 = fp;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        u = fma(rho, u, rhs(s0 + j));
+        x[j] = u;
+      }
+    }
+    E[w * 32 + lane] = u;
+  }
+  __syncthreads();
+  double rs = rho;                                         // rho^S
+#pragma unroll
+  for (int j = 1; j < S; ++j) rs *= rho;
+  {
+    double C = 0.0;                                        // true u of row s0 - 1
+    for (int q = 0; q < w; ++q) C = fma(rs, C, E[q * 32 + lane]);
+    double pw = rho, v = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) { x[j] = fma(pw, C, x[j]); pw *= rho; }
+    // ---- anti-causal filter from a zero end
+#pragma unroll
+    for (int j = S - 1; j >= 0; --j) { v = fma(rho, v, x[j]); x[j] = v; }
+  }
+  __syncthreads();                                         // E is reused for the backward carries
+  E[w * 32 + lane] = x[0];
+  __syncthreads();
+  {
+    double D = 0.0;                                        // true v of row s0 + S
+    for (int q = kRfSeg - 1; q > w; --q) D = fma(rs, D, E[q * 32 + lane]);
+    double pw = rho;
+#pragma unroll
+    for (int j = S - 1; j >= 0; --j) { x[j] = -rho * fma(pw, D, x[j]); pw *= rho; }   // m
+  }
+  if (!interior) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      if (s0 + j == fa + 1) Me[lane] = x[j];
+      if (s0 + j == fb - 1) Me[32 + lane] = x[j];
+    }
+  }
+  __syncthreads();                                         // Me complete; Fs still holds F
+  const double ib6 = 1.0 / 6.0;
+  const double mfa1 = Me[lane], mfb1 = Me[32 + lane];
+  // the not-a-knot end rows k <= fa, k >= fb and the ghosts (m_fa, m_fb known, m_0 = 2 m_1 - m_2,
+  // c_{-1} = 6 F_0 - 4 c_0 - c_1): computed now, written with the rest
+  double ev[3] = {0.0, 0.0, 0.0};
+  int ek[3] = {INT_MIN, INT_MIN, INT_MIN};
+  if (!interior) {
+    int ne = 0;
+    for (int t = 0; t < 6; ++t) {
+      const bool left = t < 3;
+      if (left ? !a.nak_a : !a.nak_b) continue;
+      const int k = left ? fa - 2 + t : fb + (t - 3);      // -1, 0, 1 | P-2, P-1, P
+      if (k < s0 || k >= s0 + S || k < k0 || k >= k1 || ne >= 3) continue;
+      const double m0 = 2.0 * ma - (fa + 1 == fb ? mb : mfa1), mP1 = 2.0 * mb - (fb - 1 == fa ? ma : mfb1);
+      double c;
+      if (k == fa) c = Fv(fa) - ma * ib6;
+      else if (k == fb) c = Fv(fb) - mb * ib6;
+      else if (k == 0) c = Fv(0) - m0 * ib6;
+      else if (k == P - 1) c = Fv(P - 1) - mP1 * ib6;
+      else if (k < 0) c = 6.0 * Fv(0) - 4.0 * (Fv(0) - m0 * ib6) - (Fv(1) - ma * ib6);
+      else c = 6.0 * Fv(P - 1) - 4.0 * (Fv(P - 1) - mP1 * ib6) - (Fv(P - 2) - mb * ib6);
+      ev[ne] = c;
+      ek[ne] = k;
+      ++ne;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < S; ++j) x[j] = Fv(s0 + j) - x[j] * ib6;   // c = F - m/6 (rows fa < k < fb)
+  const bool valid = lane < nl;
+  const int klo = max(k0, max(s0, fa + 1)), khi = min(k1, min(s0 + S, fb));   // direct output rows
+  if (STRIDED) {
+    if (valid) {
+      double* dl = dst + lb + lane;
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+        if (s0 + j >= klo && s0 + j < khi) dl[(int64_t)(s0 + j + 1) * a.d_line] = x[j];
+      for (int t = 0; t < 3; ++t)
+        if (ek[t] != INT_MIN) dl[(int64_t)(ek[t] + 1) * a.d_line] = ev[t];
+    }
+  } else {
+    __syncthreads();                                       // every F read is done: Fs -> output tile
+    double* const Ol = Fs + (1 - kb) * LD + lane;
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (s0 + j >= klo && s0 + j < khi) Ol[(s0 + j) * LD] = x[j];
+    for (int t = 0; t < 3; ++t)
+      if (ek[t] != INT_MIN) Ol[ek[t] * LD] = ev[t];
+    __syncthreads();
+    const int no = k1 - k0;
+    double* const dp = dst + lb * a.d_b1 + (int64_t)(k0 + 1) * a.d_line;
+    const double* const Op = Fs + (k0 - kb + 1) * LD;
+    for (int l = w; l < nl; l += kRfSeg) {
+      double* q = dp + (int64_t)l * a.d_b1;
+      for (int r = lane; r < no; r += 32) q[(int64_t)r * a.d_line] = Op[r * LD + l];
+    }
+  }
+  if (a.edge != nullptr && valid && w == 0) {
+    double* e = a.edge + (int64_t)blockIdx.z * a.e_b0 + lb + lane;
+    if (!a.nak_a && fa + 1 >= k0 && fa + 1 < k1) e[0] = mfa1;
+    if (!a.nak_b && fb - 1 >= k0 && fb - 1 < k1) e[a.e_side] = mfb1;
+  }
+}
+constexpr int kRfS = 20;                 // rows per segment: tiles of 320 rows, 256 outputs
+static size_t spline_rf_smem() { return ((size_t)(kRfSeg * kRfS + 2) * 33 + kRfSeg * 32 + 64) * sizeof(double); }
+
 // shared memory of one spline_pass CTA
 static size_t spline_smem(int TS, int lanes) {
   const int W = TS + 6 + 2 * kPcrHalo;
@@ -322,6 +514,17 @@ void set_wide_strided(bool on) { g_wide_strided = on; }
 static cudaError_t run_pass(PassArgs pa, bool strided, cudaStream_t st, int64_t* launches) {
   pcr_constants(pa.alpha, &pa.inv_b);
   const int64_t n = pa.out_hi - pa.out_lo + 1;             // outputs per line (default c_{-1} .. c_P)
+  // many lines: the recursive-filter pass (32 lines per CTA; strided lines must be adjacent)
+  if (pa.nb1 >= 32 && (!strided || (pa.s_b1 == 1 && pa.d_b1 == 1))) {
+    constexpr int TSr = kRfSeg * kRfS - 2 * kRfH;
+    const int64_t nt = (n + TSr - 1) / TSr;
+    pa.TS = (int)((n + nt - 1) / nt);
+    dim3 grid((unsigned)nt, (unsigned)((pa.nb1 + 31) / 32), (unsigned)pa.nb0);
+    if (strided) spline_rf<kRfS, true><<<grid, kRfT, spline_rf_smem(), st>>>(pa);
+    else spline_rf<kRfS, false><<<grid, kRfT, spline_rf_smem(), st>>>(pa);
+    ++*launches;
+    return cudaGetLastError();
+  }
   // short contiguous lines (d = 3: 514 outputs) also go 4 lines per CTA, one tile per line:
   // one 256-thread CTA per short line spends its time in barriers and launch overhead
   const bool short_lines = !strided && n <= 1024 && pa.nb1 >= 4;
@@ -745,6 +948,8 @@ cudaError_t init_device_attributes() {
   cudaError_t e = cudaFuncSetAttribute(spline_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_pass<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_rf<kRfS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_rf<kRfS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = set_attr_drv<DRV_ZERO>();
   if (e == cudaSuccess) e = set_attr_drv<DRV_AFFINE>();
   if (e == cudaSuccess) e = set_attr_drv<DRV_EX1>();
