@@ -552,11 +552,14 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       }
       __syncthreads();
       PHASE_STAMP(8);
-      // the sums of this thread's points (TP <= 2 NT for every variant) into registers, so
+      // the sums of this thread's points (TP = 32 NWPG R <= U NT, U = ceil(R / C)) into registers, so
       // the level buffers are free during the epilogue
-      double az[2] = {0.0, 0.0}, af[2] = {0.0, 0.0}, ay[2] = {0.0, 0.0};
+      constexpr int U = (R + C - 1) / C;
+      double az[U], af[U], ay[U];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) { az[u] = 0.0; af[u] = 0.0; ay[u] = 0.0; }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
         const int t = tid + u * NT;
         if (t < hi - lo) {
 #pragma unroll
@@ -603,7 +606,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       PHASE_STAMP(17);
       const double inv_gz0 = 1.0 / s.gz0;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int t = tid + u * NT;
         if (t >= hi - lo) continue;
         // z: Eq. 20 line 2 (explicit); y: Eq. 20 line 1 by Picard from E[y^{n+Ky}]
@@ -835,8 +838,12 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
 }
 
 // instantiated (R, C, NT, MB = CTAs per SM) variants of the fused kernel; index 0 is the default
+// (r2) index 0 = 12 warps in 3 point groups x 4 node chunks, one CTA per SM (cfg 2 batch 16.6 ->
+// 15.4 ms against the round-1 default, now index 7: 8 chunks x 1 group, two CTAs per SM)
+#define BSDE_FUSED_VARIANTS(X) X(0, 7, 4, 384, 1) X(1, 7, 8, 512, 1) X(2, 5, 4, 384, 1) X(3, 3, 4, 640, 1) X(4, 7, 4, 256, 1) X(5, 5, 4, 256, 2) X(6, 7, 4, 256, 2) \
+  X(7, 7, 8, 256, 2)
 struct FusedVariant { int R, C, NT, MB; };
-#define BSDE_FUSED_VARIANTS(X) X(0, 7, 8, 256, 2) X(1, 7, 8, 512, 1) X(2, 5, 4, 384, 1) X(3, 3, 4, 640, 1) X(4, 7, 4, 256, 1) X(5, 5, 4, 256, 2)
+constexpr int kFusedAltVariant = 7;   // when index 0's one-tile-per-CTA launch is not co-resident
 static const FusedVariant kVariants[] = {
 #define BSDE_V_ROW(i, R, C, NT, MB) {R, C, NT, MB},
     BSDE_FUSED_VARIANTS(BSDE_V_ROW)
@@ -844,6 +851,7 @@ static const FusedVariant kVariants[] = {
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 int fused1d_num_variants() { return kNumVariants; }
+int fused1d_alt_variant() { return kFusedAltVariant; }
 
 // shared memory of the fused kernel for fz's buffer sizes: the spline scratch gets its own
 // region when it fits (fz.sep = 1), else it overlays the level buffers; 0 if neither fits

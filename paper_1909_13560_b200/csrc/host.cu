@@ -34,6 +34,7 @@ cudaError_t launch_generic_step(const StepArgs& s, const Grid& g, const Problem&
 bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int nsm, int variant, Fused1D& fz,
                       int& threads, int& blocks, size_t& smem);
 int fused1d_num_variants();
+int fused1d_alt_variant();
 cudaError_t launch_fused1d_steps(const StepArgs& s, const Grid& g, const Problem& pb, const Fused1D& fz, int n0,
                                  int nsteps, int ring_mode, int cur, double t0, double dt, double* v0, double* v1,
                                  unsigned* flags, const int* D, int DK, int threads, int blocks, size_t smem,
@@ -1320,6 +1321,14 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     c->geo.ok = fused1d_geometry(c->g, c->K, c->L, c->qspan, c->nsm, c->fused_variant, c->geo.fz,
                                  c->geo.threads, c->geo.blocks, c->geo.smem);
     set_distances(c, c->taps, c->K, c->geo);
+    if (cfg->kernel_variant == 0 && c->geo.ok && !c->geo.single) {
+      // the default's one-tile-per-CTA launch does not fit (long lines): the two-CTA-per-SM variant
+      c->fused_variant = fused1d_alt_variant();
+      c->geo = bsde_ctx::Geo{};
+      c->geo.ok = fused1d_geometry(c->g, c->K, c->L, c->qspan, c->nsm, c->fused_variant, c->geo.fz,
+                                   c->geo.threads, c->geo.blocks, c->geo.smem);
+      set_distances(c, c->taps, c->K, c->geo);
+    }
   }
   if (cfg->sde_id != BSDE_SDE_BROWNIAN || cfg->interp != BSDE_INTERP_SPLINE) { c->wc2 = 0; c->wca = 0; }
   // small 1-D grids (no fused geometry): the single-CTA whole-sweep kernel when its shared
