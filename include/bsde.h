@@ -209,8 +209,8 @@ bsde_status bsde_solve(bsde_ctx* ctx, bsde_result* res);
  * bsde_solve (first failing context).                                                 */
 bsde_status bsde_solve_batch(bsde_ctx* const* ctxs, int32_t n, bsde_result* res);
 
-/* bsde_solve_batch with an explicit CTA schedule.  mode 0: auto (= bsde_solve_batch: the
- * schedule of mode 3 when a plan fits, else round robin); 1: round robin (every CTA steps every
+/* bsde_solve_batch with an explicit CTA schedule.  mode 0: auto (= bsde_solve_batch: mode 2 or 3,
+ * whichever the calibrated cost model predicts faster, when a plan fits, else round robin); 1: round robin (every CTA steps every
  * problem on one tile of TP points); 2: paired problem-partitioned (the problems are paired by K
  * rank -- smallest with largest -- and each pair gets its own CTAs, which step the pair's two
  * problems round robin on a range of consecutive tiles whose spline is built in one pass; the

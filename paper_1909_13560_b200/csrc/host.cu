@@ -1633,12 +1633,15 @@ static void distances_for(const bsde_ctx* c, int tile, int* D, int& DK) {
 // tile-level: sum_{i in g} steps_i (ns (K_i a + b) + c); the plan minimises the slowest group's
 // time subject to sum gcta <= slots (binary search on that time).  Returns false if none fits.
 static bool plan_batch_groups(int n, const int* K, const int* steps, const int* group, int ngroup, int tiles, int slots,
-                              int nsmax, int* gcta, int* gns) {
-  const double a = 1.0, b = 1.0, c = 2.5;
+                              int nsmax, int* gcta, int* gns, double* t_pred = nullptr) {
+  // (r2) calibrated on the 12-warp default's per-round timeline (scripts/batch_timeline.py): a tile
+  // costs ~2.4 us per level + ~4.7 us fixed (epilogue, window start, its share of the pass-2
+  // spline), a round ~3.6 us more (flag waits)
+  const double a = 1.0, b = 2.0, c = 1.5;
   auto cost = [&](int gi, int s) {
     double t = 0.0;
     for (int i = 0; i < n; ++i)
-      if (group[i] == gi) t += (double)steps[i] * (s * (K[i] * a + b) + c + 0.25 * s);
+      if (group[i] == gi) t += (double)steps[i] * (s * (K[i] * a + b) + c);
     return t;
   };
   auto fit = [&](double T, int* nc, int* nsv) {
@@ -1664,6 +1667,11 @@ static bool plan_batch_groups(int n, const int* K, const int* steps, const int* 
     if (fit(mid, nc, nsv)) hi = mid; else lo = mid;
   }
   fit(hi, gcta, gns);
+  if (t_pred) {                      // the plan's predicted time: its slowest group
+    double m = 0.0;
+    for (int gi = 0; gi < ngroup; ++gi) m = std::max(m, cost(gi, gns[gi]));
+    *t_pred = m;
+  }
   return true;
 }
 
@@ -1724,15 +1732,32 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
     }
     int Kv[kMaxBatch], st[kMaxBatch];
     for (int i = 0; i < n; ++i) { Kv[i] = cs[i]->K; st[i] = cs[i]->level; }
-    if (mode == 2) {                                 // pairs by K rank: (1st, last), (2nd, 2nd last), ...
+    auto pair_groups = [&]() {                       // pairs by K rank: (1st, last), (2nd, 2nd last), ...
       int idx[kMaxBatch];
       for (int i = 0; i < n; ++i) idx[i] = i;
       std::stable_sort(idx, idx + n, [&](int x, int y) { return Kv[x] < Kv[y]; });
+      ngroup = 0;
       for (int r = 0; r < n; ++r) {
         const int pr = std::min(r, n - 1 - r);
         group[idx[r]] = pr;
         ngroup = std::max(ngroup, pr + 1);
       }
+    };
+    if (mode == 0 && n >= 4 && mb > 0) {
+      // auto: pairs when the cost model predicts them faster than one problem per group (the
+      // one-CTA-per-SM default leaves too few CTAs for six separate groups to balance)
+      int g1[kMaxBatch], c1[kMaxBatch], s1[kMaxBatch], c2[kMaxBatch], s2[kMaxBatch];
+      for (int i = 0; i < n; ++i) g1[i] = i;
+      double t1 = 0.0, t2 = 0.0;
+      const bool ok1 = plan_batch_groups(n, Kv, st, g1, n, c0->geo.blocks, c0->nsm * mb, nsmax, c1, s1, &t1);
+      pair_groups();
+      const bool ok2 = plan_batch_groups(n, Kv, st, group, ngroup, c0->geo.blocks, c0->nsm * mb, nsmax, c2, s2, &t2);
+      if (!ok2 || (ok1 && t1 <= t2)) {
+        for (int i = 0; i < n; ++i) group[i] = i;
+        ngroup = n;
+      }
+    } else if (mode == 2) {
+      pair_groups();
     } else if ((mode == 4 || mode == 5) && n > mode - 2) {   // the m = mode - 2 smallest K share a group
       const int m = mode - 2;
       int idx[kMaxBatch];
