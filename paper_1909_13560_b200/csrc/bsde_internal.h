@@ -12,6 +12,11 @@ constexpr int kMaxL = 64;
 constexpr int kPcrLevels = 5;       // PCR levels of the constant (1,4,1) system; coupling
                                     // after 5 levels: a5/b5 = 5.0e-19
 constexpr int kPcrHalo = (1 << kPcrLevels) - 1;   // 31
+// (r2) pass 2 of the fused 1-D kernel: the recursive filter on globally aligned segments of kP2Seg
+// rows, carries over kP2Q segments (|rho|^(7 x 6) = 1e-24); its window reaches at most kP2Halo
+// rows beyond the outputs
+constexpr int kP2Seg = 7, kP2Q = 6;
+constexpr int kP2Halo = kP2Seg * (kP2Q + 1);       // 49
 constexpr int kSmoothGL = 16;       // Gauss-Legendre nodes per axis for d >= 2 smoothing
 
 // One entry of a per-level, per-axis tap table (translation-invariant stencil,

@@ -322,11 +322,13 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   int hi = min(lo + TP, chi);
   const int li0 = (pg * 32 + lane) * R;              // first local point of this lane
   bool active = lo + li0 < hi;
-  const int H = kPcrHalo;
-  // coefficients this CTA owns (c indices k = storage - 1) and the PCR extent around them
+  // coefficients this CTA owns (c indices k = storage - 1) and the pass-2 window around them:
+  // the globally aligned segments [sa, sb] of kP2Seg rows, kP2Q beyond the outputs on each side
   const int k0 = clo == 0 ? -1 : clo, k1 = chi == P ? P + 1 : chi;
-  const int base = k0 - 4 - H;
-  const int Wa = (k1 - k0) + 8 + 2 * H;
+  auto fdiv = [](int x) { return x >= 0 ? x / kP2Seg : -((-x + kP2Seg - 1) / kP2Seg); };
+  const int sa = fdiv(k0) - kP2Q, sb = fdiv(k1 - 1) + kP2Q;
+  const int base = sa * kP2Seg;
+  const int Wa = (sb - sa + 1) * kP2Seg;
   // values window [va, vb] of both fields (clamped to the grid); the grid is long enough
   // (fused1d_geometry) that every folded index of the odd extension lands inside it
   const int va = max(base - 3, 0), vb = min(base + Wa + 2, P - 1);
@@ -730,48 +732,57 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       }
       __syncthreads();
       PHASE_STAMP(13);
-      // constant-coefficient PCR, both fields, two levels per pass where possible:
-      //   u = r - a1 (r[-s] + r[+s]),   v = u - a2 (u[-2s] + u[+2s])
-      const double* A = T0;
-      double* B = T1;
+      // (r2) the moment system of both fields by the recursive filter of spline_rf (kernels.cu),
+      // (1,4,1) = (-1/rho)(1 - rho z^-1)(1 - rho z): half of the CTA per field, segments of kP2Seg
+      // rows aligned to the global grid (segment g = rows [7g, 7g + 7)), each filtered from a zero
+      // start, the carries combined over the kP2Q previous / next segments (|rho|^42 = 1e-24).
+      // Every output is the same arithmetic on the same data in every CTA schedule (bitwise
+      // identical batch modes); m in place of the right-hand side
+      {
+        constexpr double rho = -0.26794919243112270;        // sqrt(3) - 2
+        constexpr int NH = NT / 2, S = kP2Seg;
+        const int f = tid >= NH, lt = tid - (f ? NH : 0);
+        const int nseg = Wa / S;
+        double* const X = T0 + f * WP;
+        double* const Ec = T1 + f * WP;                      // forward segment ends
+        double* const Fc = Ec + nseg;                        // backward segment starts
+        double rs = 1.0;
 #pragma unroll
-      for (int l = 0; l < kPcrLevels; l += 2) {
-        const int sh = 1 << l;
-        const double a1 = fz.alpha[l];
-        if (l + 1 < kPcrLevels) {
-          const double a2 = fz.alpha[l + 1];
-          for (int p = tid; p < Wa; p += NT) {
+        for (int j = 0; j < S; ++j) rs *= rho;
+        for (int sg = lt; sg < nseg; sg += NH) {
+          double* x = X + sg * S;
+          double u = 0.0;
 #pragma unroll
-            for (int f = 0; f < 2; ++f) {
-              const double* Af_ = A + f * WP;
-              auto at = [&](int q) { return (q >= 0 && q < Wa) ? Af_[q] : 0.0; };
-              const double c0 = Af_[p];
-              const double cm1 = at(p - sh), cp1 = at(p + sh), cm2 = at(p - 2 * sh), cp2 = at(p + 2 * sh);
-              const double cm3 = at(p - 3 * sh), cp3 = at(p + 3 * sh);
-              const double u0 = c0 - a1 * (cm1 + cp1);
-              const double um = cm2 - a1 * (cm3 + cm1);
-              const double up = cp2 - a1 * (cp1 + cp3);
-              B[f * WP + p] = u0 - a2 * (um + up);
-            }
-          }
-        } else {
-          for (int p = tid; p < Wa; p += NT) {
-#pragma unroll
-            for (int f = 0; f < 2; ++f) {
-              const double* Af_ = A + f * WP;
-              const double lft = p - sh >= 0 ? Af_[p - sh] : 0.0;
-              const double rgt = p + sh < Wa ? Af_[p + sh] : 0.0;
-              B[f * WP + p] = Af_[p] - a1 * (lft + rgt);
-            }
-          }
+          for (int j = 0; j < S; ++j) { u = fma(rho, u, x[j]); x[j] = u; }
+          Ec[sg] = u;
         }
         __syncthreads();
-        const double* t = A;
-        A = B;
-        B = const_cast<double*>(t);
+        for (int sg = lt; sg < nseg; sg += NH) {
+          double* x = X + sg * S;
+          double C = 0.0;                                    // u of the row before the segment
+          for (int q = max(0, sg - kP2Q); q < sg; ++q) C = fma(rs, C, Ec[q]);
+          double pw = rho;
+#pragma unroll
+          for (int j = 0; j < S; ++j) { x[j] = fma(pw, C, x[j]); pw *= rho; }
+          double v = 0.0;
+#pragma unroll
+          for (int j = S - 1; j >= 0; --j) { v = fma(rho, v, x[j]); x[j] = v; }
+          Fc[sg] = v;
+        }
+        __syncthreads();
+        for (int sg = lt; sg < nseg; sg += NH) {
+          double* x = X + sg * S;
+          double D = 0.0;                                    // v of the row after the segment
+          for (int q = min(nseg - 1, sg + kP2Q); q > sg; --q) D = fma(rs, D, Fc[q]);
+          double pw = rho;
+#pragma unroll
+          for (int j = S - 1; j >= 0; --j) { x[j] = -rho * fma(pw, D, x[j]); pw *= rho; }
+        }
+        __syncthreads();
       }
+      const double* A = T0;
       PHASE_STAMP(14);
-      const double ib = fz.inv_b;
+      const double ib = 1.0;                                 // m itself (the PCR form had a scale)
       double* ringn = const_cast<double*>(s.ring) + (int64_t)slot_out * s.slot_elems;
 #pragma unroll
       for (int f = 0; f < 2; ++f) {
@@ -877,10 +888,10 @@ bool fused1d_geometry(const Grid& g, int K, int L, int qspan_max, int nsm, int v
   fz.variant = variant;
   fz.TP = 32 * nwpg * v.R;
   // the pass-2 values window must contain every folded index of the odd extension
-  if (P < 2 * fz.TP + 2 * kPcrHalo + 256) return false;     // small grids: generic kernels
+  if (P < 2 * fz.TP + 2 * kP2Halo + 256) return false;     // small grids: generic kernels
   threads = v.NT;
   blocks = (int)((P + fz.TP - 1) / fz.TP);
-  fz.WP = ((fz.TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;      // PCR extent of the own tile (+ window slack)
+  fz.WP = ((fz.TP + 2 + 2 * kP2Halo + 8) + 1) & ~1;          // pass-2 window of the own tile (+ slack)
   int wm = fz.TP + qspan_max + 4 + 2;                        // level window
   const int wr = (3 * v.C * fz.TP + 3) / 4;                  // reduction (overlays buf0/buf1)
   if (wr > wm) wm = wr;

@@ -409,7 +409,7 @@ void set_distances(bsde_ctx* c, const std::vector<AxisTap>& t, int K, bsde_ctx::
     const int qa = -t[(size_t)(j - 1) * L].q, qb = t[(size_t)(j - 1) * L + L - 1].q;
     return std::max(qa, qb) + 4;
   };
-  geo.D[0] = (kPcrHalo + 6 + TP - 1) / TP;     // values halo of the pass-2 own-tile spline
+  geo.D[0] = (kP2Halo + 6 + TP - 1) / TP;     // values halo of the pass-2 own-tile spline
   int dk = geo.D[0];
   for (int j = 1; j <= K; ++j) {
     geo.D[j] = (reach(j) + TP - 1) / TP;
@@ -1615,7 +1615,7 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
 static void distances_for(const bsde_ctx* c, int tile, int* D, int& DK) {
   const int L = c->L;
   for (int j = 0; j <= kMaxK; ++j) D[j] = 0;
-  D[0] = (kPcrHalo + 6 + tile - 1) / tile;
+  D[0] = (kP2Halo + 6 + tile - 1) / tile;
   int dk = D[0];
   for (int j = 1; j <= c->K; ++j) {
     const int qa = -c->taps[(size_t)(j - 1) * L].q, qb = c->taps[(size_t)(j - 1) * L + L - 1].q;
@@ -1722,10 +1722,10 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
     const int TP = fz.TP, P = (int)c0->g.P[0];
     const int mb = fused1d_blocks_per_sm(fz.variant, fused1d_smem(fzp));
     // tiles per CTA: bounded by the pass-2 window (its folded end rows) and by shared memory
-    int nsmax = std::max(1, std::min(9, (P - 2 * kPcrHalo - 256) / (2 * TP)));
+    int nsmax = std::max(1, std::min(9, (P - 2 * kP2Halo - 256) / (2 * TP)));
     while (nsmax > 1) {
       Fused1D t = fz;
-      t.WP = ((nsmax * TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;
+      t.WP = ((nsmax * TP + 2 + 2 * kP2Halo + 8) + 1) & ~1;
       t.WS = 6 * t.WP + 16;
       if (fused1d_smem(t) > 0) break;
       --nsmax;
@@ -1783,7 +1783,7 @@ bsde_status bsde_solve_batch_mode(bsde_ctx* const* cs, int32_t n, int32_t mode, 
     if (planned) {
       int nsm_ = 1;
       for (int gi = 0; gi < ngroup; ++gi) { nsm_ = std::max(nsm_, gns[gi]); pblocks += gcta[gi]; }
-      fzp.WP = ((nsm_ * TP + 1 + 8 + 2 * kPcrHalo + 8) + 1) & ~1;   // PCR extent of a CTA's range
+      fzp.WP = ((nsm_ * TP + 2 + 2 * kP2Halo + 8) + 1) & ~1;   // pass-2 window of a CTA's range
       fzp.WS = 6 * fzp.WP + 16;
       smem_p = fused1d_smem(fzp);
       part = smem_p > 0 && pblocks <= c0->nsm * fused1d_blocks_per_sm(fzp.variant, smem_p) && pblocks <= kFlagCap;
