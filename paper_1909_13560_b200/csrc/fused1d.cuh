@@ -386,11 +386,13 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
 
   const bool multi = pl - pf > 1;
   for (int it = 0; it < it_end; ++it) {
-    if (pl > pf) {
+#ifdef BSDE_DEBUG
+    for (int ip = pf; ip < pl; ++ip) {   // round start of every problem of the group (debug timeline)
       const int it_stamp = it;
-      const StepArgs& s = PB[pf].s;
-      PHASE_STAMP(20);          // round start (debug timeline, scripts/batch_timeline.py)
+      const StepArgs& s = PB[ip].s;
+      PHASE_STAMP(20);
     }
+#endif
     // ================= pass 1: levels K..1, z and Picard of step it of every problem / tile
     // one relaxed read of every problem's flags + one acquire fence serve all problems' waits of
     // the pass; a CTA with a single problem waits with per-flag acquire loads instead (no fence)

@@ -2,7 +2,7 @@
 %globaltimer stamps (PHASE_STAMP in fused1d.cuh; build libbsde_b200_debug.so with
 `python scripts/phase_timeline.py --build`).  Per problem (its own CTAs in the partitioned
 schedule): round time, pass 1 (all tiles), the pass-2 flag wait and the pass-2 spline.
-usage: BSDE_PHASE_TIMING=1 python scripts/batch_timeline.py"""
+usage: BSDE_PHASE_TIMING=1 python scripts/batch_timeline.py [grid CTAs (pairs: half the sum)]"""
 import ctypes as C
 import os
 import sys
@@ -19,7 +19,7 @@ from paper_1909_13560_b200 import Solver, solve_batch, workloads as W  # noqa: E
 
 ss = [Solver(W.cfg2(K)) for K in range(1, 7)]
 res = solve_batch(ss)
-nb = sum(r.batch_ctas for r in res)
+nb = int(sys.argv[1]) if len(sys.argv) > 1 else sum(r.batch_ctas for r in res)   # the launch's grid
 print(f"batch {res[0].t_sweep_s * 1e3:.3f} ms, {nb} CTAs")
 for K, s, r in zip(range(1, 7), ss, res):
     n = 600 * 1100 * 32
