@@ -408,10 +408,11 @@ def tts_sweep(dev, oracle_budget_s=90.0):
 # against MEASURED_PEAKS.json's copy bandwidth.
 D23_KERNELS = {
     "cfg4": [("aff_rows", "ncu_aff_rows_cfg4_summary.json", "alu"),
-             ("spline_pass<4>", "ncu_spline_pass4_cfg4_summary.json", "hbm"),
-             ("spline_pass<1>", "ncu_spline_pass1_cfg4_summary.json", "hbm")],
+             ("spline_rf<strided>", "ncu_spline_rf_strided_cfg4_summary.json", "hbm"),
+             ("spline_rf<contiguous>", "ncu_spline_rf_contig_cfg4_summary.json", "hbm")],
     "cfg5": [("quad3d<DRV_DIFF,1>", "ncu_quad3d_dec_cfg5_summary.json", "alu"),
-             ("spline_pass<4>", "ncu_spline_pass4_cfg5_summary.json", "hbm")],
+             ("spline_rf<strided>", "ncu_spline_rf_strided_cfg5_summary.json", "hbm"),
+             ("spline_rf<contiguous>", "ncu_spline_rf_contig_cfg5_summary.json", "hbm")],
 }
 
 

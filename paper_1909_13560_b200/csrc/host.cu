@@ -1545,6 +1545,7 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
   const bool fused = c->d == 1 && (c->cfg.kernel_variant == 0 || c->cfg.kernel_variant >= 10) && c->geo.ok &&
                      c->geo.single && c->tap1_off >= 0;
   int64_t pexec = -1;
+  bool read_pexec = false;
   if (c->small_ok && c->level >= 1) {                  // latency path: one single-CTA launch
     const StepArgs s = persistent_args(c);
     const int ns = c->level;
@@ -1559,10 +1560,7 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
       c->cur ^= (ns & 1);
       c->level = 0;
       steps = ns;
-      unsigned long long v = 0;
-      if (cudaMemcpyAsync(&v, pexec_counter(c), sizeof v, cudaMemcpyDeviceToHost, c->stream) == cudaSuccess &&
-          cudaStreamSynchronize(c->stream) == cudaSuccess)
-        pexec = (int64_t)v;
+      read_pexec = true;                               // after the sweep's end event
     }
   } else if (fused && c->level >= 2) {
     const StepArgs s = persistent_args(c);
@@ -1579,17 +1577,20 @@ bsde_status bsde_solve(bsde_ctx* c, bsde_result* res) {
       c->cur ^= (ns & 1);
       c->level = 0;
       steps = ns;
-      unsigned long long v = 0;
-      if (cudaMemcpyAsync(&v, pexec_counter(c), sizeof v, cudaMemcpyDeviceToHost, c->stream) == cudaSuccess &&
-          cudaStreamSynchronize(c->stream) == cudaSuccess)
-        pexec = (int64_t)v;
+      read_pexec = true;
     }
   }
   while (st == BSDE_OK && c->level > 0) {
     if ((st = step_internal(c))) break;
     ++steps;
   }
-  cudaEventRecord(e1, c->stream);
+  cudaEventRecord(e1, c->stream);                      // the sweep's device time ends here
+  if (read_pexec) {                                    // executed Picard iterations (one read-back)
+    unsigned long long v = 0;
+    if (cudaMemcpyAsync(&v, pexec_counter(c), sizeof v, cudaMemcpyDeviceToHost, c->stream) == cudaSuccess &&
+        cudaStreamSynchronize(c->stream) == cudaSuccess)
+      pexec = (int64_t)v;
+  }
   if (st) { cudaEventDestroy(e0); cudaEventDestroy(e1); return st; }
   if ((st = check_bad(c))) { cudaEventDestroy(e0); cudaEventDestroy(e1); return st; }
   float ms = 0;

@@ -17,19 +17,20 @@ $NCU --set full --import-source on -k regex:quad1d_fused -c 1 -o /tmp/r2rep/batc
 summ batch ncu_quad1d_fused_batch_summary.json quad1d_fused
 ncu -i /tmp/r2rep/batch.ncu-rep --page source --csv --print-source cuda,sass > /tmp/r2rep/src.csv 2>/dev/null
 python scripts/ncu_lines.py /tmp/r2rep/src.csv 60 > $OUT/quad1d_fused_lines.txt 2>&1
-# (3) cfg 4 full size: one step's launches, aff_rows and the spline passes
+# (3) cfg 4 full size: one step's launches, aff_rows and the two spline passes
 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active \
     --csv --log-file $OUT/launches_cfg4_step.csv python scripts/step_probe.py cfg4 1 0 4096 > $OUT/p2.log 2>&1
 $NCU --set full -k regex:aff_rows -c 1 -o /tmp/r2rep/aff python scripts/step_probe.py cfg4 1 0 4096 > $OUT/p3.log 2>&1
 summ aff ncu_aff_rows_cfg4_summary.json aff_rows
-$NCU --set full -k regex:spline_pass -s 3 -c 2 -o /tmp/r2rep/spl4 python scripts/step_probe.py cfg4 1 0 4096 > $OUT/p4.log 2>&1
-summ spl4 ncu_spline_pass4_cfg4_summary.json "spline_pass<(4|16)>"
-summ spl4 ncu_spline_pass1_cfg4_summary.json "spline_pass<1>"
-# (4) cfg 5 full size (512^3): the decomposed path's quad3d and a strided / contiguous spline pass
+$NCU --set full -k regex:spline_rf -s 6 -c 2 -o /tmp/r2rep/spl4 python scripts/step_probe.py cfg4 1 0 4096 > $OUT/p4.log 2>&1
+summ spl4 ncu_spline_rf_strided_cfg4_summary.json "spline_rf<20, true>|spline_rf<20, 1>"
+summ spl4 ncu_spline_rf_contig_cfg4_summary.json "spline_rf<20, false>|spline_rf<20, 0>"
+# (4) cfg 5 full size (512^3): the decomposed path's quad3d and the spline passes
 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active \
     --csv --log-file $OUT/launches_cfg5_step.csv python scripts/step_probe.py cfg5 1 0 512 > $OUT/p5.log 2>&1
 $NCU --set full -k regex:quad3d -c 1 -o /tmp/r2rep/q3 python scripts/step_probe.py cfg5 1 0 512 > $OUT/p6.log 2>&1
 summ q3 ncu_quad3d_dec_cfg5_summary.json quad3d
-$NCU --set full -k regex:spline_pass -s 12 -c 3 -o /tmp/r2rep/spl5 python scripts/step_probe.py cfg5 1 0 512 > $OUT/p7.log 2>&1
-summ spl5 ncu_spline_pass4_cfg5_summary.json "spline_pass<(4|16)>"
+$NCU --set full -k regex:spline_rf -s 12 -c 3 -o /tmp/r2rep/spl5 python scripts/step_probe.py cfg5 1 0 512 > $OUT/p7.log 2>&1
+summ spl5 ncu_spline_rf_strided_cfg5_summary.json "spline_rf<20, true>|spline_rf<20, 1>"
+summ spl5 ncu_spline_rf_contig_cfg5_summary.json "spline_rf<20, false>|spline_rf<20, 0>"
 ls -la $OUT
