@@ -272,7 +272,22 @@ int sturm_count(int L, long double x) {   // eigenvalues < x
   return cnt;
 }
 
+void hermite_rule_compute(int L, double* a, double* w);
+// the rule of each L is computed once per process (the long-double bisection costs ~0.7 ms at
+// L = 32: a large share of a small problem's time to solution)
 void hermite_rule(int L, double* a, double* w) {
+  static std::mutex mu;
+  static std::vector<double> cache[kMaxL + 1];
+  std::lock_guard<std::mutex> lk(mu);
+  std::vector<double>& c = cache[L];
+  if (c.empty()) {
+    c.resize(2 * (size_t)L);
+    hermite_rule_compute(L, c.data(), c.data() + L);
+  }
+  std::copy(c.begin(), c.begin() + L, a);
+  std::copy(c.begin() + L, c.end(), w);
+}
+void hermite_rule_compute(int L, double* a, double* w) {
   const long double bound = sqrtl(2.0L * L) + 2.0L;
   for (int i = 0; i < L; ++i) {           // i-th smallest eigenvalue
     long double lo = -bound, hi = bound;
@@ -1354,7 +1369,7 @@ bsde_status bsde_setup(const bsde_config* cfg, void* d_workspace, size_t bytes, 
     }
     if (ce != cudaSuccess) { set_err(c, BSDE_ERR_CUDA, "taps: %s", cudaGetErrorString(ce)); return fail(BSDE_ERR_CUDA); }
   }
-  {
+  if (cfg->smoothing && c->d >= 2) {      // the Gauss-Legendre cell rule of the d >= 2 smoothing (R11)
     double gx[kSmoothGL], gw[kSmoothGL];
     legendre_rule(kSmoothGL, gx, gw);
     ce = upload_gl(gx, gw, c->stream);
