@@ -133,8 +133,17 @@ __global__ void __launch_bounds__(256, 1) quad1d_small(const __grid_constant__ S
     const double mP2_1 = V[2 * P - 3] - 2.0 * V[2 * P - 2] + V[2 * P - 1];
     for (int p = tid; p < WA; p += NT) {
       const int k = base + p;
-      T0[p] = rhs_fold_any(V, P, k, m1_0, mP2_0);
-      T0[WA + p] = rhs_fold_any(V + P, P, k, m1_1, mP2_1);
+      if (k >= 2 && k <= P - 3) {                           // interior row: no fold (no modulo)
+        double r0 = 6.0 * (V[k - 1] - 2.0 * V[k] + V[k + 1]);
+        double r1 = 6.0 * (V[P + k - 1] - 2.0 * V[P + k] + V[P + k + 1]);
+        if (k == 2) { r0 -= m1_0; r1 -= m1_1; }
+        if (k == P - 3) { r0 -= mP2_0; r1 -= mP2_1; }
+        T0[p] = r0;
+        T0[WA + p] = r1;
+      } else {
+        T0[p] = rhs_fold_any(V, P, k, m1_0, mP2_0);
+        T0[WA + p] = rhs_fold_any(V + P, P, k, m1_1, mP2_1);
+      }
     }
     __syncthreads();
     const double* A = T0;
@@ -185,12 +194,15 @@ __global__ void __launch_bounds__(256, 1) quad1d_small(const __grid_constant__ S
       double* c = line(slot, f);
       for (int k = -1 + tid; k <= P; k += NT) c[k + 1] = coef(k);
       c[P + 2] = 0.0;                                         // zero pad c_{P+1}
-      // virtual boundary entries: s(x_0) = (c_{-1} + 4 c_0 + c_1)/6 and s(x_{P-1})
-      const double v0 = (1.0 / 6.0) * coef(-1) + (2.0 / 3.0) * coef(0) + (1.0 / 6.0) * coef(1);
-      const double v1 = (1.0 / 6.0) * coef(P - 2) + (2.0 / 3.0) * coef(P - 1) + (1.0 / 6.0) * coef(P);
-      for (int i = tid; i < cpad; i += NT) {
-        c[-1 - i] = v0;
-        c[P + 3 + i] = v1;
+      // virtual boundary entries: s(x_0) = (c_{-1} + 4 c_0 + c_1)/6 and s(x_{P-1}) (only the
+      // threads that write them evaluate them)
+      if (tid < cpad) {
+        const double v0 = (1.0 / 6.0) * coef(-1) + (2.0 / 3.0) * coef(0) + (1.0 / 6.0) * coef(1);
+        const double v1 = (1.0 / 6.0) * coef(P - 2) + (2.0 / 3.0) * coef(P - 1) + (1.0 / 6.0) * coef(P);
+        for (int i = tid; i < cpad; i += NT) {
+          c[-1 - i] = v0;
+          c[P + 3 + i] = v1;
+        }
       }
     }
     __syncthreads();
