@@ -751,34 +751,60 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         double rs = 1.0;
 #pragma unroll
         for (int j = 0; j < S; ++j) rs *= rho;
+        // (the segment in registers: its loads issue together, the filter chains run at FMA latency)
         for (int sg = lt; sg < nseg; sg += NH) {
-          double* x = X + sg * S;
+          double* xp = X + sg * S;
+          double x[S];
+#pragma unroll
+          for (int j = 0; j < S; ++j) x[j] = xp[j];
           double u = 0.0;
 #pragma unroll
           for (int j = 0; j < S; ++j) { u = fma(rho, u, x[j]); x[j] = u; }
+#pragma unroll
+          for (int j = 0; j < S; ++j) xp[j] = x[j];
           Ec[sg] = u;
         }
         __syncthreads();
         for (int sg = lt; sg < nseg; sg += NH) {
-          double* x = X + sg * S;
+          double* xp = X + sg * S;
+          double e[kP2Q];                                     // the kP2Q previous segment ends
+#pragma unroll
+          for (int q = 0; q < kP2Q; ++q) e[q] = sg - kP2Q + q >= 0 ? Ec[sg - kP2Q + q] : 0.0;
+          double x[S];
+#pragma unroll
+          for (int j = 0; j < S; ++j) x[j] = xp[j];
           double C = 0.0;                                    // u of the row before the segment
-          for (int q = max(0, sg - kP2Q); q < sg; ++q) C = fma(rs, C, Ec[q]);
+#pragma unroll
+          for (int q = 0; q < kP2Q; ++q)
+            if (sg - kP2Q + q >= 0) C = fma(rs, C, e[q]);
           double pw = rho;
 #pragma unroll
           for (int j = 0; j < S; ++j) { x[j] = fma(pw, C, x[j]); pw *= rho; }
           double v = 0.0;
 #pragma unroll
           for (int j = S - 1; j >= 0; --j) { v = fma(rho, v, x[j]); x[j] = v; }
+#pragma unroll
+          for (int j = 0; j < S; ++j) xp[j] = x[j];
           Fc[sg] = v;
         }
         __syncthreads();
         for (int sg = lt; sg < nseg; sg += NH) {
-          double* x = X + sg * S;
+          double* xp = X + sg * S;
+          double e[kP2Q];                                     // the kP2Q next segment starts
+#pragma unroll
+          for (int q = 0; q < kP2Q; ++q) e[q] = sg + kP2Q - q < nseg ? Fc[sg + kP2Q - q] : 0.0;
+          double x[S];
+#pragma unroll
+          for (int j = 0; j < S; ++j) x[j] = xp[j];
           double D = 0.0;                                    // v of the row after the segment
-          for (int q = min(nseg - 1, sg + kP2Q); q > sg; --q) D = fma(rs, D, Fc[q]);
+#pragma unroll
+          for (int q = 0; q < kP2Q; ++q)
+            if (sg + kP2Q - q < nseg) D = fma(rs, D, e[q]);
           double pw = rho;
 #pragma unroll
           for (int j = S - 1; j >= 0; --j) { x[j] = -rho * fma(pw, D, x[j]); pw *= rho; }
+#pragma unroll
+          for (int j = 0; j < S; ++j) xp[j] = x[j];
         }
         __syncthreads();
       }

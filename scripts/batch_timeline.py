@@ -35,8 +35,10 @@ for K, s, r in zip(range(1, 7), ss, res):
     s2 = (a[:, :, 15] - a[:, :, 11]) / 1e3
     lv = (a[:, :, 8] - a[:, :, 1]) / 1e3                  # last unit: taps -> reduction (levels)
     ep = (a[:, :, 9] - a[:, :, 8]) / 1e3                  # last unit: reduction + epilogue
+    ph = [np.mean((a[:, :, i + 1] - a[:, :, i]) / 1e3) for i in (11, 12, 13, 14)]
     print(f"K={K}: {r.batch_ctas} CTAs x {r.batch_tiles} tiles: round {np.mean(rnd):6.2f} us | pass1 {np.mean(p1):6.2f} "
           f"(last tile: levels {np.mean(lv):5.2f}, epilogue {np.mean(ep):5.2f}) | p2 wait {np.mean(w2):5.2f} "
-          f"p2 spline {np.mean(s2):5.2f} | p90 round {np.percentile(rnd, 90):6.2f}")
+          f"p2 spline {np.mean(s2):5.2f} (values {ph[0]:4.2f} rhs {ph[1]:4.2f} filter {ph[2]:4.2f} coef {ph[3]:4.2f})"
+          f" | p90 round {np.percentile(rnd, 90):6.2f}")
 for s in ss:
     s.close()
