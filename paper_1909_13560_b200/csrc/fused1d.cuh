@@ -370,10 +370,11 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   uint32_t ph[4] = {0, 0, 0, 0};
   unsigned pexec = 0;         // Picard iterations this thread executed (current problem-step, or the launch)
   int prefetched = 0;         // windows of the current problem already in flight
-  // the warp that issues the next problem's copies during the epilogue: one without points
-  // (its lanes would otherwise idle through the Picard iterations), else warp 0.  It touches
-  // the flag marks only between CTA barriers that separate it from warp 0's waits.
-  const int iw = (TP <= NT - 32) ? NT / 32 - 1 : 0;
+  // the warp that issues the next problem's copies during the epilogue: the last warp, which has
+  // the fewest epilogue points (none when TP <= NT - 32; (r2) one per lane instead of two in the
+  // 12-warp default), not warp 0 with its flag waits.  It touches the flag marks only between CTA
+  // barriers that separate it from warp 0's waits.
+  const int iw = NT / 32 - 1;
   bool taps_in = false;       // its tap table is in flight
   // work units of a round: round-robin mode one per problem (the CTA's tile), part mode one per
   // tile of the CTA's range (its one problem)
