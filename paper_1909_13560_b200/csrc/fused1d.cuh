@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   __syncthreads();
   uint32_t ph[4] = {0, 0, 0, 0};
   unsigned pexec = 0;         // Picard iterations this thread executed (current problem-step, or the launch)
+  unsigned pexec1 = 0;        // ... for the CTA's second problem (pairs: no shared-memory atomics per unit)
   int prefetched = 0;         // windows of the current problem already in flight
   // the warp that issues the next problem's copies during the epilogue: the last warp, which has
   // the fewest epilogue points (none when TP <= NT - 32; (r2) one per lane instead of two in the
@@ -629,10 +630,15 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         if (!isfinite(y) || !isfinite(z)) atomicMin(s.bad, bad_key(pp.ring_mode ? pp.n0 - it : s.n, p));
       }
       PHASE_STAMP(18);
-      if (multi) {   // executed Picard iterations of this problem (the roofline's executed work);
-                     // a one-problem CTA keeps counting in pexec and flushes once at the end
-        const unsigned ex = __reduce_add_sync(0xffffffffu, pexec);
-        if (lane == 0 && ex) atomicAdd(pcnt + ip, (unsigned long long)ex);
+      if (multi && ip != pf) {   // executed Picard iterations per problem (the roofline's executed work):
+                                 // the CTA's first two problems count in registers and flush once at
+                                 // the end, any further one per unit
+        if (ip == pf + 1) {
+          pexec1 += pexec;
+        } else {
+          const unsigned ex = __reduce_add_sync(0xffffffffu, pexec);
+          if (lane == 0 && ex) atomicAdd(pcnt + ip, (unsigned long long)ex);
+        }
         pexec = 0;
       }
       // generic-proxy accesses of the level buffers before later bulk copies into them
@@ -869,9 +875,13 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
       if (tid == publisher) st_release(pp.ring_flag + bid, (unsigned)it + 1);
     }
   }
-  if (!multi && pl > pf) {
+  if (pl > pf) {
     const unsigned ex = __reduce_add_sync(0xffffffffu, pexec);
     if (lane == 0 && ex) atomicAdd(pcnt + pf, (unsigned long long)ex);
+    if (multi) {
+      const unsigned ex1 = __reduce_add_sync(0xffffffffu, pexec1);
+      if (lane == 0 && ex1) atomicAdd(pcnt + pf + 1, (unsigned long long)ex1);
+    }
   }
   __syncthreads();
   if (tid < bt.nprob && PB[tid].s.picard_exec != nullptr && pcnt[tid] != 0) atomicAdd(PB[tid].s.picard_exec, pcnt[tid]);

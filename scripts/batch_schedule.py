@@ -28,7 +28,7 @@ def run(Ks, mode, reps=2):
     return best, sched
 
 
-for mode in [3, 2, 3, 2]:
+for mode in [3, 2, 1, 0]:
     t, sc = run(range(1, 7), mode)
     print(f"batch K=1..6 mode {mode}: {t * 1e3:.3f} ms  schedule {sc}", flush=True)
 for K in (1, 6):
