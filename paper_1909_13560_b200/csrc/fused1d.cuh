@@ -50,6 +50,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
                  : "=r"(done) : "r"(smem_addr(bar)), "r"(phase) : "memory");
   } while (!done);
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -281,7 +284,8 @@ __device__ __forceinline__ int start_windows_ahead(const FusedProb& fp, const in
 template <int DRV, int R, int C, int NT, int MB>
 __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ FusedBatch bt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);   // 0/1: level buffers, 2: values tile, 3: taps
+  // 0/1: level buffers (full), 2: values tile, 3: taps, 4/5: level buffers released by every warp
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
   const Fused1D& fz = bt.fz;
   const Grid& g = bt.g;
   const int WM = fz.WMAX, WP = fz.WP;
@@ -346,6 +350,8 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
     mbar_init(&bar[3], 1);
+    mbar_init(&bar[4], NT / 32);
+    mbar_init(&bar[5], NT / 32);
     fence_mbar_init();
     for (int i = 0; i < 4 * kMaxBatch; ++i) marks[i] = 0;
   }
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
   }
   grid_dep_wait();            // previous kernel in the stream has completed
   __syncthreads();
-  uint32_t ph[4] = {0, 0, 0, 0};
+  uint32_t ph[6] = {0, 0, 0, 0, 0, 0};
   unsigned pexec = 0;         // Picard iterations this thread executed (current problem-step, or the launch)
   unsigned pexec1 = 0;        // ... for the CTA's second problem (pairs: no shared-memory atomics per unit)
   int prefetched = 0;         // windows of the current problem already in flight
@@ -535,9 +541,14 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         level(j, b);
         if (j <= 6) PHASE_STAMP(1 + j);
         if (j - 2 >= 1) {                     // refill this buffer with level j-2
+          // (r2) every warp releases the buffer on an mbarrier and goes on to level j-1; only warp 0
+          // waits for all of them before it issues the copy (no CTA barrier per level)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncthreads();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar[4 + b]);
           if (warp == 0) {
+            mbar_wait(&bar[4 + b], ph[4 + b]);
+            ph[4 + b] ^= 1u;
             if (j - 2 == 1) ring_wait(fp, marks + 4 * ip, it, 1, bid, nb);
             issue_window(fp, sp, it, j - 2, b ? buf1 : buf0, WM, &bar[b], lo, hi);
           }
