@@ -554,10 +554,13 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
           }
         }
       }
-      __syncthreads();
-
-      // reduction over node chunks (fixed order) and epilogue
-      double* red = buf0;
+      // reduction over node chunks (fixed order) and epilogue.  (r2) With a separate spline scratch
+      // large enough (idle in pass 1) the partial sums go there: the level buffers need no barrier
+      // of their own before the next unit's copies (one CTA barrier less per tile)
+      const bool red_sep = fz.sep && fz.WS >= 3 * C * TP;
+      if (!red_sep) __syncthreads();
+      else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      double* red = red_sep ? Fs : buf0;
       if (active) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -589,8 +592,10 @@ __global__ void __launch_bounds__(NT, MB) quad1d_fused(const __grid_constant__ F
         }
       }
       // the next problem's first windows stream in during this epilogue
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
+      if (!red_sep) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+      }
       PHASE_STAMP(16);
       {
         // the next unit of this round (next problem, or next tile of the range)
