@@ -828,6 +828,14 @@ def test_cfg5_shape_reduced_grid_16_steps():
 
 
 @gpu
+def test_cfg5_shape_full_solve_24():
+    """cfg 5 shape (3-D geometric basket, differential rates, K = 3, N = 64, L = 8, T = 0.5,
+    [-8,8]^3) on a 24^3 grid: the FULL backward solve (62 sweep steps) through the default
+    decomposed path against the oracle's full solve (final layer, Picard counts)."""
+    assert_parity(W.basket_3d(3, 64, 8, P=24))
+
+
+@gpu
 def test_cfg5_shape_first_step_sampled():
     """cfg 5 shape (3-D geometric basket, differential rates, K=3, N=64, L=8) at 128^3: the
     first backward step on the boundary bands and 5e3 random points (the full 512^3 oracle
