@@ -506,11 +506,6 @@ void pcr_constants(double* alpha, double* inv_b) {
   *inv_b = (double)(1.0L / bv);
 }
 
-// 16-line strided passes (r2 experiment, off: 128-byte rows measured slower -- cfg 5 strided pass 2.35 ms vs
-// 1.45 ms with 4 lines, profiles/round2/launches_cfg5_step.csv of the r2 capture); kept for ablation
-static bool g_wide_strided = false;
-void set_wide_strided(bool on) { g_wide_strided = on; }
-
 static cudaError_t run_pass(PassArgs pa, bool strided, cudaStream_t st, int64_t* launches) {
   pcr_constants(pa.alpha, &pa.inv_b);
   const int64_t n = pa.out_hi - pa.out_lo + 1;             // outputs per line (default c_{-1} .. c_P)
@@ -525,18 +520,10 @@ static cudaError_t run_pass(PassArgs pa, bool strided, cudaStream_t st, int64_t*
     ++*launches;
     return cudaGetLastError();
   }
-  // short contiguous lines (d = 3: 514 outputs) also go 4 lines per CTA, one tile per line:
-  // one 256-thread CTA per short line spends its time in barriers and launch overhead
+  // (PCR) short contiguous lines go 4 lines per CTA, one tile per line: one 256-thread CTA per
+  // short line spends its time in barriers and launch overhead
   const bool short_lines = !strided && n <= 1024 && pa.nb1 >= 4;
-  if (strided && pa.nb1 >= 64 && g_wide_strided) {
-    // (r2) 16 adjacent lines per CTA: 128-byte row segments (whole DRAM bursts instead of
-    // 32-byte sectors from rows a plane apart), tiles of ~160 outputs, 2 CTAs per SM
-    constexpr int LN = 16;
-    const int64_t nt = (n + 159) / 160;
-    pa.TS = (int)((n + nt - 1) / nt);
-    dim3 grid((unsigned)nt, (unsigned)((pa.nb1 + LN - 1) / LN), (unsigned)pa.nb0);
-    spline_pass<LN><<<grid, 256, spline_smem(pa.TS, LN), st>>>(pa);
-  } else if (strided || short_lines) {
+  if (strided || short_lines) {
     // 4 adjacent lines per CTA (32-byte coalesced row segments: 6 CTAs per SM instead of 3
     // with 8 lines; cfg 4 step 4.76 -> 4.66 ms), tiles of ~256 outputs (halo 27 %)
     constexpr int LN = 4;
@@ -946,7 +933,6 @@ cudaError_t launch_generic_step(const StepArgs& s, const Grid& g, const Problem&
 cudaError_t init_device_attributes() {
   const int lim = 200 * 1024;
   cudaError_t e = cudaFuncSetAttribute(spline_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_pass<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_rf<kRfS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(spline_rf<kRfS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
